@@ -1,0 +1,211 @@
+/*
+ * ras.h — C ABI of the B200-native (a)synchronous Restricted Additive Schwarz
+ * hot path (arxiv 2003.05361).  Plain C types only; no torch types.
+ *
+ * Citations: "P<n>" = PAPER.md line n (section / equation / algorithm named),
+ * "S<n>" = SPEC.md line n, "R<n>" = reading n in DESIGN.md.
+ *
+ * What the library computes (PAPER §2.1, P114-153; Alg. 1, P233-245):
+ *   the solution of A x = b (Eq. 1, P114-118), A sparse SPD, by RAS sweeps.
+ *   One sweep, for every subdomain p (all run in this library's CUDA kernels):
+ *     a1  restrict   x^k onto Omega_p u Gamma_p (owned / halo storage)
+ *     a2  residual   r~_p = b~_p - A_p x[Omega_p] - B_p x[Gamma_p]   (P292-297)
+ *     a3  local solve A_p d = r~_p  (Jacobi-PCG, IC(0)/ILU(0)-PCG, P309-323)
+ *     a4  restricted prolongation x^{k+1}[S_p] = x^k[S_p] + d[S_p]  (P147-153)
+ *     a5  exchange of the owner values other subdomains need       (P359-397)
+ *     a6  convergence: global ||b-Ax|| < tau ||b|| (sync, P344-346) or
+ *         Eq. 2 local flags + centralized / decentralized detection (async,
+ *         P326-357), verified after termination (P346-348).
+ *
+ * Conventions (all functions):
+ *   - Every input pointer is BORROWED for the duration of the call only; the
+ *     library copies what it needs (host -> device).  Host pointers unless
+ *     stated otherwise.
+ *   - Indices are 0-based.  FP64 values (R16: the paper states no precision).
+ *   - A context (ras_ctx) owns every device buffer it allocates and is NOT
+ *     thread-safe.  ras_setup / ras_solve are COLLECTIVE over the ranks of a
+ *     multi-GPU run: every rank calls them with identical tol, mode, overlap,
+ *     partition and options.
+ *   - Errors are returned as ras_status; ras_last_error() gives the message.
+ *     A NULL context or argument where one is required returns RAS_EINVAL.
+ */
+#ifndef RAS_H_
+#define RAS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAS_ABI_VERSION 1
+
+typedef struct ras_ctx ras_ctx; /* opaque; one per rank (process) */
+
+typedef enum {
+  RAS_OK = 0,
+  RAS_EINVAL = 1,   /* bad argument: dims, unsorted/out-of-range columns, owner out of range,
+                       empty subdomain, overlap < 0, tol <= 0, row window too small (S42) */
+  RAS_ENOTSPD = 2,  /* non-positive diagonal or IC(0)/ILU(0) pivot; message names the subdomain (S480) */
+  RAS_ENOCONV = 3,  /* max_iters reached; x_out holds the last iterate, stats valid (S78, S498) */
+  RAS_EVERIFY = 4,  /* async terminated but ||b-Ax|| >= tau ||b|| after max_resumes (S507, R20) */
+  RAS_ECUDA = 5,    /* CUDA runtime error (text passed through) */
+  RAS_ENCCL = 6,    /* NCCL error (text passed through) */
+  RAS_ENOMEM = 7,   /* host or device allocation failed */
+  RAS_ESTATE = 8    /* call not valid in the current state (e.g. no GPU, NCCL missing for world>1) */
+} ras_status;
+
+typedef enum { RAS_SYNC = 0, RAS_ASYNC = 1 } ras_mode;
+
+typedef enum {
+  RAS_LS_JACOBI_PCG = 0, /* PCG, M = diag(A_p), fixed m iterations (P313-315; R6, R8) */
+  RAS_LS_IC0_PCG = 1,    /* PCG, M = L L^T, IC(0) of A_p, level-scheduled trisolves (P317-323; R9) */
+  RAS_LS_ILU0_PCG = 2,   /* PCG, M = L U, ILU(0) of A_p (R10) */
+  RAS_LS_EXACT_PCG = 3   /* Jacobi-PCG to ||r|| <= 1e-14 ||r~||, <= 10|Omega_p| iterations:
+                            the GPU stand-in for the paper's direct local solve (P317-318; R6) */
+} ras_local_solver;
+
+typedef enum { RAS_DET_CENTRAL = 0, RAS_DET_DECENTRAL = 1 } ras_detector;
+
+/* Sparse matrix A in CSR, possibly a window of rows [row_begin, row_begin+nrows)
+ * of the global n x n matrix (so a rank need not hold all of A).  row_ptr is
+ * relative: row_ptr[0] == 0, row_ptr[nrows] == nnz of the window.  Columns are
+ * global, strictly increasing within a row, in [0, n).  A rank's window must
+ * contain every row of its subdomains' Omega_p (else RAS_EINVAL). */
+typedef struct {
+  int64_t n;
+  int64_t row_begin;
+  int64_t nrows;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const double* val;
+} ras_csr;
+
+/* Non-overlapping partition (PAPER §3.2.1, P247-290): owner[g] in [0, P) is the
+ * subdomain owning global row g (len n, full on every rank).  sub_to_rank[p]
+ * maps subdomains to ranks (GPUs); NULL = contiguous blocks
+ * (rank r gets p in [r*P/world, (r+1)*P/world)). */
+typedef struct {
+  int32_t num_subdomains;
+  const int32_t* owner;
+  const int32_t* sub_to_rank;
+} ras_partition;
+
+typedef struct {
+  ras_local_solver local_solver; /* default RAS_LS_JACOBI_PCG */
+  int32_t inner_iters;           /* m (default 20); ignored by EXACT */
+  double inner_tol;              /* eta: stop the local PCG when ||r|| <= eta ||r~|| (0 = fixed m) */
+  ras_detector detector;         /* async termination detection (default DECENTRAL, P481-484) */
+  int32_t local_crit_owned_only; /* Eq. 2 over owned rows only (R12); default 0 = paper's Eq. 2 */
+  int32_t max_resumes;           /* async: resumes after failed verification (R20), default 3 */
+  int32_t use_graphs;            /* capture the sync sweep in a CUDA graph (default 1) */
+  int32_t poll_interval;         /* sweeps between host polls of the device stop flag (default 4) */
+  double async_timeout_s;        /* async wall-clock watchdog, default 1800 s */
+  int32_t scripted_flags;        /* test hook: Eq. 2 flags come from ras_set_scripted_flags */
+  int32_t reserved_i[7];
+  double reserved_d[4];
+} ras_options;
+
+/* Multi-GPU plumbing.  NULL = single GPU (current device, default stream). */
+typedef struct {
+  int32_t rank, world;          /* this process's rank and the number of ranks (GPUs) */
+  int32_t device;               /* CUDA device ordinal this rank drives */
+  const void* nccl_unique_id;   /* 128 bytes from ras_nccl_unique_id() on rank 0, broadcast by
+                                   the caller (torch.distributed); NULL when world == 1 */
+  void* cuda_stream;            /* cudaStream_t for sync-mode work; NULL = a library stream */
+  /* optional device allocator hooks (e.g. torch's caching allocator); NULL = cudaMalloc */
+  void* (*dev_alloc)(size_t bytes, void* user);
+  void (*dev_free)(void* ptr, void* user);
+  void* alloc_user;
+} ras_comm;
+
+typedef struct {
+  int32_t mode, converged, verified, resumes;
+  double time_to_solution_s;   /* start of ras_solve -> stop observed (R26; P474-480) */
+  double setup_s;              /* ras_setup wall time (untimed by the paper, P229-231) */
+  double verify_s;             /* gather + true residual after async stop */
+  int64_t sweeps;              /* sync: global sweeps performed; async: max per-subdomain updates */
+  int64_t updates_min, updates_median, updates_max; /* per-subdomain local solves (Fig. 7c, P727-735) */
+  int64_t inner_iters_total;   /* total local PCG iterations over all subdomains on this rank */
+  double final_rel_residual;   /* true ||b - A x|| / ||b|| of the returned iterate */
+  double t_residual, t_local_solve, t_prolong, t_exchange, t_convcheck; /* per-phase seconds (Figs. 3a-7a) */
+  double model_bytes;          /* algorithmic HBM bytes moved by this rank's kernels */
+  int32_t num_subdomains, world;
+  int32_t local_subdomains, reserved0;
+  int64_t rows_local;          /* sum |Omega_p| on this rank */
+  int64_t halo_values;         /* halo slots on this rank (values received per exchange) */
+  int64_t kernel_launches;     /* kernels launched by the last ras_solve on this rank */
+  int64_t fresh_halo_reads;    /* async: halo version changes observed */
+} ras_stats_t;
+
+/* Fill *opt with defaults. */
+ras_status ras_options_default(ras_options* opt);
+
+/* Alg. 1 `initialization_and_setup` (P233-237): validate; partition bookkeeping;
+ * gamma-hop overlap Omega_p and ghosts Gamma_p (P133-142, R1); restrict /
+ * prolong / pack index maps; batched local matrices on the device; optional
+ * IC(0)/ILU(0) factors and level sets; NCCL communicator and peer windows.
+ * b: RHS rows for the same window as A (len A->nrows).  overlap = gamma >= 0.
+ * On failure *out is NULL and ras_last_error(NULL) holds the message. */
+ras_status ras_setup(ras_ctx** out, const ras_csr* A, const double* b, const ras_partition* part,
+                     int32_t overlap, const ras_options* opt, const ras_comm* comm);
+
+/* Replace the right-hand side (same window as at setup). */
+ras_status ras_set_rhs(ras_ctx* ctx, const double* b);
+
+/* Alg. 1 `solve` (P238-244).  tol = tau > 0.  max_iters: sync = sweeps,
+ * async = per-subdomain updates (R21).  x0: host, len n (NULL = 0, R15).
+ * x_out: host, len n, the gathered solution (owner values, P242) on every
+ * rank, or NULL.  Returns RAS_OK, RAS_ENOCONV (x_out = x^{max_iters}; the
+ * parity hook: max_iters = k returns the k-th sync iterate), RAS_EVERIFY, or
+ * an error.  Sync mode stops at the first k with ||b - A x^k|| < tau ||b||
+ * and returns x^k (R13). */
+ras_status ras_solve(ras_ctx* ctx, double tol, int64_t max_iters, ras_mode mode, const double* x0,
+                     double* x_out);
+
+/* Device-resident variant for benchmarks: x0 / x_out are DEVICE pointers to this
+ * rank's owned values (len ras_stats_t-independent: ras_owned_count()), ordered
+ * as ras_owned_gids(); either may be NULL. */
+ras_status ras_solve_device(ras_ctx* ctx, double tol, int64_t max_iters, ras_mode mode, const double* x0_owned_dev,
+                            double* x_owned_dev);
+
+int64_t ras_owned_count(const ras_ctx* ctx);
+/* Global ids of this rank's owned values in storage order (len ras_owned_count). */
+ras_status ras_owned_gids(const ras_ctx* ctx, int64_t* gids_out);
+
+ras_status ras_stats(const ras_ctx* ctx, ras_stats_t* out);
+
+/* Per-subdomain update counts of the last solve (len = local subdomains). */
+ras_status ras_update_counts(const ras_ctx* ctx, int64_t* counts_out);
+
+void ras_free(ras_ctx* ctx);
+
+/* Message of the last failure on ctx; ctx == NULL -> thread-local message of the
+ * last failed ras_setup / ras_partition_regular / plan call.  Never NULL. */
+const char* ras_last_error(const ras_ctx* ctx);
+
+/* Regular block partition (regular1d / regular2d / 3D blocks, P277-286; R23):
+ * nx*ny*nz grid, point (x,y,z) -> (z*ny+y)*nx+x; px*py*pz blocks whose sizes
+ * differ by <= 1 per axis, earlier blocks larger; id = (bz*py+by)*px+bx.
+ * owner_out: len nx*ny*nz.  RAS_EINVAL if a block would be empty. */
+ras_status ras_partition_regular(int32_t nx, int32_t ny, int32_t nz, int32_t px, int32_t py, int32_t pz,
+                                 int32_t* owner_out);
+
+/* NCCL unique id (128 bytes) for multi-GPU setup; call on rank 0 only. */
+ras_status ras_nccl_unique_id(void* out128);
+
+/* Test hook (options.scripted_flags = 1): the Eq. 2 flag of local subdomain i in
+ * sweep k is flags[k * nlocal + i] (k >= nsweeps -> last row). */
+ras_status ras_set_scripted_flags(ras_ctx* ctx, const uint8_t* flags, int64_t nsweeps);
+
+/* Per-subdomain stop sweep of the last scripted run (len local subdomains). */
+ras_status ras_detector_stops(const ras_ctx* ctx, int64_t* stop_out);
+
+int32_t ras_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAS_H_ */

@@ -1,0 +1,109 @@
+// ras_ctx: one per rank.  Owns the plan, every device buffer, streams, NCCL.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan_internal.h"
+#include "ras.h"
+
+namespace ras {
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct AsyncRt;  // async-mode runtime (async.cu)
+
+struct ModelBytes {  // algorithmic bytes per launch over the whole row space
+  double residual, spmv_dot, update_dot, pupdate, prolong, pack;
+};
+
+}  // namespace ras
+
+struct ras_ctx {
+  ras_plan* plan = nullptr;
+  ras_options opt{};
+  int32_t rank = 0, world = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t nccl = nullptr;
+  void* (*dev_alloc)(size_t, void*) = nullptr;
+  void (*dev_free)(void*, void*) = nullptr;
+  void* alloc_user = nullptr;
+  std::vector<ras::DevBuf> bufs;
+  std::string err;
+  double setup_s = 0.0;
+  double b2_global = 0.0;  // ||b||^2
+
+  // ---- device arrays ----
+  int64_t rows_pad = 0, n_own = 0, n_halo = 0, ntiles = 0;
+  int32_t nl = 0;  // local subdomains
+  double* d_b = nullptr;
+  double* d_diag = nullptr;
+  int32_t* d_own_slot = nullptr;
+  ras::Sell R{}, L{};
+  ras::Tiles T{};
+  double* d_x = nullptr;  // storage [owned | halo]
+  double* d_r = nullptr;
+  double* d_p = nullptr;
+  double* d_q = nullptr;
+  double* d_d = nullptr;
+  ras::Scal S{};
+  int64_t* d_inner_total = nullptr;
+  // sync control
+  int32_t* d_stop = nullptr;
+  ras::SyncState* d_sync = nullptr;
+  double* d_r2_local = nullptr;
+  double* d_r2_global = nullptr;
+  int32_t* d_nactive = nullptr;
+  int32_t* h_stop = nullptr;       // mapped pinned
+  int32_t* h_stop_dev = nullptr;   // device alias of h_stop
+  int32_t* h_nactive = nullptr;    // pinned
+  // exchange (sync, NCCL)
+  int64_t n_send = 0;
+  int32_t* d_send_slot = nullptr;
+  double* d_sendbuf = nullptr;
+  std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;  // per peer
+
+  // async runtime
+  ras::AsyncRt* async = nullptr;
+
+  // stats of the last solve
+  ras_stats_t st{};
+  std::vector<int64_t> updates;
+  std::vector<int64_t> det_stops;
+  ras::ModelBytes mb{};
+  int64_t launches = 0;
+
+  std::vector<uint8_t> scripted;
+  int64_t scripted_sweeps = 0;
+};
+
+namespace ras {
+ras_status set_err(ras_ctx* c, ras_status s, const std::string& m);
+ras_status cuda_err(ras_ctx* c, cudaError_t e, const char* what);
+void* dalloc(ras_ctx* c, size_t bytes);
+ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters);
+ras_status async_setup(ras_ctx* c);
+void async_free(ras_ctx* c);
+}  // namespace ras
+
+#define RAS_CUDA(c, expr)                                         \
+  do {                                                            \
+    cudaError_t e_ = (expr);                                      \
+    if (e_ != cudaSuccess) return ras::cuda_err((c), e_, #expr);  \
+  } while (0)
+
+#define RAS_NCCL(c, expr)                                                                        \
+  do {                                                                                           \
+    ncclResult_t r_ = (expr);                                                                    \
+    if (r_ != ncclSuccess)                                                                       \
+      return ras::set_err((c), RAS_ENCCL, std::string(#expr ": ") + ncclGetErrorString(r_));     \
+  } while (0)

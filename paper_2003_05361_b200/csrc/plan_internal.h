@@ -1,0 +1,84 @@
+// Internal definition of ras_plan (host-side setup, scope row a0).  Pure C++.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ras.h"
+#include "ras_plan.h"
+
+namespace ras {
+
+// thread-local message of the last failure outside a context
+void set_tls_error(const std::string& msg);
+const std::string& tls_error();
+
+struct Fail {
+  ras_status st;
+  std::string msg;
+};
+
+struct SubPlan {
+  int32_t p = -1;                // global subdomain id
+  std::vector<int64_t> omega;    // Omega_p ascending
+  std::vector<uint8_t> owned;    // per omega row
+  std::vector<int64_t> ghosts;   // Gamma_p ascending
+  int64_t row_off = 0, nrows = 0, nrows_pad = 0;  // row space
+  int64_t own_off = 0, nown = 0;                   // owned slots
+  int64_t tile_begin = 0, ntiles = 0;
+  double b2 = 0.0;        // ||b~_p||^2 over Omega_p (Eq. 2)
+  double b2_owned = 0.0;  // ||b||^2 over S_p
+};
+
+}  // namespace ras
+
+struct ras_plan {
+  int64_t n = 0;
+  int32_t P = 0, rank = 0, world = 1, gamma = 0;
+  int32_t tile_rows = 256;
+  std::vector<int32_t> sub_to_rank;
+  std::vector<ras::SubPlan> subs;  // local subdomains, ascending global id
+  int64_t n_own = 0, n_halo = 0;
+  std::vector<int64_t> own_gid, halo_gid;
+  std::vector<int64_t> halo_off;   // world + 1 (relative to the first halo slot)
+  std::vector<std::vector<int64_t>> send_gid;
+  std::vector<std::vector<int32_t>> send_slot;
+  std::vector<int64_t> send_remote_off;
+  std::vector<uint8_t> send_set;
+  bool finalized = false;
+
+  // borrowed input window (valid from ras_plan_build until ras_plan_finalize)
+  int64_t row_begin = 0, nrows_win = 0;
+  const int64_t* A_ptr = nullptr;
+  const int32_t* A_col = nullptr;
+  const double* A_val = nullptr;
+  const double* b_win = nullptr;
+  std::vector<int32_t> slot;  // global id -> storage slot (-1 = not stored on this rank)
+
+  // ---- row space (after finalize) ----
+  int64_t rows_pad = 0, rows_local = 0;
+  std::vector<double> b_loc, diag;
+  std::vector<int32_t> own_slot;   // prolong map (-1 = overlap row / padding)
+  std::vector<int32_t> self_slot;  // restrict map of the row's own value
+  std::vector<int32_t> slice_sub;  // local subdomain of every 32-row slice
+  // SELL-32 residual matrix [A_p | B_p] with storage-slot columns (full rows)
+  std::vector<int64_t> R_sptr;
+  std::vector<int32_t> R_col;
+  std::vector<double> R_val;
+  // SELL-32 local matrix A_p, off-diagonal part, row-space columns
+  std::vector<int64_t> L_sptr;
+  std::vector<int32_t> L_col;
+  std::vector<double> L_val;
+  // CSR of A_p (subdomain-relative columns, incl. diagonal) for factorizations
+  std::vector<int64_t> Ap_ptr;   // rows_pad + 1 (padding rows: diagonal 1)
+  std::vector<int32_t> Ap_col;   // subdomain-relative
+  std::vector<double> Ap_val;
+  int64_t nnz_residual = 0, nnz_local = 0;
+  // tiles: CTA work units, never straddle subdomains
+  std::vector<int32_t> tile_sub;
+  std::vector<int64_t> tile_row0;
+  std::vector<int32_t> tile_nrows;
+  double b2_global_local = 0.0;  // sum over this rank's owned rows of b^2
+
+};

@@ -1,0 +1,696 @@
+// C ABI: ras_setup / ras_solve (sync mode) / ras_stats / ras_free.
+// PAPER Alg. 1 (P233-245): initialization_and_setup, then the solve loop
+// {local solve; exchange; update boundary; check convergence}; gather.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "kernels.cuh"
+#include "plan_internal.h"
+#include "ras.h"
+#include "ras_plan.h"
+
+namespace ras {
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+ras_status set_err(ras_ctx* c, ras_status s, const std::string& m) {
+  if (c)
+    c->err = m;
+  else
+    set_tls_error(m);
+  return s;
+}
+
+ras_status cuda_err(ras_ctx* c, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return set_err(c, e == cudaErrorMemoryAllocation ? RAS_ENOMEM : RAS_ECUDA, m);
+}
+
+void* dalloc(ras_ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  bytes = (bytes + 255) / 256 * 256;
+  void* p = nullptr;
+  if (c->dev_alloc) {
+    p = c->dev_alloc(bytes, c->alloc_user);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    p = nullptr;
+  }
+  if (p) c->bufs.push_back(DevBuf{p, bytes});
+  return p;
+}
+
+template <class T>
+static ras_status upload(ras_ctx* c, T** dst, const std::vector<T>& src, size_t min_elems = 0) {
+  size_t n = std::max(src.size(), min_elems);
+  *dst = (T*)dalloc(c, n * sizeof(T));
+  if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
+  if (!src.empty()) RAS_CUDA(c, cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return RAS_OK;
+}
+
+template <class T>
+static ras_status zalloc(ras_ctx* c, T** dst, size_t n) {
+  *dst = (T*)dalloc(c, n * sizeof(T));
+  if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
+  RAS_CUDA(c, cudaMemset(*dst, 0, std::max<size_t>(n, 1) * sizeof(T)));
+  return RAS_OK;
+}
+
+#define TRY(x)                       \
+  do {                               \
+    ras_status s_ = (x);             \
+    if (s_ != RAS_OK) return s_;     \
+  } while (0)
+
+// Multi-rank exchange of halo requests over NCCL (setup only): every rank
+// learns which of its owned values each peer needs, in the peer's halo order.
+static ras_status exchange_requests(ras_ctx* c) {
+  ras_plan* pl = c->plan;
+  const int W = c->world, me = c->rank;
+  std::vector<int64_t> my_counts(W);
+  for (int r = 0; r < W; ++r) my_counts[r] = pl->halo_off[r + 1] - pl->halo_off[r];
+  int64_t *d_counts = nullptr, *d_all = nullptr;
+  TRY(upload(c, &d_counts, my_counts));
+  TRY(zalloc(c, &d_all, (size_t)W * W));
+  RAS_NCCL(c, ncclAllGather(d_counts, d_all, W, ncclInt64, c->nccl, c->stream));
+  std::vector<int64_t> all((size_t)W * W);
+  RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  // all[q*W + r] = how many values rank q needs from rank r
+  int64_t tot_out = 0, tot_in = 0;
+  for (int q = 0; q < W; ++q) tot_in += all[(size_t)q * W + me];
+  tot_out = pl->n_halo;
+  int64_t *d_req = nullptr, *d_inc = nullptr;
+  TRY(upload(c, &d_req, pl->halo_gid, 1));
+  TRY(zalloc(c, &d_inc, std::max<int64_t>(tot_in, 1)));
+  std::vector<int64_t> inc_off(W + 1, 0);
+  for (int q = 0; q < W; ++q) inc_off[q + 1] = inc_off[q] + all[(size_t)q * W + me];
+  RAS_NCCL(c, ncclGroupStart());
+  for (int r = 0; r < W; ++r) {
+    if (r == me) continue;
+    const int64_t cnt = pl->halo_off[r + 1] - pl->halo_off[r];
+    if (cnt) RAS_NCCL(c, ncclSend(d_req + pl->halo_off[r], cnt, ncclInt64, r, c->nccl, c->stream));
+    const int64_t inc = all[(size_t)r * W + me];
+    if (inc) RAS_NCCL(c, ncclRecv(d_inc + inc_off[r], inc, ncclInt64, r, c->nccl, c->stream));
+  }
+  RAS_NCCL(c, ncclGroupEnd());
+  std::vector<int64_t> inc(std::max<int64_t>(tot_in, 1));
+  RAS_CUDA(c, cudaMemcpyAsync(inc.data(), d_inc, inc.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  (void)tot_out;
+  for (int q = 0; q < W; ++q) {
+    if (q == me) continue;
+    // where my segment lands in q's halo: sum of what q needs from ranks < me
+    int64_t roff = 0;
+    for (int r = 0; r < me; ++r) roff += all[(size_t)q * W + r];
+    const int64_t cnt = all[(size_t)q * W + me];
+    ras_status s = ras_plan_set_send(pl, q, cnt, inc.data() + inc_off[q], roff);
+    if (s != RAS_OK) return set_err(c, s, tls_error());
+  }
+  return RAS_OK;
+}
+
+static void compute_model_bytes(ras_ctx* c) {
+  const ras_plan* pl = c->plan;
+  const double rows = (double)pl->rows_local;
+  int64_t owned = pl->n_own;
+  const double nnz_off = (double)(pl->nnz_local - pl->rows_local);
+  // compulsory bytes, real (unpadded) rows and entries
+  c->mb.residual = rows * (8 /*b*/ + 8 /*diag*/ + 4 /*own_slot*/ + 8 /*x*/ + 8 /*r*/ + 8 /*p*/) +
+                   (double)pl->nnz_residual * 12.0;
+  c->mb.spmv_dot = rows * (8 /*p*/ + 8 /*diag*/ + 8 /*q*/) + nnz_off * 12.0;
+  c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + 8 /*diag*/ + 16 /*r*/ + 16 /*d*/);
+  c->mb.pupdate = rows * (8 /*diag*/ + 8 /*r*/ + 16 /*p*/);
+  c->mb.prolong = rows * 4.0 + (double)owned * (8 /*d*/ + 16 /*x*/);
+  c->mb.pack = (double)c->n_send * (4 + 8 + 8);
+}
+
+static ras_status upload_plan(ras_ctx* c) {
+  ras_plan* pl = c->plan;
+  c->rows_pad = pl->rows_pad;
+  c->n_own = pl->n_own;
+  c->n_halo = pl->n_halo;
+  c->ntiles = (int64_t)pl->tile_sub.size();
+  c->nl = (int32_t)pl->subs.size();
+  TRY(upload(c, &c->d_b, pl->b_loc));
+  TRY(upload(c, &c->d_diag, pl->diag));
+  TRY(upload(c, &c->d_own_slot, pl->own_slot));
+  int64_t* sp;
+  int32_t* ci;
+  double* va;
+  TRY(upload(c, &sp, pl->R_sptr));
+  TRY(upload(c, &ci, pl->R_col, 1));
+  TRY(upload(c, &va, pl->R_val, 1));
+  c->R = Sell{sp, ci, va};
+  TRY(upload(c, &sp, pl->L_sptr));
+  TRY(upload(c, &ci, pl->L_col, 1));
+  TRY(upload(c, &va, pl->L_val, 1));
+  c->L = Sell{sp, ci, va};
+  std::vector<int64_t> stb(c->nl);
+  std::vector<int32_t> snt(c->nl);
+  for (int i = 0; i < c->nl; ++i) {
+    stb[i] = pl->subs[i].tile_begin;
+    snt[i] = (int32_t)pl->subs[i].ntiles;
+  }
+  int32_t* ts;
+  int64_t* tr;
+  int32_t* tn;
+  int64_t* sb;
+  int32_t* sn;
+  TRY(upload(c, &ts, pl->tile_sub));
+  TRY(upload(c, &tr, pl->tile_row0));
+  TRY(upload(c, &tn, pl->tile_nrows));
+  TRY(upload(c, &sb, stb));
+  TRY(upload(c, &sn, snt));
+  c->T = Tiles{ts, tr, tn, sb, sn};
+  TRY(zalloc(c, &c->d_x, (size_t)(c->n_own + c->n_halo)));
+  TRY(zalloc(c, &c->d_r, (size_t)c->rows_pad));
+  TRY(zalloc(c, &c->d_p, (size_t)c->rows_pad));
+  TRY(zalloc(c, &c->d_q, (size_t)c->rows_pad));
+  TRY(zalloc(c, &c->d_d, (size_t)c->rows_pad));
+  const int nl = c->nl;
+  TRY(zalloc(c, &c->S.rt2, nl));
+  TRY(zalloc(c, &c->S.rho, nl));
+  TRY(zalloc(c, &c->S.own2, nl));
+  TRY(zalloc(c, &c->S.alpha, nl));
+  TRY(zalloc(c, &c->S.beta, nl));
+  TRY(zalloc(c, &c->S.rr, nl));
+  TRY(zalloc(c, &c->S.active, nl));
+  TRY(zalloc(c, &c->S.its, nl));
+  TRY(zalloc(c, &c->S.ticket, nl));
+  TRY(zalloc(c, &c->S.inner_total, nl));
+  TRY(zalloc(c, &c->S.partials, (size_t)c->ntiles * kNP));
+  TRY(zalloc(c, &c->d_stop, 1));
+  TRY(zalloc(c, &c->d_sync, 1));
+  TRY(zalloc(c, &c->d_r2_local, 1));
+  TRY(zalloc(c, &c->d_r2_global, 1));
+  TRY(zalloc(c, &c->d_nactive, 1));
+  RAS_CUDA(c, cudaHostAlloc((void**)&c->h_stop, 32 * sizeof(int32_t), cudaHostAllocMapped));
+  RAS_CUDA(c, cudaHostGetDevicePointer((void**)&c->h_stop_dev, c->h_stop, 0));
+  RAS_CUDA(c, cudaHostAlloc((void**)&c->h_nactive, 64, cudaHostAllocDefault));
+  // exchange lists (sync): concatenated per peer
+  c->send_off.assign(c->world + 1, 0);
+  c->send_cnt.assign(c->world, 0);
+  c->recv_off.assign(c->world, 0);
+  c->recv_cnt.assign(c->world, 0);
+  std::vector<int32_t> slots;
+  for (int r = 0; r < c->world; ++r) {
+    c->send_off[r] = (int64_t)slots.size();
+    c->send_cnt[r] = (int64_t)pl->send_slot[r].size();
+    slots.insert(slots.end(), pl->send_slot[r].begin(), pl->send_slot[r].end());
+    c->recv_off[r] = pl->halo_off[r];
+    c->recv_cnt[r] = pl->halo_off[r + 1] - pl->halo_off[r];
+  }
+  c->send_off[c->world] = (int64_t)slots.size();
+  c->n_send = (int64_t)slots.size();
+  TRY(upload(c, &c->d_send_slot, slots, 1));
+  TRY(zalloc(c, &c->d_sendbuf, (size_t)std::max<int64_t>(c->n_send, 1)));
+  compute_model_bytes(c);
+  return RAS_OK;
+}
+
+static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, const ras_partition* part, int32_t overlap,
+                             const ras_comm* comm) {
+  if (comm) {
+    c->rank = comm->rank;
+    c->world = comm->world;
+    c->device = comm->device;
+    c->dev_alloc = comm->dev_alloc;
+    c->dev_free = comm->dev_free;
+    c->alloc_user = comm->alloc_user;
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return set_err(c, RAS_EINVAL, "bad rank/world");
+    if (c->world > 1 && !comm->nccl_unique_id) return set_err(c, RAS_EINVAL, "world > 1 needs nccl_unique_id");
+    RAS_CUDA(c, cudaSetDevice(c->device));
+  } else {
+    RAS_CUDA(c, cudaGetDevice(&c->device));
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return set_err(c, RAS_ESTATE, "no CUDA device visible");
+  if (comm && comm->cuda_stream) {
+    c->stream = (cudaStream_t)comm->cuda_stream;
+  } else {
+    RAS_CUDA(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  // ---- plan (host, CPU-side) ----
+  ras_status s = ras_plan_build(&c->plan, A, b, part, overlap, c->rank, c->world);
+  if (s != RAS_OK) return set_err(c, s, tls_error());
+  if (c->world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, comm->nccl_unique_id, sizeof(id));
+    RAS_NCCL(c, ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+    TRY(exchange_requests(c));
+  } else {
+    // nothing to exchange: single rank
+  }
+  s = ras_plan_finalize(c->plan);
+  if (s != RAS_OK) return set_err(c, s, tls_error());
+  TRY(upload_plan(c));
+  // ||b||^2 over all ranks (owned rows), fixed order on one rank, NCCL sum across ranks
+  c->b2_global = c->plan->b2_global_local;
+  if (c->world > 1) {
+    std::vector<double> v{c->b2_global};
+    double* d;
+    TRY(upload(c, &d, v));
+    RAS_NCCL(c, ncclAllReduce(d, d, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    RAS_CUDA(c, cudaMemcpyAsync(&c->b2_global, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  if (c->opt.local_solver != RAS_LS_JACOBI_PCG && c->opt.local_solver != RAS_LS_EXACT_PCG)
+    return set_err(c, RAS_EINVAL, "local solver not available in this build");
+  TRY(async_setup(c));
+  RAS_CUDA(c, cudaDeviceSynchronize());
+  return RAS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sync sweep (lock-step, P155-161, P376-387): stream-ordered on one stream.
+// ---------------------------------------------------------------------------
+static ras_status launch_pcg_iter(ras_ctx* c, int it, int m, double inner_tol, bool last) {
+  const unsigned g = (unsigned)c->ntiles;
+  Ctl C{c->d_stop};
+  k_spmv_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C);
+  k_update_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d, c->S, C, m,
+                                              inner_tol);
+  c->launches += 2;
+  if (!last) {
+    k_pupdate<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_r, c->d_p, c->S, C);
+    c->launches += 1;
+  }
+  (void)it;
+  return RAS_OK;
+}
+
+static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact, int slot) {
+  const unsigned g = (unsigned)c->ntiles;
+  Ctl C{c->d_stop};
+  // a1+a2
+  k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x, c->d_r, c->d_p,
+                                            c->S, C);
+  // a6 (global criterion on x^k, P344-346)
+  k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local);
+  c->launches += 2;
+  const double* r2g = c->d_r2_local;
+  if (c->world > 1) {
+    RAS_NCCL(c, ncclAllReduce(c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    r2g = c->d_r2_global;
+  }
+  k_sync_check<<<1, 32, 0, c->stream>>>(r2g, c->b2_global, tol, max_iters, c->d_sync, c->d_stop, c->h_stop_dev + slot);
+  c->launches += 1;
+  // a3
+  if (!exact) {
+    for (int it = 1; it <= m; ++it) TRY(launch_pcg_iter(c, it, m, inner_tol, it == m));
+  } else {
+    // exact mode: iterate until every local subdomain stops (checked every 16 iterations)
+    for (int it = 1; it <= m; ++it) {
+      TRY(launch_pcg_iter(c, it, m, inner_tol, it == m));
+      if (it % 16 == 0) {
+        k_count_active<<<1, 32, 0, c->stream>>>(c->nl, c->S.active, c->d_nactive);
+        c->launches += 1;
+        RAS_CUDA(c, cudaMemcpyAsync(c->h_nactive, c->d_nactive, 4, cudaMemcpyDeviceToHost, c->stream));
+        RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (*c->h_nactive == 0) break;
+      }
+    }
+  }
+  // a4
+  k_prolong<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C);
+  c->launches += 1;
+  // a5: pack + NCCL grouped send/recv straight into halo storage
+  if (c->world > 1) {
+    if (c->n_send) {
+      k_pack<<<(unsigned)std::min<int64_t>((c->n_send + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
+          c->n_send, c->d_send_slot, c->d_x, c->d_sendbuf, C);
+      c->launches += 1;
+    }
+    RAS_NCCL(c, ncclGroupStart());
+    for (int r = 0; r < c->world; ++r) {
+      if (r == c->rank) continue;
+      if (c->send_cnt[r])
+        RAS_NCCL(c, ncclSend(c->d_sendbuf + c->send_off[r], c->send_cnt[r], ncclDouble, r, c->nccl, c->stream));
+      if (c->recv_cnt[r])
+        RAS_NCCL(c, ncclRecv(c->d_x + c->n_own + c->recv_off[r], c->recv_cnt[r], ncclDouble, r, c->nccl, c->stream));
+    }
+    RAS_NCCL(c, ncclGroupEnd());
+  }
+  RAS_CUDA(c, cudaGetLastError());
+  return RAS_OK;
+}
+
+static ras_status load_x0(ras_ctx* c, const double* x0) {
+  const ras_plan* pl = c->plan;
+  std::vector<double> xs((size_t)(c->n_own + c->n_halo), 0.0);
+  if (x0) {
+    for (int64_t i = 0; i < c->n_own; ++i) xs[i] = x0[pl->own_gid[i]];
+    for (int64_t i = 0; i < c->n_halo; ++i) xs[c->n_own + i] = x0[pl->halo_gid[i]];
+  }
+  RAS_CUDA(c, cudaMemcpyAsync(c->d_x, xs.data(), xs.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RAS_OK;
+}
+
+// Gather owner values to x_out (len n) on every rank (P242).
+static ras_status gather(ras_ctx* c, double* x_out) {
+  const ras_plan* pl = c->plan;
+  std::vector<double> own((size_t)c->n_own);
+  RAS_CUDA(c, cudaMemcpyAsync(own.data(), c->d_x, own.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (c->world == 1) {
+    for (int64_t i = 0; i < c->n_own; ++i) x_out[pl->own_gid[i]] = own[i];
+    return RAS_OK;
+  }
+  // all-gather padded (gid, value) pairs
+  std::vector<int64_t> cnt{c->n_own};
+  int64_t *d_cnt, *d_cnts;
+  TRY(upload(c, &d_cnt, cnt));
+  TRY(zalloc(c, &d_cnts, c->world));
+  RAS_NCCL(c, ncclAllGather(d_cnt, d_cnts, 1, ncclInt64, c->nccl, c->stream));
+  std::vector<int64_t> cnts(c->world);
+  RAS_CUDA(c, cudaMemcpyAsync(cnts.data(), d_cnts, c->world * 8, cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  const int64_t mx = *std::max_element(cnts.begin(), cnts.end());
+  std::vector<double> pack((size_t)mx * 2, 0.0);
+  for (int64_t i = 0; i < c->n_own; ++i) {
+    pack[i] = own[i];
+    int64_t g = pl->own_gid[i];
+    std::memcpy(&pack[mx + i], &g, 8);
+  }
+  double *d_pack, *d_all;
+  TRY(upload(c, &d_pack, pack));
+  TRY(zalloc(c, &d_all, (size_t)mx * 2 * c->world));
+  RAS_NCCL(c, ncclAllGather(d_pack, d_all, (size_t)mx * 2, ncclDouble, c->nccl, c->stream));
+  std::vector<double> all((size_t)mx * 2 * c->world);
+  RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < c->world; ++r) {
+    const double* v = all.data() + (size_t)r * mx * 2;
+    for (int64_t i = 0; i < cnts[r]; ++i) {
+      int64_t g;
+      std::memcpy(&g, &v[mx + i], 8);
+      x_out[g] = v[i];
+    }
+  }
+  return RAS_OK;
+}
+
+static ras_status solve_sync(ras_ctx* c, double tol, int64_t max_iters) {
+  const bool exact = c->opt.local_solver == RAS_LS_EXACT_PCG;
+  int64_t max_rows = 0;
+  for (auto& S : c->plan->subs) max_rows = std::max<int64_t>(max_rows, (int64_t)S.omega.size());
+  const int m = exact ? (int)std::min<int64_t>(10 * max_rows, INT32_MAX / 2) : c->opt.inner_iters;
+  const double inner_tol = exact ? 1e-14 : c->opt.inner_tol;
+  // The host runs up to Q sweeps ahead of the device.  Before enqueuing sweep k
+  // it waits for sweep k-Q and reads the stop flag AS OF sweep k-Q (ring slot
+  // written by that sweep's check kernel), so every rank leaves the loop after
+  // the same number of sweeps (matching NCCL calls) without a per-sweep sync.
+  const int Q = std::max(1, c->opt.poll_interval);
+  if (Q > 32) return set_err(c, RAS_EINVAL, "poll_interval must be <= 32");
+  std::vector<cudaEvent_t> ev(Q);
+  for (auto& e : ev) RAS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (int i = 0; i < 32; ++i) c->h_stop[i] = 0;
+  ras_status st = RAS_OK;
+  for (int64_t k = 0;; ++k) {
+    const int slot = (int)(k % Q);
+    if (k >= Q) {
+      if (cudaEventSynchronize(ev[slot]) != cudaSuccess) {
+        st = cuda_err(c, cudaGetLastError(), "sweep");
+        break;
+      }
+      if (((volatile int32_t*)c->h_stop)[slot]) break;
+    }
+    st = sync_sweep(c, tol, max_iters, m, inner_tol, exact, slot);
+    if (st != RAS_OK) break;
+    RAS_CUDA(c, cudaEventRecord(ev[slot], c->stream));
+  }
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return st;
+}
+
+}  // namespace ras
+
+using namespace ras;
+
+extern "C" {
+
+int32_t ras_abi_version(void) { return RAS_ABI_VERSION; }
+
+ras_status ras_options_default(ras_options* o) {
+  if (!o) return RAS_EINVAL;
+  std::memset(o, 0, sizeof(*o));
+  o->local_solver = RAS_LS_JACOBI_PCG;
+  o->inner_iters = 20;
+  o->inner_tol = 0.0;
+  o->detector = RAS_DET_DECENTRAL;
+  o->max_resumes = 3;
+  o->use_graphs = 1;
+  o->poll_interval = 4;
+  o->async_timeout_s = 1800.0;
+  return RAS_OK;
+}
+
+ras_status ras_setup(ras_ctx** out, const ras_csr* A, const double* b, const ras_partition* part, int32_t overlap,
+                     const ras_options* opt, const ras_comm* comm) {
+  if (!out) return set_err(nullptr, RAS_EINVAL, "ras_setup: out is NULL");
+  *out = nullptr;
+  const double t0 = now_s();
+  ras_ctx* c = new ras_ctx();
+  ras_options_default(&c->opt);
+  if (opt) c->opt = *opt;
+  if (c->opt.inner_iters < 1) c->opt.inner_iters = 1;
+  if (c->opt.inner_tol < 0) {
+    set_tls_error("inner_tol must be >= 0");
+    delete c;
+    return RAS_EINVAL;
+  }
+  ras_status s = setup_impl(c, A, b, part, overlap, comm);
+  if (s != RAS_OK) {
+    set_tls_error(c->err.empty() ? tls_error() : c->err);
+    ras_free(c);
+    return s;
+  }
+  c->setup_s = now_s() - t0;
+  *out = c;
+  return RAS_OK;
+}
+
+ras_status ras_set_rhs(ras_ctx* c, const double* b) {
+  if (!c || !b) return RAS_EINVAL;
+  ras_plan* pl = c->plan;
+  std::vector<double> bl(pl->rows_pad, 0.0);
+  double b2 = 0.0;
+  for (auto& S : pl->subs)
+    for (int64_t i = 0; i < S.nrows; ++i) {
+      const double v = b[S.omega[i] - pl->row_begin];
+      bl[S.row_off + i] = v;
+      if (S.owned[i]) b2 += v * v;
+    }
+  RAS_CUDA(c, cudaMemcpy(c->d_b, bl.data(), bl.size() * 8, cudaMemcpyHostToDevice));
+  c->b2_global = b2;
+  if (c->world > 1) {
+    RAS_CUDA(c, cudaMemcpy(c->d_r2_global, &b2, 8, cudaMemcpyHostToDevice));
+    RAS_NCCL(c, ncclAllReduce(c->d_r2_global, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    RAS_CUDA(c, cudaMemcpyAsync(&c->b2_global, c->d_r2_global, 8, cudaMemcpyDeviceToHost, c->stream));
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  return RAS_OK;
+}
+
+static ras_status solve_common(ras_ctx* c, double tol, int64_t max_iters, ras_mode mode) {
+  if (!(tol > 0.0)) return set_err(c, RAS_EINVAL, "tol must be > 0");
+  if (max_iters < 0) return set_err(c, RAS_EINVAL, "max_iters must be >= 0");
+  RAS_CUDA(c, cudaSetDevice(c->device));
+  std::memset(&c->st, 0, sizeof(c->st));
+  c->launches = 0;
+  SyncState z{};
+  RAS_CUDA(c, cudaMemcpyAsync(c->d_sync, &z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(c->d_stop, 0, 4, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(c->S.inner_total, 0, c->nl * 8, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(c->S.ticket, 0, c->nl * 4, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  ras_status s;
+  if (mode == RAS_SYNC) {
+    s = solve_sync(c, tol, max_iters);
+    if (s != RAS_OK) return s;
+    SyncState h{};
+    RAS_CUDA(c, cudaMemcpy(&h, c->d_sync, sizeof(h), cudaMemcpyDeviceToHost));
+    c->st.converged = h.converged;
+    c->st.verified = h.converged;
+    c->st.sweeps = h.sweeps;
+    c->st.final_rel_residual = h.rel;
+    c->updates.assign(c->nl, h.sweeps);
+    c->st.updates_min = c->st.updates_median = c->st.updates_max = h.sweeps;
+  } else if (mode == RAS_ASYNC) {
+    s = solve_async(c, tol, max_iters);
+    if (s != RAS_OK && s != RAS_ENOCONV && s != RAS_EVERIFY) return s;
+    if (s != RAS_OK) return s;
+  } else {
+    return set_err(c, RAS_EINVAL, "unknown mode");
+  }
+  return RAS_OK;
+}
+
+static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
+  c->st.mode = mode;
+  c->st.time_to_solution_s = t;
+  c->st.setup_s = c->setup_s;
+  c->st.num_subdomains = c->plan->P;
+  c->st.world = c->world;
+  c->st.local_subdomains = c->nl;
+  c->st.rows_local = c->plan->rows_local;
+  c->st.halo_values = c->n_halo;
+  c->st.kernel_launches = c->launches;
+  std::vector<int64_t> it(c->nl, 0);
+  cudaMemcpy(it.data(), c->S.inner_total, c->nl * 8, cudaMemcpyDeviceToHost);
+  c->st.inner_iters_total = std::accumulate(it.begin(), it.end(), (int64_t)0);
+  // algorithmic bytes: per sweep residual + prolong + pack; per
+  // PCG iteration of subdomain p the three passes over its |Omega_p| rows
+  double frac_iters = 0.0;
+  const double rows = (double)std::max<int64_t>(c->plan->rows_local, 1);
+  for (int i = 0; i < c->nl; ++i) frac_iters += (double)it[i] * (double)c->plan->subs[i].nrows / rows;
+  c->st.model_bytes = (double)c->st.sweeps * (c->mb.residual + c->mb.prolong + c->mb.pack) +
+                      frac_iters * (c->mb.spmv_dot + c->mb.update_dot + c->mb.pupdate);
+}
+
+ras_status ras_solve(ras_ctx* c, double tol, int64_t max_iters, ras_mode mode, const double* x0, double* x_out) {
+  if (!c) return set_err(nullptr, RAS_EINVAL, "ras_solve: ctx is NULL");
+  const double t0 = now_s();
+  RAS_CUDA(c, cudaSetDevice(c->device));
+  TRY(load_x0(c, x0));
+  ras_status s = solve_common(c, tol, max_iters, mode);
+  if (s != RAS_OK && s != RAS_ENOCONV && s != RAS_EVERIFY) return s;
+  const double t1 = now_s();
+  finish_stats(c, mode, t1 - t0);
+  if (x_out) TRY(gather(c, x_out));
+  if (s != RAS_OK) return s;
+  return c->st.converged ? RAS_OK : RAS_ENOCONV;
+}
+
+ras_status ras_solve_device(ras_ctx* c, double tol, int64_t max_iters, ras_mode mode, const double* x0_owned_dev,
+                            double* x_owned_dev) {
+  if (!c) return set_err(nullptr, RAS_EINVAL, "ras_solve_device: ctx is NULL");
+  RAS_CUDA(c, cudaSetDevice(c->device));
+  const double t0 = now_s();
+  if (x0_owned_dev) {
+    RAS_CUDA(c, cudaMemcpyAsync(c->d_x, x0_owned_dev, c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    RAS_CUDA(c, cudaMemsetAsync(c->d_x, 0, c->n_own * 8, c->stream));
+  }
+  if (c->n_halo) {
+    if (x0_owned_dev && c->world > 1) {
+      // halo = neighbours' owned x0 values: one exchange
+      Ctl C{nullptr};
+      if (c->n_send) {
+        k_pack<<<(unsigned)std::min<int64_t>((c->n_send + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
+            c->n_send, c->d_send_slot, c->d_x, c->d_sendbuf, C);
+      }
+      RAS_NCCL(c, ncclGroupStart());
+      for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        if (c->send_cnt[r])
+          RAS_NCCL(c, ncclSend(c->d_sendbuf + c->send_off[r], c->send_cnt[r], ncclDouble, r, c->nccl, c->stream));
+        if (c->recv_cnt[r])
+          RAS_NCCL(c,
+                   ncclRecv(c->d_x + c->n_own + c->recv_off[r], c->recv_cnt[r], ncclDouble, r, c->nccl, c->stream));
+      }
+      RAS_NCCL(c, ncclGroupEnd());
+    } else {
+      RAS_CUDA(c, cudaMemsetAsync(c->d_x + c->n_own, 0, c->n_halo * 8, c->stream));
+    }
+  }
+  ras_status s = solve_common(c, tol, max_iters, mode);
+  if (s != RAS_OK && s != RAS_ENOCONV && s != RAS_EVERIFY) return s;
+  finish_stats(c, mode, now_s() - t0);
+  if (x_owned_dev) RAS_CUDA(c, cudaMemcpyAsync(x_owned_dev, c->d_x, c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (s != RAS_OK) return s;
+  return c->st.converged ? RAS_OK : RAS_ENOCONV;
+}
+
+int64_t ras_owned_count(const ras_ctx* c) { return c ? c->n_own : -1; }
+
+ras_status ras_owned_gids(const ras_ctx* c, int64_t* g) {
+  if (!c || !g) return RAS_EINVAL;
+  std::copy(c->plan->own_gid.begin(), c->plan->own_gid.end(), g);
+  return RAS_OK;
+}
+
+ras_status ras_stats(const ras_ctx* c, ras_stats_t* out) {
+  if (!c || !out) return RAS_EINVAL;
+  *out = c->st;
+  return RAS_OK;
+}
+
+ras_status ras_update_counts(const ras_ctx* c, int64_t* out) {
+  if (!c || !out) return RAS_EINVAL;
+  for (int i = 0; i < c->nl; ++i) out[i] = i < (int)c->updates.size() ? c->updates[i] : 0;
+  return RAS_OK;
+}
+
+void ras_free(ras_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  async_free(c);
+  for (auto& b : c->bufs) {
+    if (c->dev_free)
+      c->dev_free(b.ptr, c->alloc_user);
+    else
+      cudaFree(b.ptr);
+  }
+  if (c->h_stop) cudaFreeHost(c->h_stop);
+  if (c->h_nactive) cudaFreeHost(c->h_nactive);
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  ras_plan_free(c->plan);
+  delete c;
+}
+
+const char* ras_last_error(const ras_ctx* c) {
+  if (!c) return tls_error().c_str();
+  return c->err.c_str();
+}
+
+ras_status ras_nccl_unique_id(void* out128) {
+  if (!out128) return RAS_EINVAL;
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    set_tls_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    return RAS_ENCCL;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return RAS_OK;
+}
+
+ras_status ras_ctx_plan(const ras_ctx* c, const ras_plan** out) {
+  if (!c || !out) return RAS_EINVAL;
+  *out = c->plan;
+  return RAS_OK;
+}
+
+ras_status ras_set_scripted_flags(ras_ctx* c, const uint8_t* flags, int64_t nsweeps) {
+  if (!c || (!flags && nsweeps)) return RAS_EINVAL;
+  c->scripted.assign(flags, flags + nsweeps * c->nl);
+  c->scripted_sweeps = nsweeps;
+  return RAS_OK;
+}
+
+ras_status ras_detector_stops(const ras_ctx* c, int64_t* out) {
+  if (!c || !out) return RAS_EINVAL;
+  for (int i = 0; i < c->nl; ++i) out[i] = i < (int)c->det_stops.size() ? c->det_stops[i] : -1;
+  return RAS_OK;
+}
+
+}  // extern "C"

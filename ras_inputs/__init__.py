@@ -29,6 +29,7 @@ __all__ = [
     "laplace_2d_rows",
     "laplace_3d_rows",
     "rhs",
+    "rhs_rows",
     "voronoi_partition",
     "read_partition_file",
     "write_partition_file",
@@ -136,6 +137,16 @@ def laplace_3d_rows(nx: int, ny: int, nz: int, r0: int, r1: int) -> CSR:
 def rhs(n: int, seed: int = 0) -> np.ndarray:
     """Random RHS, uniform in [-1, 1], FP64 (P440; SPEC S135)."""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, int(n))
+
+
+def rhs_rows(n: int, r0: int, r1: int, seed: int = 0) -> np.ndarray:
+    """rhs(n, seed)[r0:r1] without drawing the prefix (PCG64 advance: one 64-bit
+    draw per double), for row windows of very large problems."""
+    if not (0 <= r0 <= r1 <= n):
+        raise ValueError("bad window")
+    g = np.random.default_rng(seed)
+    g.bit_generator.advance(int(r0))
+    return g.uniform(-1.0, 1.0, int(r1 - r0))
 
 
 def _morton2(ix: np.ndarray, iy: np.ndarray) -> np.ndarray:

@@ -1,0 +1,141 @@
+"""GPU parity of the synchronous RAS path against the oracle, through the C ABI.
+
+Bar (BASELINE.json north_star): sync iterates within 1e-10 relative (FP64),
+converged solutions reach true relative residual <= tol, index maps bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import ras_inputs as ri
+
+pytestmark = pytest.mark.gpu
+
+R = pytest.importorskip("paper_2003_05361_b200")
+
+
+def oracle_iterates(A, b, owner, gamma, kind, m, k, inner_tol=0.0):
+    subs = O.setup(A, b, owner, gamma)
+    for s in subs:
+        O.make_local_solver(s, kind, m, inner_tol)
+    return O.ras_sync(A, b, subs, 1e-300, k, record_iterates=True)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("case", ["c1", "voronoi_ragged", "strips"])
+def test_sync_iterates_match_oracle(case):
+    if case == "c1":
+        nx = ny = 64
+        A = ri.laplace_2d(nx)
+        owner = R.partition_regular(nx, ny, 1, 2, 2, 1)
+        gamma, m = 2, 20
+    elif case == "voronoi_ragged":
+        nx, ny = 203, 157  # several 256-row tiles per subdomain and ragged tails
+        A = ri.laplace_2d(nx, ny)
+        owner = ri.voronoi_partition(nx, ny, 7, seed=4)
+        gamma, m = 3, 15
+    else:
+        nx, ny = 96, 64
+        A = ri.laplace_2d(nx, ny)
+        owner = R.partition_regular(nx, ny, 1, 1, 5, 1)
+        gamma, m = 1, 7
+    b = ri.rhs(nx * ny, 0)
+    K = 6
+    ref = oracle_iterates(A, b, owner, gamma, "jacobi", m, K)
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m))
+    for k in (1, 2, K):
+        st, x = s.solve(1e-300, k, "sync")
+        assert st == R._ffi.RAS_ENOCONV
+        assert s.stats()["sweeps"] == k
+        assert rel(x, ref.iterates[k]) <= 1e-10, (case, k, rel(x, ref.iterates[k]))
+    s.close()
+
+
+def test_sync_converges_to_tolerance_and_matches_oracle_solution():
+    N = 64
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 0)
+    owner = R.partition_regular(N, N, 1, 2, 2, 1)
+    s = R.Solver(A, b, owner, 2, R.options("jacobi", 20))
+    st, x = s.solve(1e-8, 5000, "sync")
+    assert st == R._ffi.RAS_OK
+    ok, relres = O.verify_global(A, x, b, 1e-8)
+    assert ok
+    st_ = s.stats()
+    assert abs(st_["final_rel_residual"] - relres) <= 1e-12 + 1e-6 * relres
+    subs = O.setup(A, b, owner, 2)
+    for sb in subs:
+        O.make_local_solver(sb, "jacobi", 20)
+    ref = O.ras_sync(A, b, subs, 1e-8, 5000)
+    assert st_["sweeps"] == ref.sweeps
+    assert rel(x, ref.x) <= 1e-10
+    xs = np.linalg.solve(A.to_scipy().toarray(), b)
+    assert rel(x, xs) <= 1e-6  # R25 (N <= 256)
+    s.close()
+
+
+def test_exact_mode_c1_sweeps_and_solution():
+    # C1: 64x64, 2x2, overlap 2, "exact" local solve (PCG to 1e-14, R6): 106 sweeps (oracle)
+    N = 64
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 0)
+    owner = R.partition_regular(N, N, 1, 2, 2, 1)
+    subs = O.setup(A, b, owner, 2)
+    for sb in subs:
+        O.make_local_solver(sb, "exact")
+    ref = O.ras_sync(A, b, subs, 1e-8, 1000, record_iterates=True)
+    assert ref.sweeps == 106
+    s = R.Solver(A, b, owner, 2, R.options("exact"))
+    for k in (1, 5):
+        st, x = s.solve(1e-300, k, "sync")
+        assert rel(x, ref.iterates[k]) <= 1e-10
+    st, x = s.solve(1e-8, 1000, "sync")
+    assert st == R._ffi.RAS_OK
+    assert s.stats()["sweeps"] == 106
+    assert rel(x, ref.x) <= 1e-10
+    s.close()
+
+
+def test_edge_cases():
+    N = 24
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 1)
+    xs = np.linalg.solve(A.to_scipy().toarray(), b)
+    # one subdomain, no overlap, exact local solve: one sweep solves (north_star invariant)
+    s = R.Solver(A, b, np.zeros(N * N, np.int32), 0, R.options("exact"))
+    st, x = s.solve(1e-10, 10, "sync")
+    assert st == 0 and s.stats()["sweeps"] == 1 and rel(x, xs) <= 1e-12
+    s.close()
+    owner = R.partition_regular(N, N, 1, 3, 2, 1)
+    s = R.Solver(A, b, owner, 1, R.options("jacobi", 5))
+    # max_iters = 0 returns x0 and its residual
+    st, x = s.solve(1e-8, 0, "sync")
+    assert st == R._ffi.RAS_ENOCONV and not x.any() and abs(s.stats()["final_rel_residual"] - 1.0) < 1e-14
+    # x0 = exact solution: converged at sweep 0
+    st, x = s.solve(1e-8, 10, "sync", x0=xs)
+    assert st == 0 and s.stats()["sweeps"] == 0 and np.array_equal(x, xs)
+    s.close()
+    # b = 0 -> x = 0 converged immediately (R11)
+    s = R.Solver(A, np.zeros(N * N), owner, 1, R.options("jacobi", 5))
+    st, x = s.solve(1e-8, 10, "sync")
+    assert st == 0 and not x.any()
+    s.close()
+
+
+def test_errors_are_reported():
+    N = 8
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N)
+    owner = np.zeros(N * N, np.int32)
+    owner[5] = 3  # subdomains 1, 2 empty
+    with pytest.raises(R.RasError, match="empty"):
+        R.Solver(A, b, owner, 1)
+    with pytest.raises(R.RasError, match="overlap"):
+        R.Solver(A, b, np.zeros(N * N, np.int32), -1)
+    B = ri.laplace_2d(N)
+    B.data[B.indptr[3]:B.indptr[4]] *= -1.0  # negative diagonal in row 3
+    with pytest.raises(R.RasError, match="RAS_ENOTSPD.*subdomain 0"):
+        R.Solver(B, b, np.zeros(N * N, np.int32), 1)

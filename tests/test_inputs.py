@@ -103,3 +103,9 @@ def test_partition_file_roundtrip_and_errors(tmp_path):
     own = ri.voronoi_partition(20, 20, 5)
     ri.write_partition_file(str(p), own)
     assert np.array_equal(ri.read_partition_file(str(p), 5, 400), own)
+
+
+def test_rhs_rows_window_equals_slice():
+    full = ri.rhs(5000, 3)
+    assert np.array_equal(ri.rhs_rows(5000, 1234, 4321, 3), full[1234:4321])
+    assert np.array_equal(ri.rhs_rows(5000, 0, 5000, 3), full)

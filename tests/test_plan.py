@@ -1,0 +1,146 @@
+"""Host-side setup plan (scope row a0) against the oracle, bit-exact, on CPU.
+
+The plan is pure host C++ inside libras_b200.so (no CUDA call), so partitions,
+overlap sets, ghosts, restrict/prolong/pack maps are checked here without a GPU.
+Also: the library loads and exports every symbol include/*.h declares."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import ras_inputs as ri
+
+R = pytest.importorskip("paper_2003_05361_b200")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = set()
+    for h in ("ras.h", "ras_plan.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names |= set(re.findall(r"^\s*(?:const char\*|ras_status|void|int32_t|int64_t)\s+\**(ras_\w+)\s*\(", src, re.M))
+    lib = R._ffi.lib()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(lib, n), n
+    assert {n for n, _, _ in R._ffi.SIGNATURES} == names
+    assert lib.ras_abi_version() == 1
+
+
+@pytest.mark.parametrize("dims,parts", [((10, 1, 1), (3, 1, 1)), ((64, 64, 1), (2, 2, 1)), ((17, 9, 1), (4, 3, 1)),
+                                        ((6, 5, 4), (2, 2, 2)), ((33, 12, 1), (1, 5, 1))])
+def test_partition_regular_bit_exact(dims, parts):
+    assert np.array_equal(R.partition_regular(*dims, *parts), O.partition_regular(*dims, *parts))
+
+
+def test_partition_regular_rejects_empty_blocks():
+    with pytest.raises(R.RasError):
+        R.partition_regular(3, 3, 1, 4, 1, 1)
+
+
+CASES = {
+    "c1": (lambda: ri.laplace_2d(64), lambda: O.partition_regular(64, 64, 1, 2, 2, 1), 2),
+    "voronoi": (lambda: ri.laplace_2d(41, 37), lambda: ri.voronoi_partition(41, 37, 9, seed=7), 3),
+    "strips_g0": (lambda: ri.laplace_2d(20, 30), lambda: O.partition_regular1d(30, 4)[:600], 0),
+    "3d": (lambda: ri.laplace_3d(9, 8, 7), lambda: O.partition_regular(9, 8, 7, 2, 2, 2), 2),
+}
+
+
+def _storage_order(subs_local, owner, sub_to_rank, rank):
+    own = np.concatenate([s.omega[s.owned] for s in subs_local])
+    need = set()
+    for s in subs_local:
+        need |= set(s.omega[~s.owned].tolist()) | set(s.ghosts.tolist())
+    halo = [g for g in need if sub_to_rank[owner[g]] != rank]
+    halo.sort(key=lambda g: (sub_to_rank[owner[g]], g))
+    return own, np.array(halo, dtype=np.int64)
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_plan_maps_bit_exact_vs_oracle(case, world):
+    mkA, mkown, gamma = CASES[case]
+    A = mkA()
+    owner = mkown()
+    P = int(owner.max()) + 1
+    if world > P:
+        pytest.skip("more ranks than subdomains")
+    b = ri.rhs(A.n, 0)
+    subs = O.setup(A, b, owner, gamma)
+    sub_to_rank = np.array([(p * world) // P for p in range(P)])
+    plans = [R.Plan(A, b, owner, gamma, rank=r, world=world) for r in range(world)]
+    # exchange halo requests in-process (what ras_setup does over NCCL)
+    for q in range(world):
+        for r in range(world):
+            if q != r:
+                g, off = plans[q].halo_request(r)
+                plans[r].set_send(q, g, off)
+    for pl in plans:
+        pl.finalize()
+    for r, pl in enumerate(plans):
+        info = pl.info()
+        local = [s for s in subs if sub_to_rank[s.p] == r]
+        assert info["local_subdomains"] == len(local)
+        own_gids, halo_gids = pl.storage_gids()
+        want_own, want_halo = _storage_order(local, owner, sub_to_rank, r)
+        assert np.array_equal(own_gids, want_own)
+        assert np.array_equal(halo_gids, want_halo)
+        slot = {int(g): i for i, g in enumerate(np.concatenate([own_gids, halo_gids]))}
+        assert info["rows_local"] == sum(len(s.omega) for s in local)
+        for li, s in enumerate(local):
+            p, om, ow, gh = pl.subdomain(li)
+            assert p == s.p
+            assert np.array_equal(om, s.omega) and np.array_equal(ow, s.owned) and np.array_equal(gh, s.ghosts)
+            rs, ps, gs = pl.maps(li)
+            assert np.array_equal(rs, [slot[int(g)] for g in s.omega])
+            assert np.array_equal(ps, np.where(s.owned, rs, -1))
+            assert np.array_equal(gs, [slot[int(g)] for g in s.ghosts])
+        # pack lists: what each peer q needs from r, in q's halo order, and where it lands
+        for q in range(world):
+            if q == r:
+                continue
+            g, sl, off = pl.send_list(q)
+            qh, qoff = plans[q].halo_request(r)
+            assert np.array_equal(g, qh) and off == qoff
+            assert np.array_equal(own_gids[sl], g)
+        assert info["nnz_residual"] == sum(A.to_scipy()[s.omega].nnz for s in local)
+        assert info["nnz_local"] == sum(s.A.nnz for s in local)
+
+
+def test_plan_c1_sizes():
+    A = ri.laplace_2d(64)
+    owner = O.partition_regular(64, 64, 1, 2, 2, 1)
+    pl = R.Plan(A, ri.rhs(4096), owner, 2)
+    pl.finalize()
+    i = pl.info()
+    assert i["rows_local"] == 4 * 1153 and i["nnz_local"] == 4 * 5629 and i["n_halo"] == 0
+
+
+def test_plan_row_window():
+    nx, ny = 30, 40
+    owner = O.partition_regular(nx, ny, 1, 1, 4, 1)  # 4 strips of 10 grid rows
+    full = R.Plan(ri.laplace_2d(nx, ny), None, owner, 2, rank=1, world=4)
+    # rank 1 owns grid rows 10..19; Omega needs rows 8..21 -> window rows [8*nx, 22*nx)
+    win = ri.laplace_2d_rows(nx, ny, 8 * nx, 22 * nx)
+    wp = R.Plan(win, None, owner, 2, rank=1, world=4)
+    assert np.array_equal(full.subdomain(0)[1], wp.subdomain(0)[1])
+    small = ri.laplace_2d_rows(nx, ny, 9 * nx, 21 * nx)
+    with pytest.raises(R.RasError, match="outside the CSR row window"):
+        R.Plan(small, None, owner, 2, rank=1, world=4)
+
+
+def test_plan_validation_errors():
+    A = ri.laplace_2d(6)
+    own = np.zeros(36, np.int32)
+    with pytest.raises(R.RasError, match="owner"):
+        bad = own.copy()
+        bad[3] = 7
+        R.Plan(A, None, bad, 1, num_subdomains=2)
+    with pytest.raises(R.RasError, match="no subdomain"):
+        R.Plan(A, None, own, 1, rank=1, world=2)
+    B = ri.laplace_2d(6)
+    B.indices[B.indptr[2]], B.indices[B.indptr[2] + 1] = B.indices[B.indptr[2] + 1], B.indices[B.indptr[2]]
+    with pytest.raises(R.RasError, match="strictly increasing"):
+        R.Plan(B, None, own, 1)
