@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native RAS hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1] = C2 at N=1; C3-style weak scaling at N>1):
+2D 5-point Laplacian, 1024x1024 owned unknowns per subdomain, 16 subdomains per
+GPU (4x4 tiles at N=1: 4096^2 = 16.8M unknowns), overlap 8, Jacobi-PCG m=20,
+synchronous RAS.  One "step" = one RAS sweep over the whole problem (restrict,
+residual, local solves, restricted prolongation, exchange, global check).
+
+value     = aggregate subdomain updates / s (= subdomains x sweeps / s, max over ranks)
+e2e       = the same through ras_solve() with pinned HOST x0 / x_out, copies inside
+roofline  = dominant kernel: algorithmic bytes / CUDA-event duration vs measured HBM copy peak
+cpu_baseline = the oracle on a bounded sample (rank 0, N=1)
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode sync|async]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import ras_inputs as ri  # noqa: E402
+
+SUB = 1024          # owned unknowns per subdomain side
+PER_GPU = (4, 4)    # subdomain tiles per GPU
+GAMMA = 8
+M_INNER = 20
+TILES = {1: (4, 4), 2: (4, 8), 4: (8, 8), 8: (8, 16)}
+
+
+def workload(N):
+    px, py = TILES.get(N, (4, 4 * N))
+    return px, py, px * SUB, py * SUB
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="sync", choices=["sync", "async"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--tts", action="store_true", help="also run to rel. residual 1e-8 (long)")
+    ap.add_argument("--scale", type=int, default=SUB, help="owned side per subdomain (debug)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+# ----------------------------------------------------------------------------
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, devices):
+        self.devices = devices
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", ",".join(str(d) for d in self.devices)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            # nvidia-smi needs ~1 s before its first sample: wait for it so the
+            # samples cover the timed region that follows
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.05)
+        except OSError:
+            self.proc = None
+        self.window = [None, None]
+        return self
+
+    def mark(self, i):
+        self.window[i] = time.time()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(1)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        w0, w1 = self.window
+        for ts, ln in self.lines:
+            if w0 is not None and w1 is not None and not (w0 - 0.06 <= ts <= w1 + 0.06):
+                continue  # keep samples taken during the timed region
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(REASONS, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def build_rank_problem(N, rank, scale=SUB):
+    """Row window of the global Laplacian + RHS + owner array for one rank."""
+    from paper_2003_05361_b200 import partition_regular
+
+    px, py = TILES.get(N, (4, 4 * N))
+    nx, ny = px * scale, py * scale
+    n = nx * ny
+    owner = partition_regular(nx, ny, 1, px, py, 1)
+    P = px * py
+    s0, s1 = (rank * P) // N, ((rank + 1) * P) // N  # contiguous subdomain ids (default sub_to_rank)
+    ty0, ty1 = s0 // px, (s1 - 1) // px + 1            # tile rows of this rank
+    r0 = max(0, ty0 * scale - (GAMMA + 1))
+    r1 = min(ny, ty1 * scale + (GAMMA + 1))
+    A = ri.laplace_2d_rows(nx, ny, r0 * nx, r1 * nx)
+    b = ri.rhs_rows(n, r0 * nx, r1 * nx, 0)
+    return dict(nx=nx, ny=ny, n=n, P=P, px=px, py=py, owner=owner, A=A, b=b)
+
+
+# ----------------------------------------------------------------------------
+# reference arm and cpu baseline: the oracle, as it stands, on host cores
+# ----------------------------------------------------------------------------
+def oracle_sample(nx, ny, P, px, sample_subs, sweeps_per_sub, budget_s=25.0):
+    """Time the oracle's per-subdomain work of a sync sweep (local residual +
+    Jacobi-PCG(m) + restricted prolongation) on `sample_subs` subdomains of the
+    bench workload, plus the oracle's global residual check; return
+    (subdomain updates per second, details)."""
+    from threadpoolctl import threadpool_limits
+
+    import oracle as O
+
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 0)
+    owner = O.partition_regular(nx, ny, 1, px, P // px, 1)
+    As = O.as_scipy(A)
+    x = np.zeros(nx * ny)
+    times = []
+    with threadpool_limits(1):
+        for p in sample_subs:
+            om, ow, gh = O.overlap_sets(As, owner, p, GAMMA)
+            rows = As[om]
+            sub = O.Subdomain(p, om, ow, gh, rows[:, om].tocsr(), rows[:, gh].tocsr(), b[om].copy())
+            O.make_local_solver(sub, "jacobi", M_INNER)
+            for _ in range(sweeps_per_sub):
+                t0 = time.perf_counter()
+                rt = O.local_residual(sub, x)
+                d = sub.solver(rt)
+                og = sub.owned_global
+                x[og] = x[og] + d[sub.owned]
+                times.append(time.perf_counter() - t0)
+            if sum(times) > budget_s:
+                break
+        t0 = time.perf_counter()
+        r = b - As @ x
+        _ = float(np.linalg.norm(r)) / float(np.linalg.norm(b))
+        t_res = time.perf_counter() - t0
+    t_sub = statistics.mean(times)
+    sweep_s = P * t_sub + t_res
+    return P / sweep_s, {"t_sub_update_s": t_sub, "t_global_residual_s": t_res, "sweep_s": sweep_s,
+                         "samples": len(times)}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    N = args.gpus
+    px, py, nx, ny = workload(N) if args.scale == SUB else (4, 4, 4 * args.scale, 4 * args.scale)
+    P = px * py
+    steps = max(1, args.steps)
+    warm = max(0, args.warmup)
+    # one reference "step" = one sampled subdomain update (+1/P of the global residual)
+    t0 = time.perf_counter()
+    val, det = oracle_sample(nx, ny, P, px, [5, 6], max(1, (steps + warm + 1) // 2), budget_s=120.0)
+    wall = time.perf_counter() - t0
+    line = {
+        "impl": "reference", "metric": "RAS iterations/s (aggregate subdomain updates/s)", "value": val,
+        "unit": "updates/s", "n_gpus": N, "steps": steps, "warmup": warm,
+        "ms_per_step": det["sweep_s"] * 1000.0 / P, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(N, nx, ny, P, "sync"),
+        "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle",
+                         "sample": f"oracle (NumPy/SciPy, 1 thread) local residual + Jacobi-PCG(m={M_INNER}) + prolong "
+                                   f"on subdomains 5,6 of the workload, {det['samples']} updates, plus one global "
+                                   f"residual; sweep time = P*t_update + t_residual = {det['sweep_s']:.2f} s",
+                         "host_cores_available": os.cpu_count()},
+        "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(N, nx, ny, P, mode, ws_bytes=None):
+    return {"workload": (f"{'C2' if N == 1 else 'C3-weak'}: 2D 5-pt Laplacian {nx}x{ny} ({nx * ny / 1e6:.1f}M unknowns), "
+                         f"{P} subdomains of {SUB}^2 ({P // N}/GPU), overlap {GAMMA}, Jacobi-PCG m={M_INNER}, {mode} RAS"),
+            "grid": [nx, ny], "subdomains": P, "subdomains_per_gpu": P // N, "overlap": GAMMA,
+            "inner_iters": M_INNER, "mode": mode, "precision": "fp64",
+            "parallelism": f"domain decomposition, {P // N} subdomains per GPU x {N} GPU",
+            "l2": (f"working set {ws_bytes / 1e9:.2f} GB per GPU >> 126 MB L2, no flush needed"
+                   if ws_bytes else "working set >> 126 MB L2")}
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_05361_b200 as R
+
+    rank, world, local = dist_env()
+    N = args.gpus
+    if world != N:
+        raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    nccl_id = None
+    if world > 1:
+        obj = [R.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    t_setup0 = time.perf_counter()
+    prob = build_rank_problem(N, rank, args.scale)
+    opts = R.options("jacobi", M_INNER)
+    solver = R.Solver(prob["A"], prob["b"], prob["owner"], GAMMA, opts,
+                      comm={"rank": rank, "world": world, "device": local, "nccl_id": nccl_id,
+                            "stream": stream.cuda_stream})
+    del prob["A"]
+    setup_s = time.perf_counter() - t_setup0
+    info = solver.plan().info()
+    P, nx, ny, n = prob["P"], prob["nx"], prob["ny"], prob["n"]
+    mode = args.mode
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    if args.warmup > 0:
+        solver.solve_device(1e-300, args.warmup, mode)
+    barrier()
+    solver.kernel_timing(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler([local] if world == 1 else list(range(world))) as clk:
+        barrier()
+        clk.mark(0)
+        e0.record(stream)
+        st = solver.solve_device(1e-300, args.steps, mode)
+        e1.record(stream)
+        barrier()
+        clk.mark(1)
+    ms_local = e0.elapsed_time(e1)
+    stats = solver.stats()
+    ktimes = solver.kernel_times()
+    solver.kernel_timing(False)
+    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    sweeps = stats["sweeps"] if mode == "sync" else stats["updates_max"]
+    value = P * args.steps / (ms / 1e3)  # aggregate subdomain updates / s
+
+    # roofline: dominant kernel by event time
+    tot_ms = sum(v[1] for v in ktimes.values())
+    kern = {}
+    for name, (cnt, kms, bpl) in ktimes.items():
+        if cnt == 0:
+            continue
+        avg_ms = kms / cnt
+        kern[name] = {"launches": cnt, "avg_us": avg_ms * 1e3, "share": kms / tot_ms if tot_ms else None,
+                      "bytes_per_launch": bpl, "gbs": (bpl / (avg_ms / 1e3) / 1e9) if bpl and avg_ms > 0 else None}
+    dom = max((k for k in kern if kern[k]["bytes_per_launch"]), key=lambda k: kern[k]["share"] or 0)
+    peak, peak_src = measured_peaks()
+    tr = ncu_traffic(dom)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kern[dom]["gbs"] / peak, "traffic": tr, "peak_source": peak_src,
+            "bytes_per_launch": kern[dom]["bytes_per_launch"],
+            "bytes_model": "DESIGN.md §5: compulsory bytes of real rows/entries, int32 SELL indices, FP64 values"}
+    pcg_bytes = sum(kern[k]["bytes_per_launch"] * kern[k]["launches"] for k in kern if kern[k]["bytes_per_launch"])
+    pcg_ms = sum(ktimes[k][1] for k in kern if kern[k]["bytes_per_launch"])
+    # e2e through ras_solve with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        x0 = torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
+        xo = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            _solve_host(solver, x0, xo, mode)
+        barrier()
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        d2h = n * 8 if world == 1 else (n * 8 + info["n_own"] * 8 * 2)
+        e2e = {"value": P * args.e2e_steps / el, "unit": "updates/s", "h2d_bytes_per_step": n * 8,
+               "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "note": "each step = ras_solve(x0=pinned host, max_iters=1, x_out=pinned host): H2D x0, one sweep + "
+                       "final check, gather, D2H x"}
+    # optional time-to-solution
+    tts = None
+    if args.tts:
+        barrier()
+        t0 = time.perf_counter()
+        st = solver.solve_device(1e-8, 200000, mode)
+        barrier()
+        s2 = solver.stats()
+        tts = {"time_s": time.perf_counter() - t0, "device_time_s": s2["time_to_solution_s"],
+               "sweeps": s2["sweeps"], "inner_iters_total": s2["inner_iters_total"],
+               "final_rel_residual": s2["final_rel_residual"], "converged": bool(s2["converged"])}
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        val, det = oracle_sample(nx, ny, P, prob["px"], [5, 6], 2)
+        cpu = {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle (NumPy/SciPy, BLAS limited to 1 thread) local residual + Jacobi-PCG(m={M_INNER}) + "
+                         f"prolong on subdomains 5,6 of this workload ({det['samples']} updates, "
+                         f"{det['t_sub_update_s']:.2f} s each) + one global residual ({det['t_global_residual_s']:.2f} s); "
+                         f"sweep = {P}*t_update + t_residual = {det['sweep_s']:.1f} s",
+               "host_cores_available": os.cpu_count()}
+    clocks = clk.summary()
+    if rank == 0:
+        ws = 8.0 * info["rows_padded"] * 6 + 12.0 * (info["sell_residual"] + info["sell_local"])
+        line = {
+            "metric": "RAS iterations/s (aggregate subdomain updates/s)", "value": value, "unit": "updates/s",
+            "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(N, nx, ny, P, mode, ws),
+            "ras_iters_per_s": args.steps / (ms / 1e3),
+            "sweeps_done": sweeps,
+            "inner_iters_total": stats["inner_iters_total"],
+            "roofline": roof,
+            "pcg_path_gbs": pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms else None,
+            "kernels": kern,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": stats["kernel_launches"],
+            "setup_s": setup_s,
+            "tts": tts,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _solve_host(solver, x0, xo, mode):
+    import ctypes as C
+
+    from paper_2003_05361_b200 import _ffi as F
+
+    st = F.lib().ras_solve(solver._h, 1e-300, 1, F.RAS_SYNC if mode == "sync" else F.RAS_ASYNC,
+                           x0.ctypes.data_as(C.POINTER(C.c_double)), xo.ctypes.data_as(C.POINTER(C.c_double)))
+    if st not in (F.RAS_OK, F.RAS_ENOCONV):
+        raise RuntimeError(F.lib().ras_last_error(solver._h))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

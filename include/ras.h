@@ -202,6 +202,19 @@ ras_status ras_set_scripted_flags(ras_ctx* ctx, const uint8_t* flags, int64_t ns
 /* Per-subdomain stop sweep of the last scripted run (len local subdomains). */
 ras_status ras_detector_stops(const ras_ctx* ctx, int64_t* stop_out);
 
+/* Per-kernel CUDA-event timing on the library stream (for the roofline report).
+ * When enabled, every kernel launch of ras_solve* is bracketed by events; the
+ * totals of the last solve are returned per kernel kind. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double total_ms;          /* sum of event-measured launch durations */
+  double bytes_per_launch;  /* algorithmic HBM bytes of one launch */
+} ras_kernel_time_t;
+
+ras_status ras_kernel_timing(ras_ctx* ctx, int32_t enable);
+ras_status ras_kernel_times(const ras_ctx* ctx, ras_kernel_time_t* out, int32_t max_entries, int32_t* n_out);
+
 int32_t ras_abi_version(void);
 
 #ifdef __cplusplus

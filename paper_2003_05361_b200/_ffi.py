@@ -69,6 +69,10 @@ class RasPlanInfo(C.Structure):
                 ("reserved", I32)]
 
 
+class RasKernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", I64), ("total_ms", F64), ("bytes_per_launch", F64)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/*.h
 SIGNATURES = [
     ("ras_abi_version", I32, []),
@@ -87,6 +91,8 @@ SIGNATURES = [
     ("ras_nccl_unique_id", I32, [C.c_void_p]),
     ("ras_set_scripted_flags", I32, [C.c_void_p, P(U8), I64]),
     ("ras_detector_stops", I32, [C.c_void_p, P(I64)]),
+    ("ras_kernel_timing", I32, [C.c_void_p, I32]),
+    ("ras_kernel_times", I32, [C.c_void_p, P(RasKernelTime), I32, P(I32)]),
     # ras_plan.h
     ("ras_plan_build", I32, [P(C.c_void_p), P(RasCsr), P(F64), P(RasPartition), I32, I32, I32]),
     ("ras_plan_get_info", I32, [C.c_void_p, P(RasPlanInfo)]),

@@ -1,12 +1,670 @@
-// Asynchronous mode (PAPER §3.4 "Asynchronous Schwarz setup", P389-397) — placeholder,
-// replaced by the NVLink P2P implementation.
+// Asynchronous RAS (PAPER §2.1 P163-176, §3.3.2 P326-357, §3.4 P389-397).
+//
+// Every local subdomain runs its own sweep loop on its own CUDA stream with no
+// inter-subdomain ordering: residual (reading owner / halo storage as it
+// stands: "latest data"), Eq. 2 flag + convergence-detection step, PCG,
+// restricted prolongation, and — for values other GPUs need — a fused pack +
+// store straight into the peer GPU's halo storage over NVLink (CUDA IPC
+// mapping), followed by a system-scope release of a per-subdomain version
+// counter in the peer's board (the analogue of MPI_Put + flush, P394-396).
+// Nothing waits on anything: no barriers, no collectives in the loop.
+//
+// Termination (P331-357, readings R19/R20): level flags on a spanning tree of
+// the subdomain graph, stored as int32 words in every rank's "board" (peer
+// boards mapped through CUDA IPC):
+//   board[STOP + p]      stop word of subdomain p (written by tree neighbours)
+//   board[REP + e]       report on directed tree edge e (v->parent: 2v,
+//                        parent->v: 2v+1), written by the edge's sender
+//   board[VER + p]       puts received from subdomain p (freshness statistic)
+// centralized:   R_v = c_v AND (all children reports); the root stops when
+//                c_root AND all children; STOP floods down the tree.
+// decentralized: R_{v->u} = c_v AND (reports from all other tree neighbours);
+//                v declares when c_v AND all; STOP floods over the tree.
+// After every local subdomain stopped: barrier, halo refresh, true residual
+// (P346-348); if it fails, flags are cleared and iteration resumes (R20).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
 #include "ctx.h"
+#include "kernels.cuh"
+#include "plan_internal.h"
 
 namespace ras {
-ras_status async_setup(ras_ctx* c) { (void)c; return RAS_OK; }
-void async_free(ras_ctx* c) { (void)c; }
-ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
-  (void)tol; (void)max_iters;
-  return set_err(c, RAS_ESTATE, "async mode not built yet");
+
+struct DetDev {
+  int32_t P;
+  int32_t central;        // 1 = centralized tree, 0 = decentralized
+  const int32_t* gid;     // [nl] global id of local subdomain
+  const int32_t* nb_off;  // [nl+1] into nb arrays
+  const int32_t* nb;      // tree neighbours (global id)
+  const int32_t* nb_rank; // their rank
+  const int32_t* e_in;    // edge slot nb -> me
+  const int32_t* e_out;   // edge slot me -> nb
+  const int32_t* is_parent;  // nb is my parent (centralized)
+  const int32_t* is_root;    // [nl]
+  const double* b2;       // [nl] ||b~_p||^2 (Eq. 2) or owned-only variant
+  int32_t* const* boards; // [world] board base per rank (own + IPC-mapped peers)
+  int32_t my_rank;
+  int32_t owned_only;
+};
+
+struct AsyncRt {
+  std::vector<cudaStream_t> streams;
+  int32_t* board = nullptr;  // own board (raw cudaMalloc)
+  int32_t* board2 = nullptr; // scripted lock-step: second buffer
+  size_t board_words = 0;
+  std::vector<int32_t*> peer_board;
+  std::vector<double*> peer_x;
+  std::vector<void*> opened;
+  int32_t** d_boards = nullptr;
+  int32_t** d_boards2 = nullptr;
+  double** d_peer_x = nullptr;
+  DetDev det{};
+  std::vector<int32_t> h_gid;
+  int32_t* d_lstop = nullptr;
+  int32_t* h_lstop = nullptr;      // mapped pinned mirror
+  int32_t* h_active = nullptr;     // pinned (exact-mode polling)
+  int32_t* h_lstop_dev = nullptr;
+  int64_t* d_updates = nullptr;
+  int32_t* d_noconv = nullptr;
+  int64_t* d_stop_sweep = nullptr;
+  // put lists (per local subdomain p: entries [put_off[p], put_off[p+1]))
+  std::vector<int64_t> put_off;
+  int32_t* d_put_slot = nullptr;
+  int32_t* d_put_rank = nullptr;
+  int64_t* d_put_ridx = nullptr;   // index into the destination rank's storage
+  std::vector<int32_t> put_peer_off;  // per local sub: list of destination ranks
+  int32_t* d_put_peers = nullptr;
+  uint32_t* d_put_ticket = nullptr;
+  uint8_t* d_scripted = nullptr;
+  int64_t scripted_n = 0;
+};
+
+// ---------------------------------------------------------------------------
+// device helpers: system-scope release / acquire on 32-bit words
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One detection step of local subdomain lp (P331-357).  `in` is the board the
+// reports / stop words are read from, `out` the boards they are written to
+// (the same in true async mode; previous / next buffers in the scripted
+// lock-step mode).  Returns 1 if lp stops in this step.
+__device__ int det_step(const DetDev& D, int lp, int c, const int32_t* in, int32_t* const* out_boards) {
+  const int p = D.gid[lp];
+  const int a = D.nb_off[lp], b = D.nb_off[lp + 1];
+  int stop = ld_acquire_sys(in + p) != 0;  // STOP + p (offset 0)
+  const int32_t* rep = in + D.P;
+  int all_in = 1;
+  for (int i = a; i < b; ++i) {
+    if (D.central && D.is_parent[i]) continue;
+    all_in &= ld_acquire_sys(rep + D.e_in[i]) != 0;
+  }
+  if (D.central) {
+    const int R = c && all_in;
+    if (D.is_root[lp]) {
+      if (R) stop = 1;
+    } else {
+      for (int i = a; i < b; ++i)
+        if (D.is_parent[i]) st_release_sys(out_boards[D.nb_rank[i]] + D.P + D.e_out[i], R);
+    }
+    if (stop)
+      for (int i = a; i < b; ++i)
+        if (!D.is_parent[i]) st_release_sys(out_boards[D.nb_rank[i]] + D.nb[i], 1);
+  } else {
+    for (int i = a; i < b; ++i) {
+      int R = c;
+      for (int j = a; j < b; ++j)
+        if (j != i) R &= ld_acquire_sys(rep + D.e_in[j]) != 0;
+      st_release_sys(out_boards[D.nb_rank[i]] + D.P + D.e_out[i], R);
+    }
+    if (c && all_in) stop = 1;
+    if (stop)
+      for (int i = a; i < b; ++i) st_release_sys(out_boards[D.nb_rank[i]] + D.nb[i], 1);
+  }
+  return stop;
+}
+
+// Eq. 2 (P337-340): ||r~_p||^2 < tau^2 ||b~_p||^2 (||b~_p|| = 0: ||r~_p|| = 0, R11).
+__device__ __forceinline__ int local_flag(const DetDev& D, const Scal& S, int lp, double tol) {
+  const double r2 = D.owned_only ? S.own2[lp] : S.rt2[lp];
+  const double b2 = D.b2[lp];
+  return b2 == 0.0 ? (r2 == 0.0) : (r2 < tol * tol * b2);
+}
+
+// True async: one thread, after k_residual of subdomain lp on its stream.
+static __global__ void k_detect(int lp, DetDev D, Scal S, double tol, int64_t max_iters, int32_t* lstop,
+                                volatile int32_t* h_lstop, int64_t* updates, int32_t* noconv) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (lstop[lp]) return;
+  const int64_t u = ++updates[lp];
+  const int c = local_flag(D, S, lp, tol);
+  const int32_t* in = D.boards[D.my_rank];
+  // acquire: make the peers' released reports visible
+  (void)ld_acquire_sys(in + D.gid[lp]);
+  int stop = det_step(D, lp, c, in, D.boards);
+  if (!stop && u > max_iters) {
+    noconv[lp] = 1;
+    stop = 1;
+  }
+  if (stop) {
+    updates[lp] = u - 1;  // this sweep performs no update
+    lstop[lp] = 1;
+    h_lstop[lp] = 1;
+  }
+}
+
+// Scripted lock-step mode (test hook, SURVEY §8c "Detectors"): all local
+// subdomains step together; reports of sweep k-1 are read from `prev`,
+// sweep-k reports written to `next` (whose stop section was copied from prev).
+static __global__ void k_detect_scripted(int nl, int64_t k, DetDev D, const uint8_t* flags, int64_t nsweeps,
+                                         int32_t* const* prev, int32_t* const* next, int32_t* lstop,
+                                         int64_t* stop_sweep, int64_t* updates) {
+  const int lp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lp >= nl || lstop[lp]) return;
+  updates[lp] = k + 1;
+  const int64_t row = k < nsweeps ? k : nsweeps - 1;
+  const int c = flags[row * nl + lp] != 0;
+  if (det_step(D, lp, c, prev[D.my_rank], next)) {
+    lstop[lp] = 1;
+    stop_sweep[lp] = k;
+  }
+}
+
+// a5 (async): fused pack + NVLink store into the peer's halo storage, then
+// (last CTA) fence.sc.sys and a system-scope release increment of version[p]
+// in each destination rank's board (MPI_Put + flush analogue, P394-396).
+static __global__ void k_put(int lp, int64_t e0, int64_t e1, const int32_t* __restrict__ slot,
+                             const int32_t* __restrict__ rank, const int64_t* __restrict__ ridx,
+                             const double* __restrict__ x, double* const* peer_x, uint32_t* ticket,
+                             const int32_t* peers, int npeers, int32_t* const* boards, int P, int gp,
+                             const int32_t* lstop) {
+  if (lstop[lp]) return;
+  for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1; e += (int64_t)gridDim.x * blockDim.x)
+    peer_x[rank[e]][ridx[e]] = x[slot[e]];
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&ticket[lp], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < npeers; ++i) atomicAdd_system(boards[peers[i]] + 3 * P + gp, 1);
+    ticket[lp] = 0u;
+  }
+}
+
+static __global__ void k_mirror_stops(int nl, const int32_t* lstop, volatile int32_t* h) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nl) h[i] = lstop[i];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static ras_status barrier(ras_ctx* c) {
+  if (c->world == 1) return cudaDeviceSynchronize() == cudaSuccess ? RAS_OK : set_err(c, RAS_ECUDA, "sync");
+  RAS_CUDA(c, cudaDeviceSynchronize());
+  RAS_NCCL(c, ncclAllReduce(c->d_r2_global, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RAS_OK;
+}
+
+// subdomain adjacency (p ~ q iff p needs a value owned by q or vice versa),
+// assembled over all ranks with one NCCL sum
+static ras_status subdomain_graph(ras_ctx* c, std::vector<std::vector<int32_t>>& adj) {
+  const ras_plan* pl = c->plan;
+  const int P = pl->P;
+  std::vector<int32_t> M((size_t)P * P, 0);
+  for (const auto& S : pl->subs)
+    for (int32_t q : S.nbr_subs) M[(size_t)S.p * P + q] = 1;
+  if (c->world > 1) {
+    int32_t* d;
+    TRY(upload(c, &d, M));
+    RAS_NCCL(c, ncclAllReduce(d, d, M.size(), ncclInt32, ncclSum, c->nccl, c->stream));
+    RAS_CUDA(c, cudaMemcpyAsync(M.data(), d, M.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  adj.assign(P, {});
+  for (int p = 0; p < P; ++p)
+    for (int q = 0; q < P; ++q)
+      if (p != q && (M[(size_t)p * P + q] || M[(size_t)q * P + p])) adj[p].push_back(q);
+  return RAS_OK;
+}
+
+static std::vector<int32_t> bfs_tree(const std::vector<std::vector<int32_t>>& adj) {
+  const int P = (int)adj.size();
+  std::vector<int32_t> parent(P, -2);
+  parent[0] = -1;
+  std::vector<int32_t> q{0};
+  for (size_t h = 0; h < q.size(); ++h)
+    for (int w : adj[q[h]])
+      if (parent[w] == -2) {
+        parent[w] = q[h];
+        q.push_back(w);
+      }
+  // disconnected subdomain graph: hang remaining components under the root
+  for (int v = 0; v < P; ++v)
+    if (parent[v] == -2) parent[v] = 0;
+  return parent;
+}
+
+static std::vector<int32_t> central_tree(const std::vector<int32_t>& sub_to_rank) {
+  const int P = (int)sub_to_rank.size();
+  std::vector<int32_t> leader(*std::max_element(sub_to_rank.begin(), sub_to_rank.end()) + 1, -1), parent(P);
+  for (int p = 0; p < P; ++p)
+    if (leader[sub_to_rank[p]] < 0) leader[sub_to_rank[p]] = p;
+  for (int p = 0; p < P; ++p) {
+    const int L = leader[sub_to_rank[p]];
+    parent[p] = p == 0 ? -1 : (p == L ? 0 : L);
+  }
+  return parent;
+}
+
+static ras_status setup_ipc(ras_ctx* c, AsyncRt* A) {
+  const int W = c->world;
+  A->peer_board.assign(W, nullptr);
+  A->peer_x.assign(W, nullptr);
+  A->peer_board[c->rank] = A->board;
+  A->peer_x[c->rank] = c->d_x;
+  if (W == 1) return RAS_OK;
+  cudaIpcMemHandle_t h[2];
+  RAS_CUDA(c, cudaIpcGetMemHandle(&h[0], c->d_x));
+  RAS_CUDA(c, cudaIpcGetMemHandle(&h[1], A->board));
+  std::vector<char> mine(sizeof(h));
+  std::memcpy(mine.data(), h, sizeof(h));
+  char *d_mine, *d_all;
+  TRY(upload(c, &d_mine, mine));
+  TRY(zalloc(c, &d_all, sizeof(h) * W));
+  RAS_NCCL(c, ncclAllGather(d_mine, d_all, sizeof(h), ncclChar, c->nccl, c->stream));
+  std::vector<char> all(sizeof(h) * W);
+  RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < W; ++r) {
+    if (r == c->rank) continue;
+    cudaIpcMemHandle_t hr[2];
+    std::memcpy(hr, all.data() + r * sizeof(h), sizeof(h));
+    void *px = nullptr, *pb = nullptr;
+    RAS_CUDA(c, cudaIpcOpenMemHandle(&px, hr[0], cudaIpcMemLazyEnablePeerAccess));
+    A->opened.push_back(px);
+    RAS_CUDA(c, cudaIpcOpenMemHandle(&pb, hr[1], cudaIpcMemLazyEnablePeerAccess));
+    A->opened.push_back(pb);
+    A->peer_x[r] = (double*)px;
+    A->peer_board[r] = (int32_t*)pb;
+  }
+  return RAS_OK;
+}
+
+ras_status async_setup(ras_ctx* c) {
+  AsyncRt* A = new AsyncRt();
+  c->async = A;
+  ras_plan* pl = c->plan;
+  const int P = pl->P, nl = c->nl, W = c->world;
+  // boards: [STOP: P][REP: 2P][VER: P]
+  A->board_words = (size_t)4 * P + 64;
+  A->board = (int32_t*)dalloc_raw(c, A->board_words * 4);
+  A->board2 = (int32_t*)dalloc_raw(c, A->board_words * 4);
+  if (!A->board || !A->board2) return set_err(c, RAS_ENOMEM, "board allocation failed");
+  TRY(setup_ipc(c, A));
+  TRY(upload(c, &A->d_boards, A->peer_board));
+  std::vector<int32_t*> b2v(W, nullptr);
+  b2v[c->rank] = A->board2;  // scripted mode is single-rank
+  TRY(upload(c, &A->d_boards2, b2v));
+  TRY(upload(c, &A->d_peer_x, A->peer_x));
+  // trees
+  std::vector<std::vector<int32_t>> adj;
+  TRY(subdomain_graph(c, adj));
+  const std::vector<int32_t> par = c->opt.detector == RAS_DET_CENTRAL ? central_tree(pl->sub_to_rank) : bfs_tree(adj);
+  std::vector<int32_t> gid(nl), nb_off(nl + 1, 0), nb, nb_rank, e_in, e_out, is_par, is_root(nl);
+  std::vector<double> b2(nl);
+  for (int lp = 0; lp < nl; ++lp) {
+    const int p = pl->subs[lp].p;
+    gid[lp] = p;
+    is_root[lp] = par[p] == -1;
+    b2[lp] = c->opt.local_crit_owned_only ? pl->subs[lp].b2_owned : pl->subs[lp].b2;
+    auto add = [&](int u, bool up) {
+      nb.push_back(u);
+      nb_rank.push_back(pl->sub_to_rank[u]);
+      // edge v->parent(v): 2v ; parent(v)->v: 2v+1
+      e_in.push_back(up ? 2 * p + 1 : 2 * u);
+      e_out.push_back(up ? 2 * p : 2 * u + 1);
+      is_par.push_back(up ? 1 : 0);
+    };
+    if (par[p] >= 0) add(par[p], true);
+    for (int u = 0; u < P; ++u)
+      if (par[u] == p) add(u, false);
+    nb_off[lp + 1] = (int32_t)nb.size();
+  }
+  A->h_gid = gid;
+  DetDev& D = A->det;
+  D.P = P;
+  D.central = c->opt.detector == RAS_DET_CENTRAL;
+  D.my_rank = c->rank;
+  D.owned_only = c->opt.local_crit_owned_only;
+  int32_t *dg, *dno, *dnb, *dnr, *dei, *deo, *dip, *dir;
+  double* db2;
+  TRY(upload(c, &dg, gid));
+  TRY(upload(c, &dno, nb_off));
+  TRY(upload(c, &dnb, nb, 1));
+  TRY(upload(c, &dnr, nb_rank, 1));
+  TRY(upload(c, &dei, e_in, 1));
+  TRY(upload(c, &deo, e_out, 1));
+  TRY(upload(c, &dip, is_par, 1));
+  TRY(upload(c, &dir, is_root));
+  TRY(upload(c, &db2, b2));
+  D.gid = dg;
+  D.nb_off = dno;
+  D.nb = dnb;
+  D.nb_rank = dnr;
+  D.e_in = dei;
+  D.e_out = deo;
+  D.is_parent = dip;
+  D.is_root = dir;
+  D.b2 = db2;
+  D.boards = A->d_boards;
+  TRY(zalloc(c, &A->d_lstop, nl));
+  TRY(zalloc(c, &A->d_updates, nl));
+  TRY(zalloc(c, &A->d_noconv, nl));
+  TRY(zalloc(c, &A->d_stop_sweep, nl));
+  TRY(zalloc(c, &A->d_put_ticket, nl));
+  RAS_CUDA(c, cudaHostAlloc((void**)&A->h_lstop, std::max(nl, 1) * 4, cudaHostAllocMapped));
+  RAS_CUDA(c, cudaHostGetDevicePointer((void**)&A->h_lstop_dev, A->h_lstop, 0));
+  RAS_CUDA(c, cudaHostAlloc((void**)&A->h_active, std::max(nl, 1) * 4, cudaHostAllocDefault));
+  // put lists: entries of the send lists whose source slot belongs to local p
+  std::vector<int64_t> n_own_all(W, 0);
+  n_own_all[c->rank] = c->n_own;
+  if (W > 1) {
+    int64_t* d;
+    TRY(upload(c, &d, n_own_all));
+    RAS_NCCL(c, ncclAllReduce(d, d, W, ncclInt64, ncclSum, c->nccl, c->stream));
+    RAS_CUDA(c, cudaMemcpyAsync(n_own_all.data(), d, W * 8, cudaMemcpyDeviceToHost, c->stream));
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  std::vector<int32_t> ps, pr, peers;
+  std::vector<int64_t> pi;
+  A->put_off.assign(nl + 1, 0);
+  A->put_peer_off.assign(nl + 1, 0);
+  for (int lp = 0; lp < nl; ++lp) {
+    const auto& S = pl->subs[lp];
+    for (int q = 0; q < W; ++q) {
+      bool any = false;
+      for (size_t i = 0; i < pl->send_slot[q].size(); ++i) {
+        const int32_t s = pl->send_slot[q][i];
+        if (s >= S.own_off && s < S.own_off + S.nown) {
+          ps.push_back(s);
+          pr.push_back(q);
+          pi.push_back(n_own_all[q] + pl->send_remote_off[q] + (int64_t)i);
+          any = true;
+        }
+      }
+      if (any) peers.push_back(q);
+    }
+    A->put_off[lp + 1] = (int64_t)ps.size();
+    A->put_peer_off[lp + 1] = (int32_t)peers.size();
+  }
+  TRY(upload(c, &A->d_put_slot, ps, 1));
+  TRY(upload(c, &A->d_put_rank, pr, 1));
+  TRY(upload(c, &A->d_put_ridx, pi, 1));
+  TRY(upload(c, &A->d_put_peers, peers, 1));
+  A->streams.resize(nl);
+  for (auto& s : A->streams) RAS_CUDA(c, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return RAS_OK;
+}
+
+void async_free(ras_ctx* c) {
+  AsyncRt* A = c->async;
+  if (!A) return;
+  for (auto s : A->streams) cudaStreamDestroy(s);
+  for (void* p : A->opened) cudaIpcCloseMemHandle(p);
+  if (A->h_lstop) cudaFreeHost(A->h_lstop);
+  if (A->h_active) cudaFreeHost(A->h_active);
+  delete A;
+  c->async = nullptr;
+}
+
+static ras_status reset_detection(ras_ctx* c) {
+  AsyncRt* A = c->async;
+  RAS_CUDA(c, cudaMemsetAsync(A->board, 0, A->board_words * 4, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(A->board2, 0, A->board_words * 4, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(A->d_lstop, 0, c->nl * 4, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(A->d_noconv, 0, c->nl * 4, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(A->d_put_ticket, 0, c->nl * 4, c->stream));
+  for (int i = 0; i < c->nl; ++i) A->h_lstop[i] = 0;
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  return barrier(c);  // every rank cleared its board before anyone writes again
+}
+
+// one sweep of local subdomain lp on stream s (true async)
+static ras_status enqueue_sub_sweep(ras_ctx* c, int lp, cudaStream_t s, double tol, int64_t max_iters, int m,
+                                    double inner_tol, bool exact) {
+  AsyncRt* A = c->async;
+  const ras_plan* pl = c->plan;
+  const auto& SP = pl->subs[lp];
+  const int64_t tb = SP.tile_begin;
+  const unsigned g = (unsigned)SP.ntiles;
+  Ctl C{A->d_lstop, 1};
+  k_residual<<<g, kThreads, 0, s>>>(tb, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x, c->d_r, c->d_p, c->S,
+                                    C);
+  k_detect<<<1, 32, 0, s>>>(lp, A->det, c->S, tol, max_iters, A->d_lstop, A->h_lstop_dev, A->d_updates,
+                            A->d_noconv);
+  c->launches += 2;
+  for (int it = 1; it <= m; ++it) {
+    k_spmv_dot<<<g, kThreads, 0, s>>>(tb, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C);
+    k_update_dot<<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d, c->S, C, m, inner_tol);
+    c->launches += 2;
+    if (it < m) {
+      k_pupdate<<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_r, c->d_p, c->S, C);
+      c->launches += 1;
+    }
+    if (exact && it % 16 == 0) {  // exact mode: stop enqueuing once this subdomain's PCG finished
+      RAS_CUDA(c, cudaMemcpyAsync(A->h_active + lp, c->S.active + lp, 4, cudaMemcpyDeviceToHost, s));
+      RAS_CUDA(c, cudaStreamSynchronize(s));
+      if (((volatile int32_t*)A->h_active)[lp] == 0) break;
+    }
+  }
+  k_prolong<<<g, kThreads, 0, s>>>(tb, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C);
+  c->launches += 1;
+  const int64_t e0 = A->put_off[lp], e1 = A->put_off[lp + 1];
+  if (e1 > e0) {
+    const unsigned pg = (unsigned)std::min<int64_t>((e1 - e0 + 255) / 256, 148 * 4);
+    k_put<<<pg, 256, 0, s>>>(lp, e0, e1, A->d_put_slot, A->d_put_rank, A->d_put_ridx, c->d_x, A->d_peer_x,
+                             A->d_put_ticket, A->d_put_peers + A->put_peer_off[lp],
+                             A->put_peer_off[lp + 1] - A->put_peer_off[lp], A->d_boards, pl->P, SP.p, A->d_lstop);
+    c->launches += 1;
+  }
+  return RAS_OK;
+}
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// true async loop on this rank: per-subdomain streams, host keeps <= Q sweeps
+// in flight per stream, exits when every local subdomain stopped
+static ras_status run_async_loop(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact,
+                                 bool* timeout) {
+  AsyncRt* A = c->async;
+  const int nl = c->nl;
+  const int Q = 2;
+  std::vector<std::vector<cudaEvent_t>> ev(nl, std::vector<cudaEvent_t>(Q));
+  for (auto& v : ev)
+    for (auto& e : v) RAS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  std::vector<int64_t> enq(nl, 0);
+  const double t0 = now_s();
+  *timeout = false;
+  ras_status st = RAS_OK;
+  for (;;) {
+    int nstopped = 0;
+    bool progressed = false;
+    for (int lp = 0; lp < nl; ++lp) {
+      if (((volatile int32_t*)A->h_lstop)[lp]) {
+        ++nstopped;
+        continue;
+      }
+      if (enq[lp] >= Q && cudaEventQuery(ev[lp][enq[lp] % Q]) == cudaErrorNotReady) continue;
+      st = enqueue_sub_sweep(c, lp, A->streams[lp], tol, max_iters, m, inner_tol, exact);
+      if (st != RAS_OK) break;
+      RAS_CUDA(c, cudaEventRecord(ev[lp][enq[lp] % Q], A->streams[lp]));
+      ++enq[lp];
+      progressed = true;
+    }
+    if (st != RAS_OK || nstopped == nl) break;
+    if (now_s() - t0 > c->opt.async_timeout_s) {
+      *timeout = true;
+      break;
+    }
+    if (!progressed) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      st = cuda_err(c, e, "async sweep");
+      break;
+    }
+  }
+  if (*timeout) {  // watchdog: stop every local subdomain from the host
+    std::vector<int32_t> ones(nl, 1);
+    cudaMemcpy(A->d_lstop, ones.data(), nl * 4, cudaMemcpyHostToDevice);
+  }
+  cudaDeviceSynchronize();
+  for (auto& v : ev)
+    for (auto& e : v) cudaEventDestroy(e);
+  return st;
+}
+
+// scripted lock-step mode (single rank): deterministic detector schedule
+static ras_status run_scripted(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol) {
+  AsyncRt* A = c->async;
+  const int nl = c->nl;
+  if (c->world != 1) return set_err(c, RAS_EINVAL, "scripted detector mode needs world == 1");
+  if (c->scripted_sweeps <= 0) return set_err(c, RAS_EINVAL, "no scripted flags set");
+  if (A->scripted_n != c->scripted_sweeps) {
+    TRY(upload(c, &A->d_scripted, c->scripted));
+    A->scripted_n = c->scripted_sweeps;
+  }
+  RAS_CUDA(c, cudaMemsetAsync(A->d_stop_sweep, 0xff, nl * 8, c->stream));
+  const unsigned g = (unsigned)c->ntiles;
+  Ctl C{A->d_lstop, 1};
+  int32_t** bufs[2] = {A->d_boards, A->d_boards2};
+  int32_t* raw[2] = {A->board, A->board2};
+  for (int64_t k = 0; k < max_iters; ++k) {
+    const int cur = (int)(k & 1), prv = cur ^ 1;
+    // stop words persist: next <- prev (stop section); reports are rewritten
+    RAS_CUDA(c, cudaMemcpyAsync(raw[cur], raw[prv], (size_t)c->plan->P * 4, cudaMemcpyDeviceToDevice, c->stream));
+    k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x, c->d_r,
+                                              c->d_p, c->S, C);
+    k_detect_scripted<<<(nl + 127) / 128, 128, 0, c->stream>>>(nl, k, A->det, A->d_scripted, c->scripted_sweeps,
+                                                                bufs[prv], bufs[cur], A->d_lstop, A->d_stop_sweep,
+                                                                A->d_updates);
+    for (int it = 1; it <= m; ++it) {
+      k_spmv_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C);
+      k_update_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d, c->S, C, m,
+                                                  inner_tol);
+      if (it < m) k_pupdate<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_r, c->d_p, c->S, C);
+    }
+    k_prolong<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C);
+    k_mirror_stops<<<(nl + 127) / 128, 128, 0, c->stream>>>(nl, A->d_lstop, A->h_lstop_dev);
+    c->launches += 4 + 3 * m;
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+    int all = 1;
+    for (int i = 0; i < nl; ++i) all &= ((volatile int32_t*)A->h_lstop)[i] != 0;
+    if (all) break;
+  }
+  RAS_CUDA(c, cudaGetLastError());
+  (void)tol;
+  return RAS_OK;
+}
+
+ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
+  AsyncRt* A = c->async;
+  const int nl = c->nl;
+  const bool exact = c->opt.local_solver == RAS_LS_EXACT_PCG;
+  int64_t max_rows = 0;
+  for (auto& S : c->plan->subs) max_rows = std::max<int64_t>(max_rows, (int64_t)S.omega.size());
+  const int m = exact ? (int)std::min<int64_t>(10 * max_rows, INT32_MAX / 2) : c->opt.inner_iters;
+  const double inner_tol = exact ? 1e-14 : c->opt.inner_tol;
+  const bool kt = c->kt.on;
+  c->kt.on = false;  // per-kernel event timing is a sync-mode (single stream) facility
+  RAS_CUDA(c, cudaMemsetAsync(A->d_updates, 0, nl * 8, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  ras_status st = RAS_OK;
+  double rel = INFINITY;
+  int resumes = 0;
+  bool noconv_any = false, timeout = false;
+  const double t0 = now_s();
+  for (;;) {
+    TRY(reset_detection(c));
+    if (c->opt.scripted_flags) {
+      st = run_scripted(c, tol, max_iters, m, inner_tol);
+    } else {
+      st = run_async_loop(c, tol, max_iters, m, inner_tol, exact, &timeout);
+    }
+    if (st != RAS_OK) break;
+    c->st.time_to_solution_s = now_s() - t0;
+    // post-termination verification (P346-348): barrier, halo refresh, true residual
+    const double tv = now_s();
+    TRY(barrier(c));
+    TRY(sync_exchange(c));
+    TRY(global_residual(c, &rel));
+    c->st.verify_s += now_s() - tv;
+    std::vector<int32_t> nc(nl);
+    RAS_CUDA(c, cudaMemcpy(nc.data(), A->d_noconv, nl * 4, cudaMemcpyDeviceToHost));
+    int local_nc = 0;
+    for (int v : nc) local_nc |= v;
+    noconv_any = local_nc || timeout;
+    if (c->world > 1) {  // agree on "someone hit max_iters / the watchdog"
+      double f = noconv_any ? 1.0 : 0.0;
+      RAS_CUDA(c, cudaMemcpy(c->d_r2_global, &f, 8, cudaMemcpyHostToDevice));
+      RAS_NCCL(c, ncclAllReduce(c->d_r2_global, c->d_r2_global, 1, ncclDouble, ncclMax, c->nccl, c->stream));
+      RAS_CUDA(c, cudaMemcpyAsync(&f, c->d_r2_global, 8, cudaMemcpyDeviceToHost, c->stream));
+      RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+      noconv_any = f != 0.0;
+    }
+    if (rel < tol || noconv_any || c->opt.scripted_flags || resumes >= c->opt.max_resumes) break;
+    ++resumes;  // R20: verification failed -> clear flags and resume asynchronous iteration
+  }
+  c->kt.on = kt;
+  if (st != RAS_OK) return st;
+  c->st.resumes = resumes;
+  c->st.final_rel_residual = rel;
+  c->st.converged = rel < tol;
+  c->st.verified = rel < tol;
+  std::vector<int64_t> up(nl);
+  RAS_CUDA(c, cudaMemcpy(up.data(), A->d_updates, nl * 8, cudaMemcpyDeviceToHost));
+  c->updates = up;
+  std::vector<int64_t> srt = up;
+  std::sort(srt.begin(), srt.end());
+  c->st.updates_min = srt.front();
+  c->st.updates_max = srt.back();
+  c->st.updates_median = srt[srt.size() / 2];
+  c->st.sweeps = srt.back();
+  if (c->opt.scripted_flags) {
+    c->det_stops.resize(nl);
+    RAS_CUDA(c, cudaMemcpy(c->det_stops.data(), A->d_stop_sweep, nl * 8, cudaMemcpyDeviceToHost));
+  }
+  std::vector<int32_t> ver(c->plan->P);
+  RAS_CUDA(c, cudaMemcpy(ver.data(), A->board + 3 * c->plan->P, ver.size() * 4, cudaMemcpyDeviceToHost));
+  int64_t fresh = 0;
+  for (int v : ver) fresh += v;
+  c->st.fresh_halo_reads = fresh;
+  if (c->st.converged) return RAS_OK;
+  if (noconv_any || c->opt.scripted_flags) return RAS_ENOCONV;
+  return set_err(c, RAS_EVERIFY,
+                 "async RAS terminated but the true relative residual " + std::to_string(rel) +
+                     " >= tol after " + std::to_string(resumes) + " resumes");
+}
+
 }  // namespace ras

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -17,9 +18,21 @@ namespace ras {
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  bool raw = false;  // cudaMalloc'd IPC-capable window (never through the allocator hook)
 };
 
 struct AsyncRt;  // async-mode runtime (async.cu)
+
+enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_NKINDS };
+
+struct KTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<int32_t> kind;  // per recorded pair
+  size_t used = 0;            // events used in this solve
+  double total_ms[K_NKINDS] = {};
+  int64_t count[K_NKINDS] = {};
+};
 
 struct ModelBytes {  // algorithmic bytes per launch over the whole row space
   double residual, spmv_dot, update_dot, pupdate, prolong, pack;
@@ -81,6 +94,11 @@ struct ras_ctx {
   std::vector<int64_t> det_stops;
   ras::ModelBytes mb{};
   int64_t launches = 0;
+  ras::KTimer kt;
+  // device copies of the storage gids (x0 scatter / x_out gather on device)
+  int32_t* d_own_gid = nullptr;
+  int32_t* d_halo_gid = nullptr;
+  double* d_xglob = nullptr;  // len n, allocated on first host-buffer solve
 
   std::vector<uint8_t> scripted;
   int64_t scripted_sweeps = 0;
@@ -90,9 +108,43 @@ namespace ras {
 ras_status set_err(ras_ctx* c, ras_status s, const std::string& m);
 ras_status cuda_err(ras_ctx* c, cudaError_t e, const char* what);
 void* dalloc(ras_ctx* c, size_t bytes);
+void* dalloc_raw(ras_ctx* c, size_t bytes);
 ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters);
+int kt_begin(ras_ctx* c);
+void kt_end(ras_ctx* c, int kind, int idx);
 ras_status async_setup(ras_ctx* c);
 void async_free(ras_ctx* c);
+}  // namespace ras
+
+#define TRY(x)                   \
+  do {                           \
+    ras_status s_ = (x);         \
+    if (s_ != RAS_OK) return s_; \
+  } while (0)
+
+namespace ras {
+template <class T>
+inline ras_status upload(ras_ctx* c, T** dst, const std::vector<T>& src, size_t min_elems = 0) {
+  size_t n = std::max(src.size(), min_elems);
+  *dst = (T*)dalloc(c, n * sizeof(T));
+  if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
+  if (!src.empty() && cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_err(c, RAS_ECUDA, "cudaMemcpy (upload) failed");
+  return RAS_OK;
+}
+
+template <class T>
+inline ras_status zalloc(ras_ctx* c, T** dst, size_t n) {
+  *dst = (T*)dalloc(c, n * sizeof(T));
+  if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
+  if (cudaMemset(*dst, 0, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess)
+    return set_err(c, RAS_ECUDA, "cudaMemset failed");
+  return RAS_OK;
+}
+
+// shared between the sync and async drivers (solver.cu)
+ras_status sync_exchange(ras_ctx* c);                 // pack + NCCL send/recv into halo (a5, sync)
+ras_status global_residual(ras_ctx* c, double* rel);  // true ||b - A x|| / ||b|| of the stored x
 }  // namespace ras
 
 #define RAS_CUDA(c, expr)                                         \

@@ -5,8 +5,10 @@
 // concatenated into one padded "row space"; matrices are SELL-32 (slice = 32
 // consecutive rows stored column-major, so lane i of a warp reads entry k of
 // row i at base + 32k + i: one coalesced 256 B value load + 128 B index load
-// per k).  A CTA processes one TILE of rows that never straddles subdomains;
-// per-subdomain dot products are reduced deterministically: every CTA writes
+// per k).  A CTA (256 threads) processes one TILE of kRPT*256 rows that never
+// straddles subdomains; every thread owns kRPT rows (row0 + j*256 + tid) and
+// issues all their loads before using any (memory-level parallelism).
+// Per-subdomain dot products are reduced deterministically: every CTA writes
 // its partial, the last CTA of the subdomain (atomic ticket) sums the partials
 // in fixed order and applies the PCG scalar update.
 #pragma once
@@ -15,13 +17,14 @@
 
 namespace ras {
 
-constexpr int kThreads = 256;  // = TILE rows: one 32-row slice per warp
-constexpr int kNP = 4;         // partial slots per tile
+constexpr int kThreads = 256;
+constexpr int kRPT = 4;                     // rows per thread
+constexpr int kTileRows = kThreads * kRPT;  // rows per CTA tile (plan tile_rows)
+constexpr int kNP = 4;                      // partial slots per tile
+constexpr int kMaxW = 8;                    // unrolled SELL width (wider slices take the loop path)
 
 struct Tiles {
-  const int32_t* tile_sub;
-  const int64_t* tile_row0;
-  const int32_t* tile_nrows;
+  const int4* tile;               // {row0, nrows, local subdomain, 0}
   const int64_t* sub_tile_begin;  // per local subdomain
   const int32_t* sub_ntiles;
 };
@@ -32,7 +35,7 @@ struct Sell {
   const double* val;
 };
 
-// Per local subdomain scalars (struct of arrays, one allocation).
+// Per local subdomain scalars (struct of arrays, one allocation each).
 struct Scal {
   double* rt2;     // ||r~_p||^2 over Omega_p (Eq. 2 numerator, inner stop)
   double* rho;     // r.z
@@ -47,9 +50,16 @@ struct Scal {
   double* partials;  // ntiles * kNP
 };
 
+// Stop control: sync = one global word (per_sub = 0); async = one word per
+// local subdomain (per_sub = 1).
 struct Ctl {
-  volatile int32_t* stop;  // sync: global stop flag (device); nullptr in async
+  const volatile int32_t* stop;
+  int32_t per_sub;
 };
+
+__device__ __forceinline__ bool stopped(const Ctl& C, int lp) {
+  return C.stop && C.stop[C.per_sub ? lp : 0];
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -111,15 +121,31 @@ __device__ __forceinline__ void reduce_sub_partials(double (&out)[NV], int lp, c
   block_sum<NV>(out, sh);
 }
 
+// Sum_k val[e_k] * x[col[e_k]] over SELL-32 row `row` (entries in ascending
+// column order as stored).  Matrix data is streamed with evict-first loads so
+// the gathered vector keeps its L2 lines.
 __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const double* __restrict__ x) {
   const int64_t s = row >> 5;
   const int lane = (int)(row & 31);
-  const int64_t base = M.sptr[s];
-  const int w = (int)((M.sptr[s + 1] - base) >> 5);
+  const int64_t base = __ldg(&M.sptr[s]);
+  const int w = (int)((__ldg(&M.sptr[s + 1]) - base) >> 5);
+  const double* vp = M.val + base + lane;
+  const int32_t* cp = M.col + base + lane;
   double acc = 0.0;
-  for (int k = 0; k < w; ++k) {
-    const int64_t e = base + (int64_t)k * 32 + lane;
-    acc += __ldg(&M.val[e]) * __ldg(&x[__ldg(&M.col[e])]);
+  if (w <= kMaxW) {
+    double v[kMaxW];
+    int32_t c[kMaxW];
+#pragma unroll
+    for (int k = 0; k < kMaxW; ++k)
+      if (k < w) {
+        v[k] = __ldcs(vp + 32 * k);
+        c[k] = __ldcs(cp + 32 * k);
+      }
+#pragma unroll
+    for (int k = 0; k < kMaxW; ++k)
+      if (k < w) acc += v[k] * __ldg(&x[c[k]]);
+  } else {
+    for (int k = 0; k < w; ++k) acc += __ldcs(vp + 32 * k) * __ldg(&x[__ldcs(cp + 32 * k)]);
   }
   return acc;
 }
@@ -129,25 +155,48 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
 //   r = b~ - [A_p|B_p] x (x read in place from owned/halo storage: restrict),
 //   z = D^-1 r, p = z; partials: rho = r.z, ||r~||^2, owned ||r~||^2.
 // ---------------------------------------------------------------------------
-static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base, Tiles T, Sell R, const double* __restrict__ b,
-                                                       const double* __restrict__ diag,
-                                                       const int32_t* __restrict__ own_slot,
-                                                       const double* __restrict__ x, double* __restrict__ r,
-                                                       double* __restrict__ p, Scal S, Ctl C) {
+static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base, Tiles T, Sell R,
+                                                              const double* __restrict__ b,
+                                                              const double* __restrict__ diag,
+                                                              const int32_t* __restrict__ own_slot,
+                                                              const double* __restrict__ x, double* __restrict__ r,
+                                                              double* __restrict__ p, Scal S, Ctl C) {
   __shared__ double sh[3][kThreads / 32];
-  if (C.stop && *C.stop) return;
   const int64_t t = tile_base + blockIdx.x;
-  const int lp = T.tile_sub[t];
-  const int64_t row = T.tile_row0[t] + threadIdx.x;
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp)) return;
   double v[3] = {0.0, 0.0, 0.0};
-  if ((int)threadIdx.x < T.tile_nrows[t]) {
-    const double ri = __ldg(&b[row]) - sell_dot(R, row, x);
-    const double zi = __drcp_rn(__ldg(&diag[row])) * ri;
-    r[row] = ri;
-    p[row] = zi;
-    v[0] = ri * zi;
-    v[1] = ri * ri;
-    v[2] = __ldg(&own_slot[row]) >= 0 ? ri * ri : 0.0;
+  double bi[kRPT], di[kRPT], ax[kRPT];
+  int32_t os[kRPT];
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      bi[j] = __ldcs(&b[row]);
+      di[j] = __ldcs(&diag[row]);
+      os[j] = __ldcs(&own_slot[row]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) ax[j] = sell_dot(R, ti.x + lr, x);
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      const double ri = bi[j] - ax[j];
+      const double zi = __drcp_rn(di[j]) * ri;
+      r[row] = ri;
+      p[row] = zi;
+      v[0] += ri * zi;
+      v[1] += ri * ri;
+      v[2] += os[j] >= 0 ? ri * ri : 0.0;
+    }
   }
   block_sum<3>(v, sh);
   if (tile_partials_last<3>(v, t, lp, T, S)) {
@@ -167,20 +216,38 @@ static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base,
 
 // a3 pass 1: q = A_p p (diag + SELL off-diagonal), sigma = p.q; last CTA: alpha.
 static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base, Tiles T, Sell L,
-                                                       const double* __restrict__ diag, const double* __restrict__ p,
-                                                       double* __restrict__ q, Scal S, Ctl C) {
+                                                              const double* __restrict__ diag,
+                                                              const double* __restrict__ p, double* __restrict__ q,
+                                                              Scal S, Ctl C) {
   __shared__ double sh[1][kThreads / 32];
-  if (C.stop && *C.stop) return;
   const int64_t t = tile_base + blockIdx.x;
-  const int lp = T.tile_sub[t];
-  if (!S.active[lp]) return;
-  const int64_t row = T.tile_row0[t] + threadIdx.x;
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp) || !S.active[lp]) return;
   double v[1] = {0.0};
-  if ((int)threadIdx.x < T.tile_nrows[t]) {
-    const double pi = __ldg(&p[row]);
-    const double qi = __ldg(&diag[row]) * pi + sell_dot(L, row, p);
-    q[row] = qi;
-    v[0] = pi * qi;
+  double pi[kRPT], di[kRPT], ax[kRPT];
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      pi[j] = __ldg(&p[row]);
+      di[j] = __ldcs(&diag[row]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) ax[j] = sell_dot(L, ti.x + lr, p);
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const double qi = di[j] * pi[j] + ax[j];
+      q[ti.x + lr] = qi;
+      v[0] += pi[j] * qi;
+    }
   }
   block_sum<1>(v, sh);
   if (tile_partials_last<1>(v, t, lp, T, S)) {
@@ -203,28 +270,46 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base,
 
 // a3 pass 2: d += alpha p (d = alpha p on the first iteration), r -= alpha q,
 // z = D^-1 r; partials r.z, r.r; last CTA: inner stop test, beta, rho.
-static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T, const double* __restrict__ diag,
-                                                         const double* __restrict__ p, const double* __restrict__ q,
-                                                         double* __restrict__ r, double* __restrict__ d, Scal S,
-                                                         Ctl C, int32_t m, double inner_tol) {
+static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T,
+                                                                const double* __restrict__ diag,
+                                                                const double* __restrict__ p,
+                                                                const double* __restrict__ q, double* __restrict__ r,
+                                                                double* __restrict__ d, Scal S, Ctl C, int32_t m,
+                                                                double inner_tol) {
   __shared__ double sh[2][kThreads / 32];
-  if (C.stop && *C.stop) return;
   const int64_t t = tile_base + blockIdx.x;
-  const int lp = T.tile_sub[t];
-  if (!S.active[lp]) return;
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp) || !S.active[lp]) return;
   const double alpha = S.alpha[lp];
   const bool first = S.its[lp] == 1;
-  const int64_t row = T.tile_row0[t] + threadIdx.x;
   double v[2] = {0.0, 0.0};
-  if ((int)threadIdx.x < T.tile_nrows[t]) {
-    const double pi = __ldg(&p[row]);
-    const double di = first ? alpha * pi : d[row] + alpha * pi;
-    const double ri = r[row] - alpha * __ldg(&q[row]);
-    d[row] = di;
-    r[row] = ri;
-    const double zi = __drcp_rn(__ldg(&diag[row])) * ri;
-    v[0] = ri * zi;
-    v[1] = ri * ri;
+  double pi[kRPT], qi[kRPT], ri[kRPT], di[kRPT], gi[kRPT];
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      pi[j] = __ldcs(&p[row]);
+      qi[j] = __ldcs(&q[row]);
+      ri[j] = __ldcs(&r[row]);
+      gi[j] = __ldcs(&diag[row]);
+      di[j] = first ? 0.0 : __ldcs(&d[row]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      const double dn = first ? alpha * pi[j] : di[j] + alpha * pi[j];
+      const double rn = ri[j] - alpha * qi[j];
+      d[row] = dn;
+      r[row] = rn;
+      const double zi = __drcp_rn(gi[j]) * rn;
+      v[0] += rn * zi;
+      v[1] += rn * rn;
+    }
   }
   block_sum<2>(v, sh);
   if (tile_partials_last<2>(v, t, lp, T, S)) {
@@ -246,40 +331,57 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
 }
 
 // a3 pass 3: p = D^-1 r + beta p.
-static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, Tiles T, const double* __restrict__ diag,
-                                                      const double* __restrict__ r, double* __restrict__ p, Scal S,
-                                                      Ctl C) {
-  if (C.stop && *C.stop) return;
+static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, Tiles T,
+                                                             const double* __restrict__ diag,
+                                                             const double* __restrict__ r, double* __restrict__ p,
+                                                             Scal S, Ctl C) {
   const int64_t t = tile_base + blockIdx.x;
-  const int lp = T.tile_sub[t];
-  if (!S.active[lp]) return;
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp) || !S.active[lp]) return;
   const double beta = S.beta[lp];
-  const int64_t row = T.tile_row0[t] + threadIdx.x;
-  if ((int)threadIdx.x < T.tile_nrows[t]) {
-    const double zi = __drcp_rn(__ldg(&diag[row])) * __ldg(&r[row]);
-    p[row] = zi + beta * p[row];
+  double gi[kRPT], ri[kRPT], pi[kRPT];
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      gi[j] = __ldcs(&diag[row]);
+      ri[j] = __ldcs(&r[row]);
+      pi[j] = __ldcs(&p[row]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) p[ti.x + lr] = __drcp_rn(gi[j]) * ri[j] + beta * pi[j];
   }
 }
 
 // a4: restricted prolongation x[S_p] += d[S_p] (overlap part of d discarded).
-static __global__ void __launch_bounds__(kThreads) k_prolong(int64_t tile_base, Tiles T, const int32_t* __restrict__ own_slot,
-                                                      const double* __restrict__ d, double* __restrict__ x, Scal S,
-                                                      Ctl C) {
-  if (C.stop && *C.stop) return;
+static __global__ void __launch_bounds__(kThreads) k_prolong(int64_t tile_base, Tiles T,
+                                                             const int32_t* __restrict__ own_slot,
+                                                             const double* __restrict__ d, double* __restrict__ x,
+                                                             Scal S, Ctl C) {
   const int64_t t = tile_base + blockIdx.x;
-  const int lp = T.tile_sub[t];
-  if (S.its[lp] == 0) return;  // no PCG step taken: d == 0
-  const int64_t row = T.tile_row0[t] + threadIdx.x;
-  if ((int)threadIdx.x < T.tile_nrows[t]) {
-    const int32_t s = __ldg(&own_slot[row]);
-    if (s >= 0) x[s] = x[s] + __ldg(&d[row]);
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp) || S.its[lp] == 0) return;  // no PCG step taken: d == 0
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      const int32_t s = __ldcs(&own_slot[row]);
+      if (s >= 0) x[s] = x[s] + __ldcs(&d[row]);
+    }
   }
 }
 
 // a5 (sync): pack owned values for the NCCL sends.
 static __global__ void k_pack(int64_t count, const int32_t* __restrict__ slots, const double* __restrict__ x,
-                       double* __restrict__ out, Ctl C) {
-  if (C.stop && *C.stop) return;
+                              double* __restrict__ out, Ctl C) {
+  if (stopped(C, 0)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = x[__ldg(&slots[i])];
 }
@@ -300,23 +402,25 @@ struct SyncState {
   double rel;       // relative residual of x^k
 };
 
-static __global__ void k_sync_check(const double* __restrict__ r2_global, double b2_global, double tol, int64_t max_iters,
-                             SyncState* st, int32_t* stop_flag, volatile int32_t* host_stop) {
+static __global__ void k_sync_check(const double* __restrict__ r2_global, double b2_global, double tol,
+                                    int64_t max_iters, SyncState* st, int32_t* stop_flag,
+                                    volatile int32_t* host_stop) {
   if (threadIdx.x || blockIdx.x) return;
-  if (st->stop) return;
-  const double r2 = *r2_global;
-  const double rel = b2_global > 0.0 ? sqrt(r2) / sqrt(b2_global) : (r2 == 0.0 ? 0.0 : INFINITY);
-  st->rel = rel;
-  const bool conv = b2_global > 0.0 ? (rel < tol) : (r2 == 0.0);
-  if (conv) {
-    st->stop = 1;
-    st->converged = 1;
-  } else if (st->sweeps >= max_iters) {
-    st->stop = 1;
-  } else {
-    st->sweeps += 1;
+  if (!st->stop) {
+    const double r2 = *r2_global;
+    const double rel = b2_global > 0.0 ? sqrt(r2) / sqrt(b2_global) : (r2 == 0.0 ? 0.0 : INFINITY);
+    st->rel = rel;
+    const bool conv = b2_global > 0.0 ? (rel < tol) : (r2 == 0.0);
+    if (conv) {
+      st->stop = 1;
+      st->converged = 1;
+    } else if (st->sweeps >= max_iters) {
+      st->stop = 1;
+    } else {
+      st->sweeps += 1;
+    }
+    if (st->stop) *stop_flag = 1;
   }
-  if (st->stop) *stop_flag = 1;
   if (host_stop) *host_stop = st->stop;  // mapped pinned ring slot of this sweep
 }
 
@@ -325,6 +429,22 @@ static __global__ void k_count_active(int nl, const int32_t* __restrict__ active
   int c = 0;
   for (int i = 0; i < nl; ++i) c += active[i] != 0;
   *out = c;
+}
+
+// x0 (global order, device copy of the caller's host buffer) -> storage order
+static __global__ void k_scatter_x0(int64_t n_own, int64_t n_halo, const int32_t* __restrict__ own_gid,
+                                    const int32_t* __restrict__ halo_gid, const double* __restrict__ xg,
+                                    double* __restrict__ x) {
+  const int64_t tot = n_own + n_halo;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = i < n_own ? xg[own_gid[i]] : xg[halo_gid[i - n_own]];
+}
+
+// owned storage -> global order (x_out gather, P242)
+static __global__ void k_gather_x(int64_t n_own, const int32_t* __restrict__ own_gid, const double* __restrict__ x,
+                                  double* __restrict__ xg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_own; i += (int64_t)gridDim.x * blockDim.x)
+    xg[own_gid[i]] = x[i];
 }
 
 }  // namespace ras

@@ -166,8 +166,16 @@ static void build_phase1(ras_plan* pl, const ras_partition* part) {
   };
   for (auto& S : pl->subs) {
     for (size_t i = 0; i < S.omega.size(); ++i)
-      if (!S.owned[i]) add(S.omega[i]);
-    for (int64_t g : S.ghosts) add(g);
+      if (!S.owned[i]) {
+        add(S.omega[i]);
+        S.nbr_subs.push_back(part->owner[S.omega[i]]);
+      }
+    for (int64_t g : S.ghosts) {
+      add(g);
+      S.nbr_subs.push_back(part->owner[g]);
+    }
+    std::sort(S.nbr_subs.begin(), S.nbr_subs.end());
+    S.nbr_subs.erase(std::unique(S.nbr_subs.begin(), S.nbr_subs.end()), S.nbr_subs.end());
   }
   std::vector<uint8_t>().swap(hmark);
   std::sort(halo.begin(), halo.end(), [&](int64_t a, int64_t b) {

@@ -24,6 +24,7 @@ struct SubPlan {
   std::vector<int64_t> omega;    // Omega_p ascending
   std::vector<uint8_t> owned;    // per omega row
   std::vector<int64_t> ghosts;   // Gamma_p ascending
+  std::vector<int32_t> nbr_subs; // owner subdomains of need_p (ascending, != p)
   int64_t row_off = 0, nrows = 0, nrows_pad = 0;  // row space
   int64_t own_off = 0, nown = 0;                   // owned slots
   int64_t tile_begin = 0, ntiles = 0;
@@ -36,7 +37,7 @@ struct SubPlan {
 struct ras_plan {
   int64_t n = 0;
   int32_t P = 0, rank = 0, world = 1, gamma = 0;
-  int32_t tile_rows = 256;
+  int32_t tile_rows = 1024;  // must equal ras::kTileRows (kernels.cuh)
   std::vector<int32_t> sub_to_rank;
   std::vector<ras::SubPlan> subs;  // local subdomains, ascending global id
   int64_t n_own = 0, n_halo = 0;

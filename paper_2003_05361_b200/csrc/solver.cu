@@ -46,32 +46,21 @@ void* dalloc(ras_ctx* c, size_t bytes) {
   } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
     p = nullptr;
   }
-  if (p) c->bufs.push_back(DevBuf{p, bytes});
+  if (p) c->bufs.push_back(DevBuf{p, bytes, false});
   return p;
 }
 
-template <class T>
-static ras_status upload(ras_ctx* c, T** dst, const std::vector<T>& src, size_t min_elems = 0) {
-  size_t n = std::max(src.size(), min_elems);
-  *dst = (T*)dalloc(c, n * sizeof(T));
-  if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
-  if (!src.empty()) RAS_CUDA(c, cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
-  return RAS_OK;
+// Always cudaMalloc (a base allocation that can be exported as a CUDA IPC
+// window to the peer GPUs: x storage and the detector board).
+void* dalloc_raw(ras_ctx* c, size_t bytes) {
+  bytes = std::max<size_t>(256, (bytes + 255) / 256 * 256);
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  cudaMemset(p, 0, bytes);
+  c->bufs.push_back(DevBuf{p, bytes, true});
+  return p;
 }
 
-template <class T>
-static ras_status zalloc(ras_ctx* c, T** dst, size_t n) {
-  *dst = (T*)dalloc(c, n * sizeof(T));
-  if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
-  RAS_CUDA(c, cudaMemset(*dst, 0, std::max<size_t>(n, 1) * sizeof(T)));
-  return RAS_OK;
-}
-
-#define TRY(x)                       \
-  do {                               \
-    ras_status s_ = (x);             \
-    if (s_ != RAS_OK) return s_;     \
-  } while (0)
 
 // Multi-rank exchange of halo requests over NCCL (setup only): every rank
 // learns which of its owned values each peer needs, in the peer's halo order.
@@ -163,18 +152,19 @@ static ras_status upload_plan(ras_ctx* c) {
     stb[i] = pl->subs[i].tile_begin;
     snt[i] = (int32_t)pl->subs[i].ntiles;
   }
-  int32_t* ts;
-  int64_t* tr;
-  int32_t* tn;
+  if (pl->tile_rows != kTileRows) return set_err(c, RAS_ESTATE, "plan tile_rows != kernel tile rows");
+  std::vector<int4> tiles(pl->tile_sub.size());
+  for (size_t i = 0; i < tiles.size(); ++i)
+    tiles[i] = make_int4((int)pl->tile_row0[i], pl->tile_nrows[i], pl->tile_sub[i], 0);
+  int4* ti;
   int64_t* sb;
   int32_t* sn;
-  TRY(upload(c, &ts, pl->tile_sub));
-  TRY(upload(c, &tr, pl->tile_row0));
-  TRY(upload(c, &tn, pl->tile_nrows));
+  TRY(upload(c, &ti, tiles));
   TRY(upload(c, &sb, stb));
   TRY(upload(c, &sn, snt));
-  c->T = Tiles{ts, tr, tn, sb, sn};
-  TRY(zalloc(c, &c->d_x, (size_t)(c->n_own + c->n_halo)));
+  c->T = Tiles{ti, sb, sn};
+  c->d_x = (double*)dalloc_raw(c, (size_t)(c->n_own + c->n_halo) * 8);
+  if (!c->d_x) return set_err(c, RAS_ENOMEM, "device allocation failed (x storage)");
   TRY(zalloc(c, &c->d_r, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_p, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_q, (size_t)c->rows_pad));
@@ -275,49 +265,97 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
 }
 
 // ---------------------------------------------------------------------------
+// Per-kernel CUDA-event timing (ras_kernel_timing): events recorded on the
+// library stream around each launch; durations summed per kernel kind.
+// ---------------------------------------------------------------------------
+int kt_begin(ras_ctx* c) {
+  if (!c->kt.on) return -1;
+  KTimer& t = c->kt;
+  while (t.used + 2 > t.pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    t.pool.push_back(e);
+  }
+  const int idx = (int)t.used;
+  t.used += 2;
+  cudaEventRecord(t.pool[idx], c->stream);
+  return idx;
+}
+
+void kt_end(ras_ctx* c, int kind, int idx) {
+  ++c->launches;
+  if (idx < 0) return;
+  cudaEventRecord(c->kt.pool[idx + 1], c->stream);
+  c->kt.kind.push_back(kind);
+  (void)0;
+}
+
+static void kt_reset(ras_ctx* c) {
+  c->kt.used = 0;
+  c->kt.kind.clear();
+  for (int k = 0; k < K_NKINDS; ++k) {
+    c->kt.total_ms[k] = 0.0;
+    c->kt.count[k] = 0;
+  }
+}
+
+static void kt_collect(ras_ctx* c) {
+  if (!c->kt.on) return;
+  cudaStreamSynchronize(c->stream);
+  for (size_t i = 0; i < c->kt.kind.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->kt.pool[2 * i], c->kt.pool[2 * i + 1]);
+    c->kt.total_ms[c->kt.kind[i]] += ms;
+    c->kt.count[c->kt.kind[i]] += 1;
+  }
+}
+
+#define LAUNCH(kind, ...)          \
+  do {                             \
+    const int ti_ = kt_begin(c);   \
+    __VA_ARGS__;                   \
+    kt_end(c, (kind), ti_);        \
+  } while (0)
+
+// ---------------------------------------------------------------------------
 // Sync sweep (lock-step, P155-161, P376-387): stream-ordered on one stream.
 // ---------------------------------------------------------------------------
-static ras_status launch_pcg_iter(ras_ctx* c, int it, int m, double inner_tol, bool last) {
+static ras_status launch_pcg_iter(ras_ctx* c, int m, double inner_tol, bool last) {
   const unsigned g = (unsigned)c->ntiles;
   Ctl C{c->d_stop};
-  k_spmv_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C);
-  k_update_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d, c->S, C, m,
-                                              inner_tol);
-  c->launches += 2;
-  if (!last) {
-    k_pupdate<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_r, c->d_p, c->S, C);
-    c->launches += 1;
-  }
-  (void)it;
+  LAUNCH(K_SPMV, k_spmv_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C));
+  LAUNCH(K_UPD, k_update_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d,
+                                                            c->S, C, m, inner_tol));
+  if (!last) LAUNCH(K_PUPD, k_pupdate<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_r, c->d_p, c->S, C));
   return RAS_OK;
 }
+
+static ras_status exchange(ras_ctx* c, Ctl C);
 
 static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact, int slot) {
   const unsigned g = (unsigned)c->ntiles;
   Ctl C{c->d_stop};
   // a1+a2
-  k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x, c->d_r, c->d_p,
-                                            c->S, C);
+  LAUNCH(K_RES, k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x,
+                                                          c->d_r, c->d_p, c->S, C));
   // a6 (global criterion on x^k, P344-346)
-  k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local);
-  c->launches += 2;
+  LAUNCH(K_CTRL, k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local));
   const double* r2g = c->d_r2_local;
   if (c->world > 1) {
     RAS_NCCL(c, ncclAllReduce(c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
     r2g = c->d_r2_global;
   }
-  k_sync_check<<<1, 32, 0, c->stream>>>(r2g, c->b2_global, tol, max_iters, c->d_sync, c->d_stop, c->h_stop_dev + slot);
-  c->launches += 1;
+  LAUNCH(K_CTRL, k_sync_check<<<1, 32, 0, c->stream>>>(r2g, c->b2_global, tol, max_iters, c->d_sync, c->d_stop,
+                                                       c->h_stop_dev + slot));
   // a3
   if (!exact) {
-    for (int it = 1; it <= m; ++it) TRY(launch_pcg_iter(c, it, m, inner_tol, it == m));
+    for (int it = 1; it <= m; ++it) TRY(launch_pcg_iter(c, m, inner_tol, it == m));
   } else {
     // exact mode: iterate until every local subdomain stops (checked every 16 iterations)
     for (int it = 1; it <= m; ++it) {
-      TRY(launch_pcg_iter(c, it, m, inner_tol, it == m));
+      TRY(launch_pcg_iter(c, m, inner_tol, it == m));
       if (it % 16 == 0) {
-        k_count_active<<<1, 32, 0, c->stream>>>(c->nl, c->S.active, c->d_nactive);
-        c->launches += 1;
+        LAUNCH(K_CTRL, k_count_active<<<1, 32, 0, c->stream>>>(c->nl, c->S.active, c->d_nactive));
         RAS_CUDA(c, cudaMemcpyAsync(c->h_nactive, c->d_nactive, 4, cudaMemcpyDeviceToHost, c->stream));
         RAS_CUDA(c, cudaStreamSynchronize(c->stream));
         if (*c->h_nactive == 0) break;
@@ -325,51 +363,96 @@ static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, d
     }
   }
   // a4
-  k_prolong<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C);
-  c->launches += 1;
-  // a5: pack + NCCL grouped send/recv straight into halo storage
-  if (c->world > 1) {
-    if (c->n_send) {
-      k_pack<<<(unsigned)std::min<int64_t>((c->n_send + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
-          c->n_send, c->d_send_slot, c->d_x, c->d_sendbuf, C);
-      c->launches += 1;
-    }
-    RAS_NCCL(c, ncclGroupStart());
-    for (int r = 0; r < c->world; ++r) {
-      if (r == c->rank) continue;
-      if (c->send_cnt[r])
-        RAS_NCCL(c, ncclSend(c->d_sendbuf + c->send_off[r], c->send_cnt[r], ncclDouble, r, c->nccl, c->stream));
-      if (c->recv_cnt[r])
-        RAS_NCCL(c, ncclRecv(c->d_x + c->n_own + c->recv_off[r], c->recv_cnt[r], ncclDouble, r, c->nccl, c->stream));
-    }
-    RAS_NCCL(c, ncclGroupEnd());
-  }
+  LAUNCH(K_PROL, k_prolong<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C));
+  // a5
+  TRY(exchange(c, C));
   RAS_CUDA(c, cudaGetLastError());
   return RAS_OK;
 }
 
-static ras_status load_x0(ras_ctx* c, const double* x0) {
-  const ras_plan* pl = c->plan;
-  std::vector<double> xs((size_t)(c->n_own + c->n_halo), 0.0);
-  if (x0) {
-    for (int64_t i = 0; i < c->n_own; ++i) xs[i] = x0[pl->own_gid[i]];
-    for (int64_t i = 0; i < c->n_halo; ++i) xs[c->n_own + i] = x0[pl->halo_gid[i]];
+// a5 (sync, P376-387): pack + NCCL grouped send/recv straight into halo storage
+// (no unpack: the receive buffer IS the halo segment of the peer's values).
+static ras_status exchange(ras_ctx* c, Ctl C) {
+  if (c->world == 1) return RAS_OK;
+  if (c->n_send) {
+    LAUNCH(K_PACK, k_pack<<<(unsigned)std::min<int64_t>((c->n_send + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
+                       c->n_send, c->d_send_slot, c->d_x, c->d_sendbuf, C));
   }
-  RAS_CUDA(c, cudaMemcpyAsync(c->d_x, xs.data(), xs.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  RAS_NCCL(c, ncclGroupStart());
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    if (c->send_cnt[r])
+      RAS_NCCL(c, ncclSend(c->d_sendbuf + c->send_off[r], c->send_cnt[r], ncclDouble, r, c->nccl, c->stream));
+    if (c->recv_cnt[r])
+      RAS_NCCL(c, ncclRecv(c->d_x + c->n_own + c->recv_off[r], c->recv_cnt[r], ncclDouble, r, c->nccl, c->stream));
+  }
+  RAS_NCCL(c, ncclGroupEnd());
+  return RAS_OK;
+}
+
+ras_status sync_exchange(ras_ctx* c) { return exchange(c, Ctl{nullptr, 0}); }
+
+// True relative residual ||b - A x|| / ||b|| of the stored iterate (halo must be
+// current): one residual pass over every tile + owned partial sums + allreduce.
+ras_status global_residual(ras_ctx* c, double* rel) {
+  const unsigned g = (unsigned)c->ntiles;
+  Ctl C{nullptr, 0};
+  LAUNCH(K_RES, k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x,
+                                                          c->d_r, c->d_p, c->S, C));
+  LAUNCH(K_CTRL, k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local));
+  const double* r2g = c->d_r2_local;
+  if (c->world > 1) {
+    RAS_NCCL(c, ncclAllReduce(c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    r2g = c->d_r2_global;
+  }
+  double r2 = 0.0;
+  RAS_CUDA(c, cudaMemcpyAsync(&r2, r2g, 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  *rel = c->b2_global > 0.0 ? std::sqrt(r2) / std::sqrt(c->b2_global) : (r2 == 0.0 ? 0.0 : INFINITY);
+  return RAS_OK;
+}
+
+static ras_status ensure_xglob(ras_ctx* c) {
+  if (c->d_xglob) return RAS_OK;
+  const ras_plan* pl = c->plan;
+  std::vector<int32_t> og(pl->own_gid.begin(), pl->own_gid.end()), hg(pl->halo_gid.begin(), pl->halo_gid.end());
+  TRY(upload(c, &c->d_own_gid, og, 1));
+  TRY(upload(c, &c->d_halo_gid, hg, 1));
+  c->d_xglob = (double*)dalloc(c, (size_t)pl->n * 8);
+  if (!c->d_xglob) return set_err(c, RAS_ENOMEM, "device allocation failed (global x buffer)");
+  return RAS_OK;
+}
+
+// x0 (host, global order) -> storage order on the device (one H2D copy + gather kernel)
+static ras_status load_x0(ras_ctx* c, const double* x0) {
+  const int64_t tot = c->n_own + c->n_halo;
+  if (!x0) {
+    RAS_CUDA(c, cudaMemsetAsync(c->d_x, 0, tot * 8, c->stream));
+    return RAS_OK;
+  }
+  TRY(ensure_xglob(c));
+  RAS_CUDA(c, cudaMemcpyAsync(c->d_xglob, x0, (size_t)c->plan->n * 8, cudaMemcpyHostToDevice, c->stream));
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 16));
+  LAUNCH(K_CTRL, k_scatter_x0<<<g, 256, 0, c->stream>>>(c->n_own, c->n_halo, c->d_own_gid, c->d_halo_gid, c->d_xglob,
+                                                         c->d_x));
+  RAS_CUDA(c, cudaGetLastError());
   return RAS_OK;
 }
 
 // Gather owner values to x_out (len n) on every rank (P242).
 static ras_status gather(ras_ctx* c, double* x_out) {
   const ras_plan* pl = c->plan;
+  if (c->world == 1) {
+    TRY(ensure_xglob(c));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n_own + 255) / 256, 148 * 16));
+    LAUNCH(K_CTRL, k_gather_x<<<g, 256, 0, c->stream>>>(c->n_own, c->d_own_gid, c->d_x, c->d_xglob));
+    RAS_CUDA(c, cudaMemcpyAsync(x_out, c->d_xglob, (size_t)pl->n * 8, cudaMemcpyDeviceToHost, c->stream));
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return RAS_OK;
+  }
   std::vector<double> own((size_t)c->n_own);
   RAS_CUDA(c, cudaMemcpyAsync(own.data(), c->d_x, own.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  if (c->world == 1) {
-    for (int64_t i = 0; i < c->n_own; ++i) x_out[pl->own_gid[i]] = own[i];
-    return RAS_OK;
-  }
   // all-gather padded (gid, value) pairs
   std::vector<int64_t> cnt{c->n_own};
   int64_t *d_cnt, *d_cnts;
@@ -429,6 +512,7 @@ static ras_status solve_sync(ras_ctx* c, double tol, int64_t max_iters) {
       }
       if (((volatile int32_t*)c->h_stop)[slot]) break;
     }
+    if (k > max_iters) break;  // sweep max_iters only checks x^{max_iters}; the device stops there
     st = sync_sweep(c, tol, max_iters, m, inner_tol, exact, slot);
     if (st != RAS_OK) break;
     RAS_CUDA(c, cudaEventRecord(ev[slot], c->stream));
@@ -512,7 +596,6 @@ static ras_status solve_common(ras_ctx* c, double tol, int64_t max_iters, ras_mo
   if (max_iters < 0) return set_err(c, RAS_EINVAL, "max_iters must be >= 0");
   RAS_CUDA(c, cudaSetDevice(c->device));
   std::memset(&c->st, 0, sizeof(c->st));
-  c->launches = 0;
   SyncState z{};
   RAS_CUDA(c, cudaMemcpyAsync(c->d_sync, &z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
   RAS_CUDA(c, cudaMemsetAsync(c->d_stop, 0, 4, c->stream));
@@ -543,7 +626,7 @@ static ras_status solve_common(ras_ctx* c, double tol, int64_t max_iters, ras_mo
 
 static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   c->st.mode = mode;
-  c->st.time_to_solution_s = t;
+  if (mode == RAS_SYNC) c->st.time_to_solution_s = t;  // async sets it at observed stop (R26)
   c->st.setup_s = c->setup_s;
   c->st.num_subdomains = c->plan->P;
   c->st.world = c->world;
@@ -567,12 +650,15 @@ ras_status ras_solve(ras_ctx* c, double tol, int64_t max_iters, ras_mode mode, c
   if (!c) return set_err(nullptr, RAS_EINVAL, "ras_solve: ctx is NULL");
   const double t0 = now_s();
   RAS_CUDA(c, cudaSetDevice(c->device));
+  c->launches = 0;
+  kt_reset(c);
   TRY(load_x0(c, x0));
   ras_status s = solve_common(c, tol, max_iters, mode);
   if (s != RAS_OK && s != RAS_ENOCONV && s != RAS_EVERIFY) return s;
   const double t1 = now_s();
-  finish_stats(c, mode, t1 - t0);
   if (x_out) TRY(gather(c, x_out));
+  finish_stats(c, mode, t1 - t0);
+  kt_collect(c);
   if (s != RAS_OK) return s;
   return c->st.converged ? RAS_OK : RAS_ENOCONV;
 }
@@ -582,6 +668,8 @@ ras_status ras_solve_device(ras_ctx* c, double tol, int64_t max_iters, ras_mode 
   if (!c) return set_err(nullptr, RAS_EINVAL, "ras_solve_device: ctx is NULL");
   RAS_CUDA(c, cudaSetDevice(c->device));
   const double t0 = now_s();
+  c->launches = 0;
+  kt_reset(c);
   if (x0_owned_dev) {
     RAS_CUDA(c, cudaMemcpyAsync(c->d_x, x0_owned_dev, c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
   } else {
@@ -589,22 +677,7 @@ ras_status ras_solve_device(ras_ctx* c, double tol, int64_t max_iters, ras_mode 
   }
   if (c->n_halo) {
     if (x0_owned_dev && c->world > 1) {
-      // halo = neighbours' owned x0 values: one exchange
-      Ctl C{nullptr};
-      if (c->n_send) {
-        k_pack<<<(unsigned)std::min<int64_t>((c->n_send + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
-            c->n_send, c->d_send_slot, c->d_x, c->d_sendbuf, C);
-      }
-      RAS_NCCL(c, ncclGroupStart());
-      for (int r = 0; r < c->world; ++r) {
-        if (r == c->rank) continue;
-        if (c->send_cnt[r])
-          RAS_NCCL(c, ncclSend(c->d_sendbuf + c->send_off[r], c->send_cnt[r], ncclDouble, r, c->nccl, c->stream));
-        if (c->recv_cnt[r])
-          RAS_NCCL(c,
-                   ncclRecv(c->d_x + c->n_own + c->recv_off[r], c->recv_cnt[r], ncclDouble, r, c->nccl, c->stream));
-      }
-      RAS_NCCL(c, ncclGroupEnd());
+      TRY(sync_exchange(c));  // halo = neighbours' owned x0 values
     } else {
       RAS_CUDA(c, cudaMemsetAsync(c->d_x + c->n_own, 0, c->n_halo * 8, c->stream));
     }
@@ -614,11 +687,38 @@ ras_status ras_solve_device(ras_ctx* c, double tol, int64_t max_iters, ras_mode 
   finish_stats(c, mode, now_s() - t0);
   if (x_owned_dev) RAS_CUDA(c, cudaMemcpyAsync(x_owned_dev, c->d_x, c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  kt_collect(c);
   if (s != RAS_OK) return s;
   return c->st.converged ? RAS_OK : RAS_ENOCONV;
 }
 
 int64_t ras_owned_count(const ras_ctx* c) { return c ? c->n_own : -1; }
+
+ras_status ras_kernel_timing(ras_ctx* c, int32_t enable) {
+  if (!c) return RAS_EINVAL;
+  c->kt.on = enable != 0;
+  return RAS_OK;
+}
+
+ras_status ras_kernel_times(const ras_ctx* c, ras_kernel_time_t* out, int32_t max_entries, int32_t* n_out) {
+  if (!c || !n_out) return RAS_EINVAL;
+  static const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", "k_update_dot", "k_pupdate",
+                                        "k_prolong",  "k_pack",     "control"};
+  const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate,
+                                  c->mb.prolong,  c->mb.pack,     0.0};
+  int n = 0;
+  for (int k = 0; k < K_NKINDS && n < max_entries; ++k) {
+    if (!out) break;
+    std::memset(&out[n], 0, sizeof(out[n]));
+    std::strncpy(out[n].name, names[k], sizeof(out[n].name) - 1);
+    out[n].launches = c->kt.count[k];
+    out[n].total_ms = c->kt.total_ms[k];
+    out[n].bytes_per_launch = bytes[k];
+    ++n;
+  }
+  *n_out = out ? n : K_NKINDS;
+  return RAS_OK;
+}
 
 ras_status ras_owned_gids(const ras_ctx* c, int64_t* g) {
   if (!c || !g) return RAS_EINVAL;
@@ -643,8 +743,9 @@ void ras_free(ras_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   async_free(c);
+  for (auto e : c->kt.pool) cudaEventDestroy(e);
   for (auto& b : c->bufs) {
-    if (c->dev_free)
+    if (c->dev_free && !b.raw)
       c->dev_free(b.ptr, c->alloc_user);
     else
       cudaFree(b.ptr);

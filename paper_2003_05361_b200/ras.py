@@ -235,6 +235,17 @@ class Solver:
         _check(F.lib().ras_ctx_plan(self._h, C.byref(h)), self._h)
         return Plan._borrow(h, self)
 
+    def kernel_timing(self, enable=True):
+        _check(F.lib().ras_kernel_timing(self._h, 1 if enable else 0), self._h)
+
+    def kernel_times(self) -> dict:
+        """{name: (launches, total_ms, bytes_per_launch)} of the last solve."""
+        arr = (F.RasKernelTime * 16)()
+        n = F.I32()
+        _check(F.lib().ras_kernel_times(self._h, arr, 16, C.byref(n)), self._h)
+        return {arr[i].name.decode(): (arr[i].launches, arr[i].total_ms, arr[i].bytes_per_launch)
+                for i in range(n.value)}
+
     def set_scripted_flags(self, flags):
         f = np.ascontiguousarray(flags, dtype=np.uint8)
         _check(F.lib().ras_set_scripted_flags(self._h, F.ptr(f, F.U8), f.shape[0]), self._h)
