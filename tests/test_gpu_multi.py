@@ -1,0 +1,138 @@
+"""Multi-GPU RAS (one process per GPU): sync mode with NCCL halo exchange +
+allreduce (parity with the oracle at 1e-10 per sweep), async mode with NVLink
+P2P puts and both detectors (verified residual).  Skipped with < 2 GPUs."""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import ras_inputs as ri
+
+pytestmark = pytest.mark.gpu
+
+
+def _ngpus():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _worker(rank, world, nccl_id, cfg, q):
+    try:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        import paper_2003_05361_b200 as R
+
+        nx, ny, P, gamma = cfg["nx"], cfg["ny"], cfg["P"], cfg["gamma"]
+        A = ri.laplace_2d(nx, ny)
+        b = ri.rhs(nx * ny, 0)
+        owner = cfg["owner"]
+        if cfg.get("window"):
+            # this rank's rows +- (gamma+1) grid rows: exercises the row-window ABI
+            s2r = np.array([(p * world) // P for p in range(P)])
+            rows = np.nonzero(s2r[owner] == rank)[0]
+            r0 = max(0, rows.min() - (gamma + 1) * nx)
+            r1 = min(nx * ny, rows.max() + 1 + (gamma + 1) * nx)
+            A = ri.laplace_2d_rows(nx, ny, r0, r1)
+            b = b[r0:r1]
+        s = R.Solver(A, b, owner, gamma, R.options(cfg["solver"], cfg["m"], detector=cfg.get("detector", "decentral")),
+                     comm={"rank": rank, "world": world, "device": rank, "nccl_id": nccl_id})
+        out = {}
+        for k in cfg.get("ks", []):
+            st, x = s.solve(1e-300, k, "sync")
+            out[("sync", k)] = (st, x, s.stats()["sweeps"])
+        if cfg.get("converge"):
+            st, x = s.solve(1e-8, 20000, cfg["converge"])
+            out[("conv", cfg["converge"])] = (st, x, s.stats())
+        s.close()
+        q.put((rank, "ok", out))
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+
+        q.put((rank, "err", traceback.format_exc()))
+
+
+def _run(world, cfg, timeout=300):
+    import paper_2003_05361_b200 as R
+
+    nid = R.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, nid, cfg, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, st, out = q.get(timeout=timeout)
+        assert st == "ok", out
+        res[r] = out
+    for p in ps:
+        p.join(60)
+    return res
+
+
+def _oracle(cfg, K):
+    A = ri.laplace_2d(cfg["nx"], cfg["ny"])
+    b = ri.rhs(cfg["nx"] * cfg["ny"], 0)
+    subs = O.setup(A, b, cfg["owner"], cfg["gamma"])
+    for s in subs:
+        O.make_local_solver(s, cfg["solver"], cfg["m"])
+    return A, b, O.ras_sync(A, b, subs, 1e-300, K, record_iterates=True)
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_sync_parity(world):
+    if _ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    nx, ny = 96, 80
+    cfg = dict(nx=nx, ny=ny, P=8, gamma=3, solver="jacobi", m=12, ks=[1, 4],
+               owner=ri.voronoi_partition(nx, ny, 8, seed=5), window=True)
+    res = _run(world, cfg)
+    A, b, ref = _oracle(cfg, 4)
+    for r in range(world):
+        for k in (1, 4):
+            st, x, sw = res[r][("sync", k)]
+            assert sw == k
+            err = np.linalg.norm(x - ref.iterates[k]) / np.linalg.norm(ref.iterates[k])
+            assert err <= 1e-10, (r, k, err)
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("detector", ["central", "decentral"])
+def test_multi_gpu_async_p2p_converges(detector):
+    nx, ny = 80, 80
+    cfg = dict(nx=nx, ny=ny, P=6, gamma=4, solver="jacobi", m=10, converge="async", detector=detector,
+               owner=ri.voronoi_partition(nx, ny, 6, seed=2))
+    res = _run(2, cfg)
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 0)
+    xs = np.linalg.solve(A.to_scipy().toarray(), b)
+    for r in range(2):
+        st, x, stats = res[r][("conv", "async")]
+        assert st == 0, stats
+        assert O.verify_global(A, x, b, 1e-8)[0]
+        assert np.linalg.norm(x - xs) / np.linalg.norm(xs) <= 1e-6
+        assert stats["fresh_halo_reads"] > 0  # peers' puts arrived over NVLink
+    np.testing.assert_array_equal(res[0][("conv", "async")][1], res[1][("conv", "async")][1])
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
+def test_multi_gpu_sync_converges():
+    nx = ny = 64
+    cfg = dict(nx=nx, ny=ny, P=4, gamma=2, solver="jacobi", m=20, converge="sync",
+               owner=O.partition_regular(nx, ny, 1, 2, 2, 1))
+    res = _run(2, cfg)
+    A, b, _ = _oracle(cfg, 0)
+    subs = O.setup(A, b, cfg["owner"], 2)
+    for s in subs:
+        O.make_local_solver(s, "jacobi", 20)
+    ref = O.ras_sync(A, b, subs, 1e-8, 20000)
+    for r in range(2):
+        st, x, stats = res[r][("conv", "sync")]
+        assert st == 0 and stats["sweeps"] == ref.sweeps
+        assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-10
