@@ -455,30 +455,14 @@ static ras_status enqueue_sub_sweep(ras_ctx* c, int lp, cudaStream_t s, double t
   AsyncRt* A = c->async;
   const ras_plan* pl = c->plan;
   const auto& SP = pl->subs[lp];
-  const int64_t tb = SP.tile_begin;
-  const unsigned g = (unsigned)SP.ntiles;
+  const Range R = range_sub(c, lp);
   Ctl C{A->d_lstop, 1};
-  k_residual<<<g, kThreads, 0, s>>>(tb, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x, c->d_r, c->d_p, c->S,
-                                    C);
+  TRY(enq_residual(c, s, R, C));
   k_detect<<<1, 32, 0, s>>>(lp, A->det, c->S, tol, max_iters, A->d_lstop, A->h_lstop_dev, A->d_updates,
                             A->d_noconv);
-  c->launches += 2;
-  for (int it = 1; it <= m; ++it) {
-    k_spmv_dot<<<g, kThreads, 0, s>>>(tb, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C);
-    k_update_dot<<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d, c->S, C, m, inner_tol);
-    c->launches += 2;
-    if (it < m) {
-      k_pupdate<<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_r, c->d_p, c->S, C);
-      c->launches += 1;
-    }
-    if (exact && it % 16 == 0) {  // exact mode: stop enqueuing once this subdomain's PCG finished
-      RAS_CUDA(c, cudaMemcpyAsync(A->h_active + lp, c->S.active + lp, 4, cudaMemcpyDeviceToHost, s));
-      RAS_CUDA(c, cudaStreamSynchronize(s));
-      if (((volatile int32_t*)A->h_active)[lp] == 0) break;
-    }
-  }
-  k_prolong<<<g, kThreads, 0, s>>>(tb, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C);
   c->launches += 1;
+  TRY(enq_pcg(c, s, R, C, m, inner_tol, exact));
+  TRY(enq_prolong(c, s, R, C));
   const int64_t e0 = A->put_off[lp], e1 = A->put_off[lp + 1];
   if (e1 > e0) {
     const unsigned pg = (unsigned)std::min<int64_t>((e1 - e0 + 255) / 256, 148 * 4);
@@ -564,20 +548,15 @@ static ras_status run_scripted(ras_ctx* c, double tol, int64_t max_iters, int m,
     const int cur = (int)(k & 1), prv = cur ^ 1;
     // stop words persist: next <- prev (stop section); reports are rewritten
     RAS_CUDA(c, cudaMemcpyAsync(raw[cur], raw[prv], (size_t)c->plan->P * 4, cudaMemcpyDeviceToDevice, c->stream));
-    k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x, c->d_r,
-                                              c->d_p, c->S, C);
+    const Range R = range_all(c);
+    TRY(enq_residual(c, c->stream, R, C));
     k_detect_scripted<<<(nl + 127) / 128, 128, 0, c->stream>>>(nl, k, A->det, A->d_scripted, c->scripted_sweeps,
                                                                 bufs[prv], bufs[cur], A->d_lstop, A->d_stop_sweep,
                                                                 A->d_updates);
-    for (int it = 1; it <= m; ++it) {
-      k_spmv_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C);
-      k_update_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d, c->S, C, m,
-                                                  inner_tol);
-      if (it < m) k_pupdate<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_r, c->d_p, c->S, C);
-    }
-    k_prolong<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C);
+    TRY(enq_pcg(c, c->stream, R, C, m, inner_tol, false));
+    TRY(enq_prolong(c, c->stream, R, C));
     k_mirror_stops<<<(nl + 127) / 128, 128, 0, c->stream>>>(nl, A->d_lstop, A->h_lstop_dev);
-    c->launches += 4 + 3 * m;
+    c->launches += 2;
     RAS_CUDA(c, cudaStreamSynchronize(c->stream));
     int all = 1;
     for (int i = 0; i < nl; ++i) all &= ((volatile int32_t*)A->h_lstop)[i] != 0;

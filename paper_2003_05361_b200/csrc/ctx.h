@@ -23,7 +23,24 @@ struct DevBuf {
 
 struct AsyncRt;  // async-mode runtime (async.cu)
 
-enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_NKINDS };
+enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_ZDOT, K_NKINDS };
+
+// A range of tiles: every local subdomain (lp < 0) or one subdomain.
+struct Range {
+  int64_t tile_base;
+  unsigned ntiles;
+  int lp;
+};
+
+// Device copy of one level-ordered triangular factor (factor.cpp / k_trsv).
+struct TriBuf {
+  TriDev dev{};
+  int32_t nchunks = 0;
+  int32_t nlev_slots = 0;  // size of the per-(subdomain, level) done counters
+  std::vector<int32_t> sub_c0, sub_nc, sub_lev_off, sub_nlev;
+  int32_t* d_lev_done = nullptr;
+  double bytes = 0.0;      // algorithmic bytes of one solve
+};
 
 struct KTimer {
   bool on = false;
@@ -35,7 +52,7 @@ struct KTimer {
 };
 
 struct ModelBytes {  // algorithmic bytes per launch over the whole row space
-  double residual, spmv_dot, update_dot, pupdate, prolong, pack;
+  double residual, spmv_dot, update_dot, pupdate, prolong, pack, trsv, zdot;
 };
 
 }  // namespace ras
@@ -68,6 +85,11 @@ struct ras_ctx {
   double* d_p = nullptr;
   double* d_q = nullptr;
   double* d_d = nullptr;
+  // IC(0)/ILU(0) path (a3')
+  bool ic = false;
+  double* d_z = nullptr;
+  ras::TriBuf tri_f, tri_b;
+  uint32_t* d_trsv_ctr = nullptr;  // [2][nl + 1] chunk counters (per subdomain + batched)
   ras::Scal S{};
   int64_t* d_inner_total = nullptr;
   // sync control
@@ -110,8 +132,13 @@ ras_status cuda_err(ras_ctx* c, cudaError_t e, const char* what);
 void* dalloc(ras_ctx* c, size_t bytes);
 void* dalloc_raw(ras_ctx* c, size_t bytes);
 ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters);
-int kt_begin(ras_ctx* c);
-void kt_end(ras_ctx* c, int kind, int idx);
+int kt_begin(ras_ctx* c, cudaStream_t s);
+void kt_end(ras_ctx* c, cudaStream_t s, int kind, int idx);
+Range range_all(ras_ctx* c);
+Range range_sub(ras_ctx* c, int lp);
+ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C);
+ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol, bool exact);
+ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C);
 ras_status async_setup(ras_ctx* c);
 void async_free(ras_ctx* c);
 }  // namespace ras

@@ -153,8 +153,10 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
 // ---------------------------------------------------------------------------
 // a1+a2: restrict + residual + PCG start.
 //   r = b~ - [A_p|B_p] x (x read in place from owned/halo storage: restrict),
-//   z = D^-1 r, p = z; partials: rho = r.z, ||r~||^2, owned ||r~||^2.
+//   JAC: z = D^-1 r, p = z; partials: rho = r.z, ||r~||^2, owned ||r~||^2.
+//   !JAC (IC(0)/ILU(0)): only r and the norms; z = M^-1 r follows (trsv).
 // ---------------------------------------------------------------------------
+template <bool JAC = true>
 static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base, Tiles T, Sell R,
                                                               const double* __restrict__ b,
                                                               const double* __restrict__ diag,
@@ -190,10 +192,12 @@ static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base,
     if (lr < ti.y) {
       const int64_t row = ti.x + lr;
       const double ri = bi[j] - ax[j];
-      const double zi = __drcp_rn(di[j]) * ri;
       r[row] = ri;
-      p[row] = zi;
-      v[0] += ri * zi;
+      if (JAC) {
+        const double zi = __drcp_rn(di[j]) * ri;
+        p[row] = zi;
+        v[0] += ri * zi;
+      }
       v[1] += ri * ri;
       v[2] += os[j] >= 0 ? ri * ri : 0.0;
     }
@@ -207,7 +211,8 @@ static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base,
       S.rt2[lp] = o[1];
       S.own2[lp] = o[2];
       S.rr[lp] = o[1];
-      S.active[lp] = (o[0] != 0.0);  // "if rho == 0: break" (R7)
+      // "if rho == 0: break" (R7); IC path: decided after z = M^-1 r (k_zdot<true>)
+      S.active[lp] = JAC ? (o[0] != 0.0) : 1;
       S.its[lp] = 0;
       S.ticket[lp] = 0u;
     }
@@ -269,7 +274,9 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base,
 }
 
 // a3 pass 2: d += alpha p (d = alpha p on the first iteration), r -= alpha q,
-// z = D^-1 r; partials r.z, r.r; last CTA: inner stop test, beta, rho.
+// JAC: z = D^-1 r; partials r.z, r.r; last CTA: inner stop test, beta, rho.
+// !JAC: only r.r (inner stop test, iteration cap); rho' after the trisolves.
+template <bool JAC = true>
 static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T,
                                                                 const double* __restrict__ diag,
                                                                 const double* __restrict__ p,
@@ -293,7 +300,7 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
       pi[j] = __ldcs(&p[row]);
       qi[j] = __ldcs(&q[row]);
       ri[j] = __ldcs(&r[row]);
-      gi[j] = __ldcs(&diag[row]);
+      if (JAC) gi[j] = __ldcs(&diag[row]);
       di[j] = first ? 0.0 : __ldcs(&d[row]);
     }
   }
@@ -306,8 +313,10 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
       const double rn = ri[j] - alpha * qi[j];
       d[row] = dn;
       r[row] = rn;
-      const double zi = __drcp_rn(gi[j]) * rn;
-      v[0] += rn * zi;
+      if (JAC) {
+        const double zi = __drcp_rn(gi[j]) * rn;
+        v[0] += rn * zi;
+      }
       v[1] += rn * rn;
     }
   }
@@ -319,6 +328,8 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
       S.rr[lp] = o[1];
       if (inner_tol > 0.0 && sqrt(o[1]) <= inner_tol * sqrt(S.rt2[lp])) {
         S.active[lp] = 0;  // inner tolerance reached (exact mode / eta)
+      } else if (!JAC) {
+        if (S.its[lp] >= m) S.active[lp] = 0;  // z, rho', p of the last iteration are never used
       } else {
         const double rho_new = o[0];
         S.beta[lp] = rho_new / S.rho[lp];
@@ -355,6 +366,143 @@ static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, 
   for (int j = 0; j < kRPT; ++j) {
     const int lr = j * kThreads + threadIdx.x;
     if (lr < ti.y) p[ti.x + lr] = __drcp_rn(gi[j]) * ri[j] + beta * pi[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a3' (IC(0)/ILU(0)-PCG): M = L U, z = U^-1 L^-1 r by two level-scheduled
+// triangular solves (P320-323, level-set strategy).
+// ---------------------------------------------------------------------------
+struct TriDev {
+  const int32_t* rows;    // level-ordered row-space rows
+  const int32_t* rp;      // entry offsets per level-ordered position
+  const int32_t* col;     // dependency rows
+  const double* val;
+  const double* diag;     // divisor per row-space row
+  const int4* chunk;      // {rows begin, rows end, local subdomain, level}
+  const int32_t* batched; // chunk order of a batched (all-subdomain) solve
+  const int32_t* sub_lev_off;
+  const int32_t* lev_nchunks;
+};
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// out[i] = (in[i] - sum_j T_ij out[j]) / diag[i], rows in level order.
+// Chunks (256 rows of one level of one subdomain) are claimed from an atomic
+// counter in level order; a chunk of level l of subdomain p first waits until
+// every chunk of level l-1 of p has completed.  A waited-on chunk was claimed
+// earlier by a running CTA, so the wait always terminates (no co-residency
+// assumption, no inter-launch waiting).
+static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batched, int32_t c0, int32_t nchunk,
+                                                          uint32_t* counter, int32_t* lev_done,
+                                                          const double* __restrict__ in, double* out,
+                                                          const int32_t* __restrict__ active, Ctl C) {
+  __shared__ int s_c;
+  for (;;) {
+    if (threadIdx.x == 0) s_c = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int c = s_c;
+    __syncthreads();
+    if (c >= nchunk) return;
+    const int cid = use_batched ? T.batched[c] : c0 + c;
+    const int4 ch = T.chunk[cid];
+    const int lp = ch.z, lev = ch.w;
+    const int32_t* done = lev_done + T.sub_lev_off[lp];
+    const bool skip = stopped(C, lp) || !active[lp];
+    if (!skip && lev > 0 && threadIdx.x == 0) {
+      const int32_t need = T.lev_nchunks[T.sub_lev_off[lp] + lev - 1];
+      while (ld_acquire_gpu(done + lev - 1) < need) __nanosleep(64);
+    }
+    __syncthreads();
+    const int k = ch.x + threadIdx.x;
+    if (!skip && k < ch.y) {
+      const int32_t i = __ldg(&T.rows[k]);
+      double s = __ldg(&in[i]);
+      const int32_t e1 = __ldg(&T.rp[k + 1]);
+      for (int32_t e = __ldg(&T.rp[k]); e < e1; ++e) s -= __ldg(&T.val[e]) * __ldcg(&out[__ldg(&T.col[e])]);
+      __stcg(&out[i], s / __ldg(&T.diag[i]));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&lev_done[T.sub_lev_off[lp] + lev], 1);
+    }
+  }
+}
+
+// IC path, after z = M^-1 r.  INIT (PCG start): p = z, rho = r.z, active = rho != 0.
+// !INIT: rho' = r.z, beta = rho'/rho, rho = rho' (rho' == 0 -> stop, R7).
+template <bool INIT>
+static __global__ void __launch_bounds__(kThreads) k_zdot(int64_t tile_base, Tiles T, const double* __restrict__ r,
+                                                          const double* __restrict__ z, double* __restrict__ p, Scal S,
+                                                          Ctl C) {
+  __shared__ double sh[1][kThreads / 32];
+  const int64_t t = tile_base + blockIdx.x;
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp) || !S.active[lp]) return;
+  double v[1] = {0.0};
+  double ri[kRPT], zi[kRPT];
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      ri[j] = __ldcs(&r[ti.x + lr]);
+      zi[j] = __ldcs(&z[ti.x + lr]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      v[0] += ri[j] * zi[j];
+      if (INIT) p[ti.x + lr] = zi[j];
+    }
+  }
+  block_sum<1>(v, sh);
+  if (tile_partials_last<1>(v, t, lp, T, S)) {
+    double o[1];
+    reduce_sub_partials<1>(o, lp, T, S, sh);
+    if (threadIdx.x == 0) {
+      if (INIT) {
+        S.rho[lp] = o[0];
+        S.active[lp] = o[0] != 0.0;
+      } else {
+        S.beta[lp] = o[0] / S.rho[lp];
+        S.rho[lp] = o[0];
+        if (o[0] == 0.0) S.active[lp] = 0;
+      }
+      S.ticket[lp] = 0u;
+    }
+  }
+}
+
+// IC path: p = z + beta p.
+static __global__ void __launch_bounds__(kThreads) k_pupdate_z(int64_t tile_base, Tiles T,
+                                                               const double* __restrict__ z, double* __restrict__ p,
+                                                               Scal S, Ctl C) {
+  const int64_t t = tile_base + blockIdx.x;
+  const int4 ti = T.tile[t];
+  const int lp = ti.z;
+  if (stopped(C, lp) || !S.active[lp]) return;
+  const double beta = S.beta[lp];
+  double zi[kRPT], pi[kRPT];
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      zi[j] = __ldcs(&z[ti.x + lr]);
+      pi[j] = __ldcs(&p[ti.x + lr]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) p[ti.x + lr] = zi[j] + beta * pi[j];
   }
 }
 

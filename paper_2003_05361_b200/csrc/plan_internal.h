@@ -1,6 +1,7 @@
 // Internal definition of ras_plan (host-side setup, scope row a0).  Pure C++.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -17,6 +18,21 @@ const std::string& tls_error();
 struct Fail {
   ras_status st;
   std::string msg;
+};
+
+// One triangular factor of every local A_p in level order (factor.cpp).
+struct TriHost {
+  std::vector<int32_t> rows;  // row-space rows, per subdomain, by level, ascending within a level
+  std::vector<int32_t> rp;    // offsets into col/val, per position in `rows` (size rows+1)
+  std::vector<int32_t> col;   // row-space column of each off-diagonal dependency
+  std::vector<double> val;
+  std::vector<double> diag;   // per row-space row: divisor
+  std::vector<std::array<int32_t, 4>> chunk;  // {rows begin, rows end, local subdomain, level}
+  std::vector<int32_t> batched;               // chunk ids ordered by (level, subdomain)
+  std::vector<int32_t> sub_chunk_begin, sub_chunk_end;  // per subdomain (contiguous, level order)
+  std::vector<int32_t> sub_lev_off, sub_nlev;           // per subdomain: offset into lev_nchunks
+  std::vector<int32_t> lev_nchunks;                     // chunks per (subdomain, level)
+  int64_t max_levels = 0;
 };
 
 struct SubPlan {
@@ -81,5 +97,10 @@ struct ras_plan {
   std::vector<int64_t> tile_row0;
   std::vector<int32_t> tile_nrows;
   double b2_global_local = 0.0;  // sum over this rank's owned rows of b^2
-
 };
+
+namespace ras {
+// IC(0) (kind = RAS_LS_IC0_PCG) or ILU(0) factors of every local A_p, in level
+// order: F = forward (L), B = backward (L^T or U).  Throws Fail on a pivot <= 0.
+void build_factors(ras_plan* pl, int kind, TriHost& F, TriHost& B);
+}  // namespace ras

@@ -125,6 +125,58 @@ static void compute_model_bytes(ras_ctx* c) {
   c->mb.pack = (double)c->n_send * (4 + 8 + 8);
 }
 
+// a3' setup: IC(0)/ILU(0) factors + level sets on the host (factor.cpp), uploaded once
+static ras_status upload_tri(ras_ctx* c, const TriHost& H, TriBuf& B) {
+  const ras_plan* pl = c->plan;
+  int32_t *rows, *rp, *col, *bat, *slo, *lnc;
+  double *val, *diag;
+  int4* ch;
+  TRY(upload(c, &rows, H.rows, 1));
+  TRY(upload(c, &rp, H.rp, 1));
+  TRY(upload(c, &col, H.col, 1));
+  TRY(upload(c, &val, H.val, 1));
+  TRY(upload(c, &diag, H.diag, 1));
+  std::vector<int4> chunks(H.chunk.size());
+  for (size_t i = 0; i < chunks.size(); ++i)
+    chunks[i] = make_int4(H.chunk[i][0], H.chunk[i][1], H.chunk[i][2], H.chunk[i][3]);
+  TRY(upload(c, &ch, chunks, 1));
+  TRY(upload(c, &bat, H.batched, 1));
+  TRY(upload(c, &slo, H.sub_lev_off, 1));
+  TRY(upload(c, &lnc, H.lev_nchunks, 1));
+  B.dev = TriDev{rows, rp, col, val, diag, ch, bat, slo, lnc};
+  B.nchunks = (int32_t)H.chunk.size();
+  B.nlev_slots = (int32_t)H.lev_nchunks.size();
+  B.sub_lev_off = H.sub_lev_off;
+  B.sub_nlev = H.sub_nlev;
+  B.sub_c0 = H.sub_chunk_begin;
+  B.sub_nc.resize(H.sub_chunk_begin.size());
+  for (size_t i = 0; i < B.sub_nc.size(); ++i) B.sub_nc[i] = H.sub_chunk_end[i] - H.sub_chunk_begin[i];
+  TRY(zalloc(c, &B.d_lev_done, (size_t)std::max(B.nlev_slots, 1)));
+  // algorithmic bytes of one solve: per real row rows/rp/in/out/diag, per entry val+col
+  B.bytes = (double)pl->rows_local * (4 + 4 + 8 + 8 + 8) + (double)(pl->nnz_local - pl->rows_local) / 2.0 * 12.0;
+  return RAS_OK;
+}
+
+static ras_status upload_factors(ras_ctx* c) {
+  TriHost F, B;
+  try {
+    build_factors(c->plan, c->opt.local_solver, F, B);
+  } catch (const Fail& f) {
+    return set_err(c, f.st, f.msg);
+  }
+  TRY(upload_tri(c, F, c->tri_f));
+  TRY(upload_tri(c, B, c->tri_b));
+  TRY(zalloc(c, &c->d_z, (size_t)c->rows_pad));
+  TRY(zalloc(c, &c->d_trsv_ctr, (size_t)2 * (c->nl + 1)));
+  c->ic = true;
+  const double rows = (double)c->plan->rows_local;
+  c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + 16 /*r*/ + 16 /*d*/);
+  c->mb.pupdate = rows * (8 /*z*/ + 16 /*p*/);
+  c->mb.trsv = 0.5 * (c->tri_f.bytes + c->tri_b.bytes);
+  c->mb.zdot = rows * 16.0;
+  return RAS_OK;
+}
+
 static ras_status upload_plan(ras_ctx* c) {
   ras_plan* pl = c->plan;
   c->rows_pad = pl->rows_pad;
@@ -188,7 +240,7 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(zalloc(c, &c->d_nactive, 1));
   RAS_CUDA(c, cudaHostAlloc((void**)&c->h_stop, 32 * sizeof(int32_t), cudaHostAllocMapped));
   RAS_CUDA(c, cudaHostGetDevicePointer((void**)&c->h_stop_dev, c->h_stop, 0));
-  RAS_CUDA(c, cudaHostAlloc((void**)&c->h_nactive, 64, cudaHostAllocDefault));
+  RAS_CUDA(c, cudaHostAlloc((void**)&c->h_nactive, (size_t)(c->nl + 1) * 4, cudaHostAllocDefault));
   // exchange lists (sync): concatenated per peer
   c->send_off.assign(c->world + 1, 0);
   c->send_cnt.assign(c->world, 0);
@@ -257,8 +309,11 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
     RAS_CUDA(c, cudaMemcpyAsync(&c->b2_global, d, 8, cudaMemcpyDeviceToHost, c->stream));
     RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   }
-  if (c->opt.local_solver != RAS_LS_JACOBI_PCG && c->opt.local_solver != RAS_LS_EXACT_PCG)
-    return set_err(c, RAS_EINVAL, "local solver not available in this build");
+  if (c->opt.local_solver == RAS_LS_IC0_PCG || c->opt.local_solver == RAS_LS_ILU0_PCG) {
+    TRY(upload_factors(c));
+  } else if (c->opt.local_solver != RAS_LS_JACOBI_PCG && c->opt.local_solver != RAS_LS_EXACT_PCG) {
+    return set_err(c, RAS_EINVAL, "unknown local solver");
+  }
   TRY(async_setup(c));
   RAS_CUDA(c, cudaDeviceSynchronize());
   return RAS_OK;
@@ -268,8 +323,8 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
 // Per-kernel CUDA-event timing (ras_kernel_timing): events recorded on the
 // library stream around each launch; durations summed per kernel kind.
 // ---------------------------------------------------------------------------
-int kt_begin(ras_ctx* c) {
-  if (!c->kt.on) return -1;
+int kt_begin(ras_ctx* c, cudaStream_t s) {
+  if (!c->kt.on || s != c->stream) return -1;
   KTimer& t = c->kt;
   while (t.used + 2 > t.pool.size()) {
     cudaEvent_t e;
@@ -278,16 +333,15 @@ int kt_begin(ras_ctx* c) {
   }
   const int idx = (int)t.used;
   t.used += 2;
-  cudaEventRecord(t.pool[idx], c->stream);
+  cudaEventRecord(t.pool[idx], s);
   return idx;
 }
 
-void kt_end(ras_ctx* c, int kind, int idx) {
+void kt_end(ras_ctx* c, cudaStream_t s, int kind, int idx) {
   ++c->launches;
   if (idx < 0) return;
-  cudaEventRecord(c->kt.pool[idx + 1], c->stream);
+  cudaEventRecord(c->kt.pool[idx + 1], s);
   c->kt.kind.push_back(kind);
-  (void)0;
 }
 
 static void kt_reset(ras_ctx* c) {
@@ -310,34 +364,125 @@ static void kt_collect(ras_ctx* c) {
   }
 }
 
-#define LAUNCH(kind, ...)          \
-  do {                             \
-    const int ti_ = kt_begin(c);   \
-    __VA_ARGS__;                   \
-    kt_end(c, (kind), ti_);        \
+// every kernel launch goes through LAUNCH: counted, and event-timed when the
+// timing mode is on and the launch is on the library stream (`s` in scope or c->stream)
+#define LAUNCH_ON(strm, kind, ...)        \
+  do {                                    \
+    const int ti_ = kt_begin(c, (strm));  \
+    __VA_ARGS__;                          \
+    kt_end(c, (strm), (kind), ti_);       \
   } while (0)
+#define LAUNCH(kind, ...) LAUNCH_ON(c->stream, kind, __VA_ARGS__)
 
 // ---------------------------------------------------------------------------
 // Sync sweep (lock-step, P155-161, P376-387): stream-ordered on one stream.
 // ---------------------------------------------------------------------------
-static ras_status launch_pcg_iter(ras_ctx* c, int m, double inner_tol, bool last) {
-  const unsigned g = (unsigned)c->ntiles;
-  Ctl C{c->d_stop};
-  LAUNCH(K_SPMV, k_spmv_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C));
-  LAUNCH(K_UPD, k_update_dot<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d,
-                                                            c->S, C, m, inner_tol));
-  if (!last) LAUNCH(K_PUPD, k_pupdate<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_diag, c->d_r, c->d_p, c->S, C));
-  return RAS_OK;
-}
 
 static ras_status exchange(ras_ctx* c, Ctl C);
 
+// ---------------------------------------------------------------------------
+// Enqueue helpers shared by the sync sweep (all local subdomains batched on the
+// library stream), the async loop (one subdomain on its own stream) and the
+// scripted lock-step mode.  Range.lp < 0 = every local subdomain.
+// ---------------------------------------------------------------------------
+Range range_all(ras_ctx* c) { return Range{0, (unsigned)c->ntiles, -1}; }
+Range range_sub(ras_ctx* c, int lp) {
+  const auto& S = c->plan->subs[lp];
+  return Range{S.tile_begin, (unsigned)S.ntiles, lp};
+}
+
+// a1+a2 (+ Jacobi PCG start)
+ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
+  if (!c->ic)
+    LAUNCH_ON(s, K_RES, k_residual<true><<<R.ntiles, kThreads, 0, s>>>(R.tile_base, c->T, c->R, c->d_b, c->d_diag,
+                                                                 c->d_own_slot, c->d_x, c->d_r, c->d_p, c->S, C));
+  else
+    LAUNCH_ON(s, K_RES, k_residual<false><<<R.ntiles, kThreads, 0, s>>>(R.tile_base, c->T, c->R, c->d_b, c->d_diag,
+                                                                  c->d_own_slot, c->d_x, c->d_r, c->d_p, c->S, C));
+  return RAS_OK;
+}
+
+// z = M^-1 in via the forward (L) and backward (L^T / U) level-scheduled solves
+static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, const double* in, double* z) {
+  for (int dir = 0; dir < 2; ++dir) {
+    const TriBuf& T = dir == 0 ? c->tri_f : c->tri_b;
+    uint32_t* ctr = c->d_trsv_ctr + dir * (c->nl + 1) + (R.lp < 0 ? c->nl : R.lp);
+    int32_t* done = T.d_lev_done;
+    RAS_CUDA(c, cudaMemsetAsync(ctr, 0, 4, s));
+    int32_t c0 = 0, nch = T.nchunks;
+    if (R.lp < 0) {
+      RAS_CUDA(c, cudaMemsetAsync(done, 0, (size_t)T.nlev_slots * 4, s));
+    } else {
+      c0 = T.sub_c0[R.lp];
+      nch = T.sub_nc[R.lp];
+      RAS_CUDA(c, cudaMemsetAsync(done + T.sub_lev_off[R.lp], 0, (size_t)T.sub_nlev[R.lp] * 4, s));
+    }
+    const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));
+    const double* src = dir == 0 ? in : c->d_q;  // forward: in -> y (in q), backward: y -> z
+    double* dst = dir == 0 ? c->d_q : z;
+    LAUNCH_ON(s, K_TRSV, k_trsv<<<g, kThreads, 0, s>>>(T.dev, R.lp < 0, c0, nch, ctr, done, src, dst, c->S.active, C));
+  }
+  return RAS_OK;
+}
+
+static ras_status poll_inactive(ras_ctx* c, cudaStream_t s, const Range& R, bool* all_done) {
+  if (R.lp < 0) {
+    LAUNCH_ON(s, K_CTRL, k_count_active<<<1, 32, 0, s>>>(c->nl, c->S.active, c->d_nactive));
+    RAS_CUDA(c, cudaMemcpyAsync(c->h_nactive + c->nl, c->d_nactive, 4, cudaMemcpyDeviceToHost, s));
+    RAS_CUDA(c, cudaStreamSynchronize(s));
+    *all_done = c->h_nactive[c->nl] == 0;
+  } else {
+    RAS_CUDA(c, cudaMemcpyAsync(c->h_nactive + R.lp, c->S.active + R.lp, 4, cudaMemcpyDeviceToHost, s));
+    RAS_CUDA(c, cudaStreamSynchronize(s));
+    *all_done = c->h_nactive[R.lp] == 0;
+  }
+  return RAS_OK;
+}
+
+// a3: local PCG solve (m iterations; exact mode polls every 16 iterations)
+ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol, bool exact) {
+  const unsigned g = R.ntiles;
+  const int64_t tb = R.tile_base;
+  if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
+    TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
+    LAUNCH_ON(s, K_ZDOT, k_zdot<true><<<g, kThreads, 0, s>>>(tb, c->T, c->d_r, c->d_z, c->d_p, c->S, C));
+  }
+  for (int it = 1; it <= m; ++it) {
+    const bool last = it == m;
+    LAUNCH_ON(s, K_SPMV, k_spmv_dot<<<g, kThreads, 0, s>>>(tb, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C));
+    if (!c->ic) {
+      LAUNCH_ON(s, K_UPD, k_update_dot<true><<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d,
+                                                              c->S, C, m, inner_tol));
+      if (!last) LAUNCH_ON(s, K_PUPD, k_pupdate<<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_r, c->d_p, c->S, C));
+    } else {
+      LAUNCH_ON(s, K_UPD, k_update_dot<false><<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d,
+                                                               c->S, C, m, inner_tol));
+      if (!last) {
+        TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
+        LAUNCH_ON(s, K_ZDOT, k_zdot<false><<<g, kThreads, 0, s>>>(tb, c->T, c->d_r, c->d_z, c->d_p, c->S, C));
+        LAUNCH_ON(s, K_PUPD, k_pupdate_z<<<g, kThreads, 0, s>>>(tb, c->T, c->d_z, c->d_p, c->S, C));
+      }
+    }
+    if (exact && it % 16 == 0) {
+      bool done = false;
+      TRY(poll_inactive(c, s, R, &done));
+      if (done) break;
+    }
+  }
+  return RAS_OK;
+}
+
+// a4
+ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
+  LAUNCH_ON(s, K_PROL, k_prolong<<<R.ntiles, kThreads, 0, s>>>(R.tile_base, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C));
+  return RAS_OK;
+}
+
 static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact, int slot) {
-  const unsigned g = (unsigned)c->ntiles;
-  Ctl C{c->d_stop};
+  Ctl C{c->d_stop, 0};
+  const Range R = range_all(c);
   // a1+a2
-  LAUNCH(K_RES, k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x,
-                                                          c->d_r, c->d_p, c->S, C));
+  TRY(enq_residual(c, c->stream, R, C));
   // a6 (global criterion on x^k, P344-346)
   LAUNCH(K_CTRL, k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local));
   const double* r2g = c->d_r2_local;
@@ -348,22 +493,9 @@ static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, d
   LAUNCH(K_CTRL, k_sync_check<<<1, 32, 0, c->stream>>>(r2g, c->b2_global, tol, max_iters, c->d_sync, c->d_stop,
                                                        c->h_stop_dev + slot));
   // a3
-  if (!exact) {
-    for (int it = 1; it <= m; ++it) TRY(launch_pcg_iter(c, m, inner_tol, it == m));
-  } else {
-    // exact mode: iterate until every local subdomain stops (checked every 16 iterations)
-    for (int it = 1; it <= m; ++it) {
-      TRY(launch_pcg_iter(c, m, inner_tol, it == m));
-      if (it % 16 == 0) {
-        LAUNCH(K_CTRL, k_count_active<<<1, 32, 0, c->stream>>>(c->nl, c->S.active, c->d_nactive));
-        RAS_CUDA(c, cudaMemcpyAsync(c->h_nactive, c->d_nactive, 4, cudaMemcpyDeviceToHost, c->stream));
-        RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-        if (*c->h_nactive == 0) break;
-      }
-    }
-  }
+  TRY(enq_pcg(c, c->stream, R, C, m, inner_tol, exact));
   // a4
-  LAUNCH(K_PROL, k_prolong<<<g, kThreads, 0, c->stream>>>(0, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C));
+  TRY(enq_prolong(c, c->stream, R, C));
   // a5
   TRY(exchange(c, C));
   RAS_CUDA(c, cudaGetLastError());
@@ -643,7 +775,8 @@ static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   const double rows = (double)std::max<int64_t>(c->plan->rows_local, 1);
   for (int i = 0; i < c->nl; ++i) frac_iters += (double)it[i] * (double)c->plan->subs[i].nrows / rows;
   c->st.model_bytes = (double)c->st.sweeps * (c->mb.residual + c->mb.prolong + c->mb.pack) +
-                      frac_iters * (c->mb.spmv_dot + c->mb.update_dot + c->mb.pupdate);
+                      frac_iters * (c->mb.spmv_dot + c->mb.update_dot + c->mb.pupdate +
+                                    (c->ic ? 2.0 * c->mb.trsv + c->mb.zdot : 0.0));
 }
 
 ras_status ras_solve(ras_ctx* c, double tol, int64_t max_iters, ras_mode mode, const double* x0, double* x_out) {
@@ -702,10 +835,11 @@ ras_status ras_kernel_timing(ras_ctx* c, int32_t enable) {
 
 ras_status ras_kernel_times(const ras_ctx* c, ras_kernel_time_t* out, int32_t max_entries, int32_t* n_out) {
   if (!c || !n_out) return RAS_EINVAL;
-  static const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", "k_update_dot", "k_pupdate",
-                                        "k_prolong",  "k_pack",     "control"};
-  const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate,
-                                  c->mb.prolong,  c->mb.pack,     0.0};
+  static const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", c->ic ? "k_update_dot<ic>" : "k_update_dot",
+                                        c->ic ? "k_pupdate_z" : "k_pupdate", "k_prolong", "k_pack", "control",
+                                        "k_trsv", "k_zdot"};
+  const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate, c->mb.prolong,
+                                  c->mb.pack,     0.0,            c->mb.trsv,       c->mb.zdot};
   int n = 0;
   for (int k = 0; k < K_NKINDS && n < max_entries; ++k) {
     if (!out) break;
