@@ -309,7 +309,6 @@ def main():
     if args.warmup > 0:
         solver.solve_device(1e-300, args.warmup, mode)
     barrier()
-    solver.kernel_timing(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler([local] if world == 1 else list(range(world))) as clk:
@@ -322,6 +321,18 @@ def main():
         clk.mark(1)
     ms_local = e0.elapsed_time(e1)
     stats = solver.stats()
+    # per-kernel breakdown: the same K sweeps again with every launch bracketed by
+    # CUDA events on the library stream (events between launches disable the
+    # programmatic-dependent-launch overlap, so this pass is not the value pass)
+    solver.kernel_timing(True)
+    barrier()
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    solver.solve_device(1e-300, args.steps, mode)
+    k1.record(stream)
+    barrier()
+    ms_kpass = k0.elapsed_time(k1)
     ktimes = solver.kernel_times()
     solver.kernel_timing(False)
     t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
@@ -403,6 +414,7 @@ def main():
             "roofline": roof,
             "pcg_path_gbs": pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms else None,
             "kernels": kern,
+            "kernel_pass_ms_per_step": ms_kpass / args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -79,10 +79,13 @@ struct ras_ctx {
   double* d_diag = nullptr;
   int32_t* d_own_slot = nullptr;
   ras::Sell R{}, L{};
+  int wR = 0, wL = 0;  // widest SELL slice of each matrix (kernel width dispatch)
   ras::Tiles T{};
   double* d_x = nullptr;  // storage [owned | halo]
   double* d_r = nullptr;
   double* d_p = nullptr;
+  double* d_p2 = nullptr;  // p double buffer (fused p update + SpMV)
+  bool fuse_p = false;     // options.reserved_i[0]: fuse pass 3 into the next pass 1
   double* d_q = nullptr;
   double* d_d = nullptr;
   // IC(0)/ILU(0) path (a3')

@@ -1,5 +1,5 @@
-// sm_100a kernels of one RAS sweep (scope rows a1-a5).  FP64, no tensor cores:
-// every kernel here is an HBM-streaming sparse/vector kernel.
+// sm_100a kernels of one RAS sweep (scope rows a1-a5, a3').  FP64, no tensor
+// cores: every kernel here is an HBM-streaming sparse/vector kernel.
 //
 // Layout (see include/ras_plan.h): the rank's subdomains' Omega_p rows are
 // concatenated into one padded "row space"; matrices are SELL-32 (slice = 32
@@ -8,9 +8,12 @@
 // per k).  A CTA (256 threads) processes one TILE of kRPT*256 rows that never
 // straddles subdomains; every thread owns kRPT rows (row0 + j*256 + tid) and
 // issues all their loads before using any (memory-level parallelism).
-// Per-subdomain dot products are reduced deterministically: every CTA writes
-// its partial, the last CTA of the subdomain (atomic ticket) sums the partials
-// in fixed order and applies the PCG scalar update.
+//
+// Per-subdomain dot products are reduced deterministically and without
+// atomics or CTA barriers in the streaming kernels: every WARP writes its
+// partial sums to partials[tile][warp][slot]; a small k_finish kernel (one CTA
+// per subdomain) sums them in fixed order and applies the PCG scalar update
+// (alpha, beta, stop tests) that the next streaming kernel reads.
 #pragma once
 
 #include <cstdint>
@@ -18,9 +21,10 @@
 namespace ras {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kRPT = 4;                     // rows per thread
 constexpr int kTileRows = kThreads * kRPT;  // rows per CTA tile (plan tile_rows)
-constexpr int kNP = 4;                      // partial slots per tile
+constexpr int kNP = 4;                      // partial slots per warp
 constexpr int kMaxW = 8;                    // unrolled SELL width (wider slices take the loop path)
 
 struct Tiles {
@@ -47,7 +51,7 @@ struct Scal {
   int32_t* its;    // PCG iterations performed this sweep
   uint32_t* ticket;
   int64_t* inner_total;  // PCG iterations accumulated over the solve
-  double* partials;  // ntiles * kNP
+  double* partials;      // ntiles * kWarps * kNP
 };
 
 // Stop control: sync = one global word (per_sub = 0); async = one word per
@@ -56,6 +60,14 @@ struct Ctl {
   const volatile int32_t* stop;
   int32_t per_sub;
 };
+
+// Programmatic dependent launch: let the next kernel of the stream be scheduled
+// now, then wait for the full completion (and memory) of the previous kernel.
+// Both are no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_start() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 __device__ __forceinline__ bool stopped(const Ctl& C, int lp) {
   return C.stop && C.stop[C.per_sub ? lp : 0];
@@ -67,63 +79,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Deterministic block sum of NV values; result valid in thread 0.
+// Each warp writes its NV partial sums of tile t (lane 0 after a shuffle tree).
 template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double (*sh)[kThreads / 32]) {
+__device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, double* partials) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    double s = warp_sum(v[j]);
-    if (lane == 0) sh[j][w] = s;
+    const double s = warp_sum(v[j]);
+    if (lane == 0) partials[(t * kWarps + w) * kNP + j] = s;
   }
-  __syncthreads();
-  if (w == 0) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      double s = lane < kThreads / 32 ? sh[j][lane] : 0.0;
-      s = warp_sum(s);
-      v[j] = s;
-    }
-  }
-  __syncthreads();
-}
-
-// Writes this tile's partials; returns true in every thread of the CTA that
-// is the last one of subdomain lp to finish (that CTA then owns the reduction).
-template <int NV>
-__device__ __forceinline__ bool tile_partials_last(const double (&v)[NV], int64_t t, int lp, const Tiles& T,
-                                                   const Scal& S) {
-  __shared__ int s_last;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) S.partials[t * kNP + j] = v[j];
-    __threadfence();
-    const uint32_t prev = atomicAdd(&S.ticket[lp], 1u);
-    s_last = (prev == (uint32_t)T.sub_ntiles[lp] - 1u);
-  }
-  __syncthreads();
-  return s_last != 0;
-}
-
-// In the last CTA: fixed-order sum of subdomain lp's partials (result in thread 0).
-template <int NV>
-__device__ __forceinline__ void reduce_sub_partials(double (&out)[NV], int lp, const Tiles& T, const Scal& S,
-                                                    double (*sh)[kThreads / 32]) {
-  __threadfence();
-  const int64_t tb = T.sub_tile_begin[lp];
-  const int nt = T.sub_ntiles[lp];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) out[j] = 0.0;
-  for (int i = threadIdx.x; i < nt; i += kThreads) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) out[j] += __ldcg(&S.partials[(tb + i) * kNP + j]);
-  }
-  block_sum<NV>(out, sh);
 }
 
 // Sum_k val[e_k] * x[col[e_k]] over SELL-32 row `row` (entries in ascending
 // column order as stored).  Matrix data is streamed with evict-first loads so
 // the gathered vector keeps its L2 lines.
+// W > 0: every slice of the matrix is at most W wide (host-dispatched, fully
+// unrolled, predicated on the slice's own width); W == 0: generic loop.
+template <int W>
 __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const double* __restrict__ x) {
   const int64_t s = row >> 5;
   const int lane = (int)(row & 31);
@@ -132,17 +104,17 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
   const double* vp = M.val + base + lane;
   const int32_t* cp = M.col + base + lane;
   double acc = 0.0;
-  if (w <= kMaxW) {
-    double v[kMaxW];
-    int32_t c[kMaxW];
+  if (W > 0) {
+    double v[W > 0 ? W : 1];
+    int32_t c[W > 0 ? W : 1];
 #pragma unroll
-    for (int k = 0; k < kMaxW; ++k)
+    for (int k = 0; k < W; ++k)
       if (k < w) {
         v[k] = __ldcs(vp + 32 * k);
         c[k] = __ldcs(cp + 32 * k);
       }
 #pragma unroll
-    for (int k = 0; k < kMaxW; ++k)
+    for (int k = 0; k < W; ++k)
       if (k < w) acc += v[k] * __ldg(&x[c[k]]);
   } else {
     for (int k = 0; k < w; ++k) acc += __ldcs(vp + 32 * k) * __ldg(&x[__ldcs(cp + 32 * k)]);
@@ -150,140 +122,175 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
   return acc;
 }
 
+#define RAS_ROWS_LOOP(j) \
+  _Pragma("unroll") for (int j = 0; j < kRPT; ++j) if (j * kThreads + (int)threadIdx.x < ti.y)
+#define RAS_ROW(j) ((int64_t)ti.x + j * kThreads + threadIdx.x)
+
 // ---------------------------------------------------------------------------
-// a1+a2: restrict + residual + PCG start.
-//   r = b~ - [A_p|B_p] x (x read in place from owned/halo storage: restrict),
-//   JAC: z = D^-1 r, p = z; partials: rho = r.z, ||r~||^2, owned ||r~||^2.
-//   !JAC (IC(0)/ILU(0)): only r and the norms; z = M^-1 r follows (trsv).
+// a1+a2: restrict + residual (+ Jacobi PCG start).
+//   r = b~ - [A_p|B_p] x (x read in place from owned/halo storage: restrict);
+//   JAC: z = D^-1 r, p = z.  Partials: r.z, ||r~||^2, owned ||r~||^2.
 // ---------------------------------------------------------------------------
-template <bool JAC = true>
+template <bool JAC, int W>
 static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base, Tiles T, Sell R,
                                                               const double* __restrict__ b,
                                                               const double* __restrict__ diag,
                                                               const int32_t* __restrict__ own_slot,
                                                               const double* __restrict__ x, double* __restrict__ r,
                                                               double* __restrict__ p, Scal S, Ctl C) {
-  __shared__ double sh[3][kThreads / 32];
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
-  const int lp = ti.z;
-  if (stopped(C, lp)) return;
+  if (stopped(C, ti.z)) return;
   double v[3] = {0.0, 0.0, 0.0};
   double bi[kRPT], di[kRPT], ax[kRPT];
   int32_t os[kRPT];
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      const int64_t row = ti.x + lr;
-      bi[j] = __ldcs(&b[row]);
-      di[j] = __ldcs(&diag[row]);
-      os[j] = __ldcs(&own_slot[row]);
+  RAS_ROWS_LOOP(j) {
+    bi[j] = __ldcs(&b[RAS_ROW(j)]);
+    if (JAC) di[j] = __ldcs(&diag[RAS_ROW(j)]);
+    os[j] = __ldcs(&own_slot[RAS_ROW(j)]);
+  }
+  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W>(R, RAS_ROW(j), x);
+  RAS_ROWS_LOOP(j) {
+    const double ri = bi[j] - ax[j];
+    r[RAS_ROW(j)] = ri;
+    if (JAC) {
+      const double zi = __drcp_rn(di[j]) * ri;
+      p[RAS_ROW(j)] = zi;
+      v[0] += ri * zi;
     }
+    v[1] += ri * ri;
+    v[2] += os[j] >= 0 ? ri * ri : 0.0;
   }
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) ax[j] = sell_dot(R, ti.x + lr, x);
-  }
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      const int64_t row = ti.x + lr;
-      const double ri = bi[j] - ax[j];
-      r[row] = ri;
-      if (JAC) {
-        const double zi = __drcp_rn(di[j]) * ri;
-        p[row] = zi;
-        v[0] += ri * zi;
-      }
-      v[1] += ri * ri;
-      v[2] += os[j] >= 0 ? ri * ri : 0.0;
-    }
-  }
-  block_sum<3>(v, sh);
-  if (tile_partials_last<3>(v, t, lp, T, S)) {
-    double o[3];
-    reduce_sub_partials<3>(o, lp, T, S, sh);
-    if (threadIdx.x == 0) {
-      S.rho[lp] = o[0];
-      S.rt2[lp] = o[1];
-      S.own2[lp] = o[2];
-      S.rr[lp] = o[1];
-      // "if rho == 0: break" (R7); IC path: decided after z = M^-1 r (k_zdot<true>)
-      S.active[lp] = JAC ? (o[0] != 0.0) : 1;
-      S.its[lp] = 0;
-      S.ticket[lp] = 0u;
-    }
-  }
+  warp_partials<3>(v, t, S.partials);
 }
 
-// a3 pass 1: q = A_p p (diag + SELL off-diagonal), sigma = p.q; last CTA: alpha.
+// a3 pass 1: q = A_p p (diag + SELL off-diagonal); partial p.q.
+template <int W>
 static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base, Tiles T, Sell L,
                                                               const double* __restrict__ diag,
                                                               const double* __restrict__ p, double* __restrict__ q,
                                                               Scal S, Ctl C) {
-  __shared__ double sh[1][kThreads / 32];
+  pdl_start();
+  const int64_t t = tile_base + blockIdx.x;
+  const int4 ti = T.tile[t];
+  if (stopped(C, ti.z) || !S.active[ti.z]) return;
+  double v[1] = {0.0};
+  double pi[kRPT], di[kRPT], ax[kRPT];
+  RAS_ROWS_LOOP(j) {
+    pi[j] = __ldg(&p[RAS_ROW(j)]);
+    di[j] = __ldcs(&diag[RAS_ROW(j)]);
+  }
+  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W>(L, RAS_ROW(j), p);
+  RAS_ROWS_LOOP(j) {
+    const double qi = di[j] * pi[j] + ax[j];
+    q[RAS_ROW(j)] = qi;
+    v[0] += pi[j] * qi;
+  }
+  warp_partials<1>(v, t, S.partials);
+}
+
+// p_new = z + beta p_old, z = D^-1 r (Jacobi) or z from the trisolves (IC):
+// one expression so that a row's own value and its neighbours' recomputation
+// of it are bitwise identical.
+template <bool IC>
+__device__ __forceinline__ double p_next(double g_or_z, double r, double po, double beta, bool first) {
+  const double z = IC ? g_or_z : __drcp_rn(g_or_z) * r;
+  return first ? z : z + beta * po;
+}
+
+// a3 pass 3 of iteration it-1 fused into pass 1 of iteration it (double-
+// buffered p): p_new = z + beta p_old for the tile's rows AND, recomputed on
+// the fly, for every column it touches; q = A_p p_new; partial p_new.q.
+// FIRST (it = 1): p_new = z (beta and p_old unused).
+template <int W, bool IC, bool FIRST>
+static __global__ void __launch_bounds__(kThreads) k_spmv_pdot(int64_t tile_base, Tiles T, Sell L,
+                                                               const double* __restrict__ diag,
+                                                               const double* __restrict__ zr,  // r (Jacobi) | z (IC)
+                                                               const double* __restrict__ p_old,
+                                                               double* __restrict__ p_new, double* __restrict__ q,
+                                                               Scal S, Ctl C) {
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
+  const double beta = FIRST ? 0.0 : S.beta[lp];
   double v[1] = {0.0};
   double pi[kRPT], di[kRPT], ax[kRPT];
+  // the gathered arrays stay in L1 (ld.global.nc, L1-allocating): neighbours in
+  // the same slice hit the lines this warp just loaded
+  for (int j = 0; j < kRPT; ++j) {
+    const int lr = j * kThreads + threadIdx.x;
+    if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
+      di[j] = __ldg(&diag[row]);
+      const double a = IC ? __ldg(&zr[row]) : di[j];
+      pi[j] = p_next<IC>(a, IC ? 0.0 : __ldg(&zr[row]), FIRST ? 0.0 : __ldg(&p_old[row]), beta, FIRST);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < kRPT; ++j) {
     const int lr = j * kThreads + threadIdx.x;
     if (lr < ti.y) {
       const int64_t row = ti.x + lr;
-      pi[j] = __ldg(&p[row]);
-      di[j] = __ldcs(&diag[row]);
-    }
-  }
+      const int64_t s = row >> 5;
+      const int lane = (int)(row & 31);
+      const int64_t base = __ldg(&L.sptr[s]);
+      const int w = (int)((__ldg(&L.sptr[s + 1]) - base) >> 5);
+      const double* vp = L.val + base + lane;
+      const int32_t* cp = L.col + base + lane;
+      double acc = 0.0;
+      if (W > 0) {
+        double vv[W > 0 ? W : 1];
+        int32_t cc[W > 0 ? W : 1];
 #pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) ax[j] = sell_dot(L, ti.x + lr, p);
+        for (int k = 0; k < W; ++k)
+          if (k < w) {
+            vv[k] = __ldcs(vp + 32 * k);
+            cc[k] = __ldcs(cp + 32 * k);
+          }
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          if (k < w) {
+            const int32_t c = cc[k];
+            const double gz = IC ? __ldg(&zr[c]) : __ldg(&diag[c]);
+            acc += vv[k] * p_next<IC>(gz, IC ? 0.0 : __ldg(&zr[c]), FIRST ? 0.0 : __ldg(&p_old[c]), beta, FIRST);
+          }
+      } else {
+        for (int k = 0; k < w; ++k) {
+          const int32_t c = __ldcs(cp + 32 * k);
+          const double gz = IC ? __ldg(&zr[c]) : __ldg(&diag[c]);
+          acc += __ldcs(vp + 32 * k) *
+                 p_next<IC>(gz, IC ? 0.0 : __ldg(&zr[c]), FIRST ? 0.0 : __ldg(&p_old[c]), beta, FIRST);
+        }
+      }
+      ax[j] = acc;
+    }
   }
 #pragma unroll
   for (int j = 0; j < kRPT; ++j) {
     const int lr = j * kThreads + threadIdx.x;
     if (lr < ti.y) {
+      const int64_t row = ti.x + lr;
       const double qi = di[j] * pi[j] + ax[j];
-      q[ti.x + lr] = qi;
+      p_new[row] = pi[j];
+      q[row] = qi;
       v[0] += pi[j] * qi;
     }
   }
-  block_sum<1>(v, sh);
-  if (tile_partials_last<1>(v, t, lp, T, S)) {
-    double o[1];
-    reduce_sub_partials<1>(o, lp, T, S, sh);
-    if (threadIdx.x == 0) {
-      const double sigma = o[0];
-      if (sigma == 0.0) {  // "if sigma == 0: break" (R7)
-        S.active[lp] = 0;
-        S.alpha[lp] = 0.0;
-      } else {
-        S.alpha[lp] = S.rho[lp] / sigma;
-        S.its[lp] += 1;
-        S.inner_total[lp] += 1;
-      }
-      S.ticket[lp] = 0u;
-    }
-  }
+  warp_partials<1>(v, t, S.partials);
 }
 
-// a3 pass 2: d += alpha p (d = alpha p on the first iteration), r -= alpha q,
-// JAC: z = D^-1 r; partials r.z, r.r; last CTA: inner stop test, beta, rho.
-// !JAC: only r.r (inner stop test, iteration cap); rho' after the trisolves.
+// a3 pass 2: d += alpha p (d = alpha p on the first iteration), r -= alpha q;
+// JAC: z = D^-1 r, partials r.z, r.r.  !JAC: partial r.r only.
 template <bool JAC = true>
 static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T,
                                                                 const double* __restrict__ diag,
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ q, double* __restrict__ r,
-                                                                double* __restrict__ d, Scal S, Ctl C, int32_t m,
-                                                                double inner_tol) {
-  __shared__ double sh[2][kThreads / 32];
+                                                                double* __restrict__ d, Scal S, Ctl C) {
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
   const int lp = ti.z;
@@ -292,80 +299,138 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
   const bool first = S.its[lp] == 1;
   double v[2] = {0.0, 0.0};
   double pi[kRPT], qi[kRPT], ri[kRPT], di[kRPT], gi[kRPT];
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      const int64_t row = ti.x + lr;
-      pi[j] = __ldcs(&p[row]);
-      qi[j] = __ldcs(&q[row]);
-      ri[j] = __ldcs(&r[row]);
-      if (JAC) gi[j] = __ldcs(&diag[row]);
-      di[j] = first ? 0.0 : __ldcs(&d[row]);
-    }
+  RAS_ROWS_LOOP(j) {
+    pi[j] = __ldcs(&p[RAS_ROW(j)]);
+    qi[j] = __ldcs(&q[RAS_ROW(j)]);
+    ri[j] = __ldcs(&r[RAS_ROW(j)]);
+    if (JAC) gi[j] = __ldcs(&diag[RAS_ROW(j)]);
+    di[j] = first ? 0.0 : __ldcs(&d[RAS_ROW(j)]);
   }
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      const int64_t row = ti.x + lr;
-      const double dn = first ? alpha * pi[j] : di[j] + alpha * pi[j];
-      const double rn = ri[j] - alpha * qi[j];
-      d[row] = dn;
-      r[row] = rn;
-      if (JAC) {
-        const double zi = __drcp_rn(gi[j]) * rn;
-        v[0] += rn * zi;
-      }
-      v[1] += rn * rn;
-    }
+  RAS_ROWS_LOOP(j) {
+    const double dn = first ? alpha * pi[j] : di[j] + alpha * pi[j];
+    const double rn = ri[j] - alpha * qi[j];
+    d[RAS_ROW(j)] = dn;
+    r[RAS_ROW(j)] = rn;
+    if (JAC) v[0] += rn * (__drcp_rn(gi[j]) * rn);
+    v[1] += rn * rn;
   }
-  block_sum<2>(v, sh);
-  if (tile_partials_last<2>(v, t, lp, T, S)) {
-    double o[2];
-    reduce_sub_partials<2>(o, lp, T, S, sh);
-    if (threadIdx.x == 0) {
-      S.rr[lp] = o[1];
-      if (inner_tol > 0.0 && sqrt(o[1]) <= inner_tol * sqrt(S.rt2[lp])) {
-        S.active[lp] = 0;  // inner tolerance reached (exact mode / eta)
-      } else if (!JAC) {
-        if (S.its[lp] >= m) S.active[lp] = 0;  // z, rho', p of the last iteration are never used
-      } else {
-        const double rho_new = o[0];
-        S.beta[lp] = rho_new / S.rho[lp];
-        S.rho[lp] = rho_new;
-        if (S.its[lp] >= m || rho_new == 0.0) S.active[lp] = 0;
-      }
-      S.ticket[lp] = 0u;
-    }
-  }
+  warp_partials<2>(v, t, S.partials);
 }
 
-// a3 pass 3: p = D^-1 r + beta p.
+// a3 pass 3 (Jacobi): p = D^-1 r + beta p.
 static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, Tiles T,
                                                              const double* __restrict__ diag,
                                                              const double* __restrict__ r, double* __restrict__ p,
                                                              Scal S, Ctl C) {
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
   const double beta = S.beta[lp];
   double gi[kRPT], ri[kRPT], pi[kRPT];
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      const int64_t row = ti.x + lr;
-      gi[j] = __ldcs(&diag[row]);
-      ri[j] = __ldcs(&r[row]);
-      pi[j] = __ldcs(&p[row]);
-    }
+  RAS_ROWS_LOOP(j) {
+    gi[j] = __ldcs(&diag[RAS_ROW(j)]);
+    ri[j] = __ldcs(&r[RAS_ROW(j)]);
+    pi[j] = __ldcs(&p[RAS_ROW(j)]);
   }
+  RAS_ROWS_LOOP(j) p[RAS_ROW(j)] = __drcp_rn(gi[j]) * ri[j] + beta * pi[j];
+}
+
+// ---------------------------------------------------------------------------
+// Per-subdomain scalar steps of PCG (SURVEY §8c "Exact recurrences"), one CTA
+// per subdomain: fixed-order sum of the warp partials of its tiles, then
+//   F_RES_JAC : rho = r.z, ||r~||^2, owned ||r~||^2; active = rho != 0 (R7)
+//   F_RES_IC  : ||r~||^2, owned ||r~||^2 (rho after z = M^-1 r)
+//   F_SPMV    : sigma = p.q; sigma == 0 -> stop (R7) else alpha = rho/sigma, its++
+//   F_UPD_JAC : rr; inner stop (||r|| <= eta ||r~||) ; else beta = rho'/rho, rho = rho',
+//               stop when its == m or rho' == 0
+//   F_UPD_IC  : rr; inner stop; its == m -> stop
+//   F_ZDOT0   : rho = r.z, active = rho != 0          (IC path, PCG start)
+//   F_ZDOT    : beta = rho'/rho, rho = rho'; rho' == 0 -> stop
+// ---------------------------------------------------------------------------
+enum FinishOp { F_RES_JAC = 0, F_RES_IC, F_SPMV, F_UPD_JAC, F_UPD_IC, F_ZDOT0, F_ZDOT };
+
+constexpr int kFinThreads = 1024;
+
+template <int OP>
+static __global__ void __launch_bounds__(kFinThreads) k_finish(int lp_base, Tiles T, Scal S, Ctl C, int32_t m,
+                                                               double inner_tol) {
+  constexpr int NV = (OP == F_RES_JAC || OP == F_RES_IC) ? 3 : (OP == F_UPD_JAC || OP == F_UPD_IC) ? 2 : 1;
+  constexpr int U = 4;  // independent loads in flight per thread
+  __shared__ double sh[NV][kFinThreads / 32];
+  const int lp = lp_base + blockIdx.x;
+  pdl_start();
+  if (stopped(C, lp)) return;
+  if (OP != F_RES_JAC && OP != F_RES_IC && !S.active[lp]) return;
+  const int64_t base = T.sub_tile_begin[lp] * kWarps;
+  const int n = T.sub_ntiles[lp] * kWarps;
+  double v[NV];
 #pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) p[ti.x + lr] = __drcp_rn(gi[j]) * ri[j] + beta * pi[j];
+  for (int j = 0; j < NV; ++j) v[j] = 0.0;
+  for (int i0 = threadIdx.x; i0 < n; i0 += U * kFinThreads) {
+    double a[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kFinThreads;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) a[u][j] = i < n ? __ldcg(&S.partials[(base + i) * kNP + j]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < NV; ++j) v[j] += a[u][j];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double s = warp_sum(v[j]);
+    if (lane == 0) sh[j][w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double o[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    o[j] = 0.0;
+    for (int k = 0; k < kFinThreads / 32; ++k) o[j] += sh[j][k];
+  }
+  if (OP == F_RES_JAC || OP == F_RES_IC) {
+    if (OP == F_RES_JAC) S.rho[lp] = o[0];
+    S.rt2[lp] = o[1];
+    S.own2[lp] = o[2];
+    S.rr[lp] = o[1];
+    S.active[lp] = OP == F_RES_JAC ? (o[0] != 0.0) : 1;
+    S.its[lp] = 0;
+  } else if (OP == F_SPMV) {
+    if (o[0] == 0.0) {
+      S.active[lp] = 0;
+      S.alpha[lp] = 0.0;
+    } else {
+      S.alpha[lp] = S.rho[lp] / o[0];
+      S.its[lp] += 1;
+      S.inner_total[lp] += 1;
+    }
+  } else if (OP == F_UPD_JAC || OP == F_UPD_IC) {
+    const double rr = o[NV - 1];
+    S.rr[lp] = rr;
+    if (inner_tol > 0.0 && sqrt(rr) <= inner_tol * sqrt(S.rt2[lp])) {
+      S.active[lp] = 0;  // inner tolerance reached (exact mode / eta)
+    } else if (OP == F_UPD_IC) {
+      if (S.its[lp] >= m) S.active[lp] = 0;  // z, rho', p of the last iteration are never used
+    } else {
+      const double rho_new = o[0];
+      S.beta[lp] = rho_new / S.rho[lp];
+      S.rho[lp] = rho_new;
+      if (S.its[lp] >= m || rho_new == 0.0) S.active[lp] = 0;
+    }
+  } else if (OP == F_ZDOT0) {
+    S.rho[lp] = o[0];
+    S.active[lp] = o[0] != 0.0;
+  } else {  // F_ZDOT
+    S.beta[lp] = o[0] / S.rho[lp];
+    S.rho[lp] = o[0];
+    if (o[0] == 0.0) S.active[lp] = 0;
   }
 }
 
@@ -402,6 +467,7 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
                                                           const double* __restrict__ in, double* out,
                                                           const int32_t* __restrict__ active, Ctl C) {
   __shared__ int s_c;
+  pdl_start();
   for (;;) {
     if (threadIdx.x == 0) s_c = (int)atomicAdd(counter, 1u);
     __syncthreads();
@@ -434,76 +500,44 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
   }
 }
 
-// IC path, after z = M^-1 r.  INIT (PCG start): p = z, rho = r.z, active = rho != 0.
-// !INIT: rho' = r.z, beta = rho'/rho, rho = rho' (rho' == 0 -> stop, R7).
+// IC path, after z = M^-1 r: partial r.z (INIT: also p = z).
 template <bool INIT>
 static __global__ void __launch_bounds__(kThreads) k_zdot(int64_t tile_base, Tiles T, const double* __restrict__ r,
                                                           const double* __restrict__ z, double* __restrict__ p, Scal S,
                                                           Ctl C) {
-  __shared__ double sh[1][kThreads / 32];
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
-  const int lp = ti.z;
-  if (stopped(C, lp) || !S.active[lp]) return;
+  if (stopped(C, ti.z) || !S.active[ti.z]) return;
   double v[1] = {0.0};
   double ri[kRPT], zi[kRPT];
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      ri[j] = __ldcs(&r[ti.x + lr]);
-      zi[j] = __ldcs(&z[ti.x + lr]);
-    }
+  RAS_ROWS_LOOP(j) {
+    ri[j] = __ldcs(&r[RAS_ROW(j)]);
+    zi[j] = __ldcs(&z[RAS_ROW(j)]);
   }
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      v[0] += ri[j] * zi[j];
-      if (INIT) p[ti.x + lr] = zi[j];
-    }
+  RAS_ROWS_LOOP(j) {
+    v[0] += ri[j] * zi[j];
+    if (INIT) p[RAS_ROW(j)] = zi[j];
   }
-  block_sum<1>(v, sh);
-  if (tile_partials_last<1>(v, t, lp, T, S)) {
-    double o[1];
-    reduce_sub_partials<1>(o, lp, T, S, sh);
-    if (threadIdx.x == 0) {
-      if (INIT) {
-        S.rho[lp] = o[0];
-        S.active[lp] = o[0] != 0.0;
-      } else {
-        S.beta[lp] = o[0] / S.rho[lp];
-        S.rho[lp] = o[0];
-        if (o[0] == 0.0) S.active[lp] = 0;
-      }
-      S.ticket[lp] = 0u;
-    }
-  }
+  warp_partials<1>(v, t, S.partials);
 }
 
 // IC path: p = z + beta p.
 static __global__ void __launch_bounds__(kThreads) k_pupdate_z(int64_t tile_base, Tiles T,
                                                                const double* __restrict__ z, double* __restrict__ p,
                                                                Scal S, Ctl C) {
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
   const double beta = S.beta[lp];
   double zi[kRPT], pi[kRPT];
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      zi[j] = __ldcs(&z[ti.x + lr]);
-      pi[j] = __ldcs(&p[ti.x + lr]);
-    }
+  RAS_ROWS_LOOP(j) {
+    zi[j] = __ldcs(&z[RAS_ROW(j)]);
+    pi[j] = __ldcs(&p[RAS_ROW(j)]);
   }
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) p[ti.x + lr] = zi[j] + beta * pi[j];
-  }
+  RAS_ROWS_LOOP(j) p[RAS_ROW(j)] = zi[j] + beta * pi[j];
 }
 
 // a4: restricted prolongation x[S_p] += d[S_p] (overlap part of d discarded).
@@ -511,20 +545,21 @@ static __global__ void __launch_bounds__(kThreads) k_prolong(int64_t tile_base, 
                                                              const int32_t* __restrict__ own_slot,
                                                              const double* __restrict__ d, double* __restrict__ x,
                                                              Scal S, Ctl C) {
+  pdl_start();
   const int64_t t = tile_base + blockIdx.x;
   const int4 ti = T.tile[t];
-  const int lp = ti.z;
-  if (stopped(C, lp) || S.its[lp] == 0) return;  // no PCG step taken: d == 0
-#pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
-    if (lr < ti.y) {
-      const int64_t row = ti.x + lr;
-      const int32_t s = __ldcs(&own_slot[row]);
-      if (s >= 0) x[s] = x[s] + __ldcs(&d[row]);
-    }
+  if (stopped(C, ti.z) || S.its[ti.z] == 0) return;  // no PCG step taken: d == 0
+  int32_t os[kRPT];
+  double di[kRPT];
+  RAS_ROWS_LOOP(j) {
+    os[j] = __ldcs(&own_slot[RAS_ROW(j)]);
+    di[j] = __ldcs(&d[RAS_ROW(j)]);
   }
+  RAS_ROWS_LOOP(j) if (os[j] >= 0) x[os[j]] = x[os[j]] + di[j];
 }
+
+#undef RAS_ROWS_LOOP
+#undef RAS_ROW
 
 // a5 (sync): pack owned values for the NCCL sends.
 static __global__ void k_pack(int64_t count, const int32_t* __restrict__ slots, const double* __restrict__ x,

@@ -118,9 +118,15 @@ static void compute_model_bytes(ras_ctx* c) {
   // compulsory bytes, real (unpadded) rows and entries
   c->mb.residual = rows * (8 /*b*/ + 8 /*diag*/ + 4 /*own_slot*/ + 8 /*x*/ + 8 /*r*/ + 8 /*p*/) +
                    (double)pl->nnz_residual * 12.0;
-  c->mb.spmv_dot = rows * (8 /*p*/ + 8 /*diag*/ + 8 /*q*/) + nnz_off * 12.0;
+  if (c->fuse_p) {
+    // pass 1 with the fused p update: r (or z), diag, p_old in; p_new, q out (+ off-diagonal entries)
+    c->mb.spmv_dot = rows * (8 /*r|z*/ + 8 /*diag*/ + 8 /*p_old*/ + 8 /*p_new*/ + 8 /*q*/) + nnz_off * 12.0;
+    c->mb.pupdate = 0.0;
+  } else {
+    c->mb.spmv_dot = rows * (8 /*p*/ + 8 /*diag*/ + 8 /*q*/) + nnz_off * 12.0;
+    c->mb.pupdate = rows * (8 /*diag*/ + 8 /*r*/ + 16 /*p*/);
+  }
   c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + 8 /*diag*/ + 16 /*r*/ + 16 /*d*/);
-  c->mb.pupdate = rows * (8 /*diag*/ + 8 /*r*/ + 16 /*p*/);
   c->mb.prolong = rows * 4.0 + (double)owned * (8 /*d*/ + 16 /*x*/);
   c->mb.pack = (double)c->n_send * (4 + 8 + 8);
 }
@@ -171,7 +177,7 @@ static ras_status upload_factors(ras_ctx* c) {
   c->ic = true;
   const double rows = (double)c->plan->rows_local;
   c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + 16 /*r*/ + 16 /*d*/);
-  c->mb.pupdate = rows * (8 /*z*/ + 16 /*p*/);
+  c->mb.pupdate = c->fuse_p ? 0.0 : rows * (8 /*z*/ + 16 /*p*/);
   c->mb.trsv = 0.5 * (c->tri_f.bytes + c->tri_b.bytes);
   c->mb.zdot = rows * 16.0;
   return RAS_OK;
@@ -198,6 +204,11 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(upload(c, &ci, pl->L_col, 1));
   TRY(upload(c, &va, pl->L_val, 1));
   c->L = Sell{sp, ci, va};
+  c->wR = c->wL = 0;
+  for (size_t s = 0; s + 1 < pl->R_sptr.size(); ++s) {
+    c->wR = std::max<int>(c->wR, (int)((pl->R_sptr[s + 1] - pl->R_sptr[s]) / 32));
+    c->wL = std::max<int>(c->wL, (int)((pl->L_sptr[s + 1] - pl->L_sptr[s]) / 32));
+  }
   std::vector<int64_t> stb(c->nl);
   std::vector<int32_t> snt(c->nl);
   for (int i = 0; i < c->nl; ++i) {
@@ -219,6 +230,7 @@ static ras_status upload_plan(ras_ctx* c) {
   if (!c->d_x) return set_err(c, RAS_ENOMEM, "device allocation failed (x storage)");
   TRY(zalloc(c, &c->d_r, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_p, (size_t)c->rows_pad));
+  TRY(zalloc(c, &c->d_p2, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_q, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_d, (size_t)c->rows_pad));
   const int nl = c->nl;
@@ -232,7 +244,7 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(zalloc(c, &c->S.its, nl));
   TRY(zalloc(c, &c->S.ticket, nl));
   TRY(zalloc(c, &c->S.inner_total, nl));
-  TRY(zalloc(c, &c->S.partials, (size_t)c->ntiles * kNP));
+  TRY(zalloc(c, &c->S.partials, (size_t)c->ntiles * kWarps * kNP));
   TRY(zalloc(c, &c->d_stop, 1));
   TRY(zalloc(c, &c->d_sync, 1));
   TRY(zalloc(c, &c->d_r2_local, 1));
@@ -374,6 +386,26 @@ static void kt_collect(ras_ctx* c) {
   } while (0)
 #define LAUNCH(kind, ...) LAUNCH_ON(c->stream, kind, __VA_ARGS__)
 
+// Programmatic dependent launch (sm_90+): the next kernel of the PCG chain is
+// scheduled while the previous one drains; every kernel starts with
+// griddepcontrol.launch_dependents + griddepcontrol.wait (kernels.cuh), so
+// the data dependence is still the full completion of the predecessor.
+template <typename Kern, typename... Args>
+static void pdl_launch(cudaStream_t s, unsigned grid, unsigned block, Kern k, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+#define KL(strm, kind, grid, block, KERNEL, ...) LAUNCH_ON(strm, kind, pdl_launch(strm, grid, block, KERNEL, __VA_ARGS__))
+
 // ---------------------------------------------------------------------------
 // Sync sweep (lock-step, P155-161, P376-387): stream-ordered on one stream.
 // ---------------------------------------------------------------------------
@@ -392,13 +424,40 @@ Range range_sub(ras_ctx* c, int lp) {
 }
 
 // a1+a2 (+ Jacobi PCG start)
+// per-subdomain scalar step after a streaming kernel (one CTA per subdomain in R)
+template <int OP>
+static void enq_finish(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m = 0, double inner_tol = 0.0) {
+  const unsigned nsub = R.lp < 0 ? (unsigned)c->nl : 1u;
+  KL(s, K_CTRL, nsub, kFinThreads, k_finish<OP>, R.lp < 0 ? 0 : R.lp, c->T, c->S, C, m, inner_tol);
+}
+
+// SELL width dispatch: the smallest unrolled width >= the matrix's widest slice
+#define RAS_DISPATCH_W(w, CALL) \
+  switch ((w) <= 4 ? 4 : (w) <= 5 ? 5 : (w) <= 6 ? 6 : (w) <= 7 ? 7 : (w) <= 8 ? 8 : 0) { \
+    case 4: CALL(4); break;                                                                \
+    case 5: CALL(5); break;                                                                \
+    case 6: CALL(6); break;                                                                \
+    case 7: CALL(7); break;                                                                \
+    case 8: CALL(8); break;                                                                \
+    default: CALL(0); break;                                                               \
+  }
+
 ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
-  if (!c->ic)
-    LAUNCH_ON(s, K_RES, k_residual<true><<<R.ntiles, kThreads, 0, s>>>(R.tile_base, c->T, c->R, c->d_b, c->d_diag,
-                                                                 c->d_own_slot, c->d_x, c->d_r, c->d_p, c->S, C));
-  else
-    LAUNCH_ON(s, K_RES, k_residual<false><<<R.ntiles, kThreads, 0, s>>>(R.tile_base, c->T, c->R, c->d_b, c->d_diag,
-                                                                  c->d_own_slot, c->d_x, c->d_r, c->d_p, c->S, C));
+#define RAS_RES(JAC, W)                                                                                         \
+  KL(s, K_RES, R.ntiles, kThreads, (k_residual<JAC, W>), R.tile_base, c->T, c->R, (const double*)c->d_b,       \
+     (const double*)c->d_diag, (const int32_t*)c->d_own_slot, (const double*)c->d_x, c->d_r, c->d_p, c->S, C)
+#define RAS_RES_J(W) RAS_RES(true, W)
+#define RAS_RES_I(W) RAS_RES(false, W)
+  if (!c->ic) {
+    RAS_DISPATCH_W(c->wR, RAS_RES_J);
+    enq_finish<F_RES_JAC>(c, s, R, C);
+  } else {
+    RAS_DISPATCH_W(c->wR, RAS_RES_I);
+    enq_finish<F_RES_IC>(c, s, R, C);
+  }
+#undef RAS_RES_I
+#undef RAS_RES_J
+#undef RAS_RES
   return RAS_OK;
 }
 
@@ -420,7 +479,8 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
     const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));
     const double* src = dir == 0 ? in : c->d_q;  // forward: in -> y (in q), backward: y -> z
     double* dst = dir == 0 ? c->d_q : z;
-    LAUNCH_ON(s, K_TRSV, k_trsv<<<g, kThreads, 0, s>>>(T.dev, R.lp < 0, c0, nch, ctr, done, src, dst, c->S.active, C));
+    KL(s, K_TRSV, g, kThreads, k_trsv, T.dev, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
+       (const int32_t*)c->S.active, C);
   }
   return RAS_OK;
 }
@@ -445,22 +505,64 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
   const int64_t tb = R.tile_base;
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
     TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
-    LAUNCH_ON(s, K_ZDOT, k_zdot<true><<<g, kThreads, 0, s>>>(tb, c->T, c->d_r, c->d_z, c->d_p, c->S, C));
+    KL(s, K_ZDOT, g, kThreads, k_zdot<true>, tb, c->T, (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
+    enq_finish<F_ZDOT0>(c, s, R, C);
   }
   for (int it = 1; it <= m; ++it) {
     const bool last = it == m;
-    LAUNCH_ON(s, K_SPMV, k_spmv_dot<<<g, kThreads, 0, s>>>(tb, c->T, c->L, c->d_diag, c->d_p, c->d_q, c->S, C));
-    if (!c->ic) {
-      LAUNCH_ON(s, K_UPD, k_update_dot<true><<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d,
-                                                              c->S, C, m, inner_tol));
-      if (!last) LAUNCH_ON(s, K_PUPD, k_pupdate<<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_r, c->d_p, c->S, C));
+    // p double buffer: iteration it writes p_new, reads p_old (p of it-1)
+    double* p_new = c->fuse_p ? ((it & 1) ? c->d_p : c->d_p2) : c->d_p;
+    const double* p_old = c->fuse_p ? ((it & 1) ? c->d_p2 : c->d_p) : c->d_p;
+    const double* zr = c->ic ? c->d_z : c->d_r;
+#define RAS_SPMV_V(W, IC, FIRST)                                                                                  \
+  KL(s, K_SPMV, g, kThreads, (k_spmv_pdot<W, IC, FIRST>), tb, c->T, c->L, (const double*)c->d_diag, zr, p_old, \
+     p_new, c->d_q, c->S, C)
+#define RAS_SPMV_JF(W) RAS_SPMV_V(W, false, true)
+#define RAS_SPMV_JN(W) RAS_SPMV_V(W, false, false)
+#define RAS_SPMV_IF(W) RAS_SPMV_V(W, true, true)
+#define RAS_SPMV_IN(W) RAS_SPMV_V(W, true, false)
+#define RAS_SPMV_PLAIN(W)                                                                                      \
+  KL(s, K_SPMV, g, kThreads, (k_spmv_dot<W>), tb, c->T, c->L, (const double*)c->d_diag, (const double*)p_new, \
+     c->d_q, c->S, C)
+    if (!c->fuse_p) {
+      // p_new was written by the previous iteration's p update (or the PCG start)
+      RAS_DISPATCH_W(c->wL, RAS_SPMV_PLAIN);
+    } else if (!c->ic) {
+      if (it == 1) {
+        RAS_DISPATCH_W(c->wL, RAS_SPMV_JF);
+      } else {
+        RAS_DISPATCH_W(c->wL, RAS_SPMV_JN);
+      }
     } else {
-      LAUNCH_ON(s, K_UPD, k_update_dot<false><<<g, kThreads, 0, s>>>(tb, c->T, c->d_diag, c->d_p, c->d_q, c->d_r, c->d_d,
-                                                               c->S, C, m, inner_tol));
+      if (it == 1) {
+        RAS_DISPATCH_W(c->wL, RAS_SPMV_IF);
+      } else {
+        RAS_DISPATCH_W(c->wL, RAS_SPMV_IN);
+      }
+    }
+#undef RAS_SPMV_PLAIN
+#undef RAS_SPMV_IN
+#undef RAS_SPMV_IF
+#undef RAS_SPMV_JN
+#undef RAS_SPMV_JF
+#undef RAS_SPMV_V
+    enq_finish<F_SPMV>(c, s, R, C);
+    if (!c->ic) {
+      KL(s, K_UPD, g, kThreads, k_update_dot<true>, tb, c->T, (const double*)c->d_diag, (const double*)p_new,
+         (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
+      enq_finish<F_UPD_JAC>(c, s, R, C, m, inner_tol);
+      if (!c->fuse_p && !last)
+        KL(s, K_PUPD, g, kThreads, k_pupdate, tb, c->T, (const double*)c->d_diag, (const double*)c->d_r, c->d_p, c->S,
+           C);
+    } else {
+      KL(s, K_UPD, g, kThreads, k_update_dot<false>, tb, c->T, (const double*)c->d_diag, (const double*)p_new,
+         (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
+      enq_finish<F_UPD_IC>(c, s, R, C, m, inner_tol);
       if (!last) {
         TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
-        LAUNCH_ON(s, K_ZDOT, k_zdot<false><<<g, kThreads, 0, s>>>(tb, c->T, c->d_r, c->d_z, c->d_p, c->S, C));
-        LAUNCH_ON(s, K_PUPD, k_pupdate_z<<<g, kThreads, 0, s>>>(tb, c->T, c->d_z, c->d_p, c->S, C));
+        KL(s, K_ZDOT, g, kThreads, k_zdot<false>, tb, c->T, (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
+        enq_finish<F_ZDOT>(c, s, R, C);
+        if (!c->fuse_p) KL(s, K_PUPD, g, kThreads, k_pupdate_z, tb, c->T, (const double*)c->d_z, c->d_p, c->S, C);
       }
     }
     if (exact && it % 16 == 0) {
@@ -474,7 +576,8 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 
 // a4
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
-  LAUNCH_ON(s, K_PROL, k_prolong<<<R.ntiles, kThreads, 0, s>>>(R.tile_base, c->T, c->d_own_slot, c->d_d, c->d_x, c->S, C));
+  KL(s, K_PROL, R.ntiles, kThreads, k_prolong, R.tile_base, c->T, (const int32_t*)c->d_own_slot, (const double*)c->d_d,
+     c->d_x, c->S, C);
   return RAS_OK;
 }
 
@@ -527,10 +630,8 @@ ras_status sync_exchange(ras_ctx* c) { return exchange(c, Ctl{nullptr, 0}); }
 // True relative residual ||b - A x|| / ||b|| of the stored iterate (halo must be
 // current): one residual pass over every tile + owned partial sums + allreduce.
 ras_status global_residual(ras_ctx* c, double* rel) {
-  const unsigned g = (unsigned)c->ntiles;
   Ctl C{nullptr, 0};
-  LAUNCH(K_RES, k_residual<<<g, kThreads, 0, c->stream>>>(0, c->T, c->R, c->d_b, c->d_diag, c->d_own_slot, c->d_x,
-                                                          c->d_r, c->d_p, c->S, C));
+  TRY(enq_residual(c, c->stream, range_all(c), C));
   LAUNCH(K_CTRL, k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local));
   const double* r2g = c->d_r2_local;
   if (c->world > 1) {
@@ -685,6 +786,7 @@ ras_status ras_setup(ras_ctx** out, const ras_csr* A, const double* b, const ras
   ras_options_default(&c->opt);
   if (opt) c->opt = *opt;
   if (c->opt.inner_iters < 1) c->opt.inner_iters = 1;
+  c->fuse_p = c->opt.reserved_i[0] != 0;
   if (c->opt.inner_tol < 0) {
     set_tls_error("inner_tol must be >= 0");
     delete c;
