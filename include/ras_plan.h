@@ -42,7 +42,8 @@ typedef struct {
   int64_t sell_residual;      /* padded SELL-32 entries, residual matrix */
   int64_t sell_local;         /* padded SELL-32 entries, local off-diagonal matrix */
   int64_t ntiles;
-  int32_t finalized, reserved;
+  int32_t finalized;
+  int32_t z_format;           /* 1 = the compressed SELL-Z copy exists (dictionary values, 16-bit column offsets) */
 } ras_plan_info;
 
 /* Phase 1 (local): validate inputs, build Omega_p / Gamma_p for this rank's

@@ -66,7 +66,7 @@ class RasPlanInfo(C.Structure):
                 ("local_subdomains", I32), ("tile_rows", I32), ("n_own", I64), ("n_halo", I64),
                 ("rows_local", I64), ("rows_padded", I64), ("nnz_residual", I64), ("nnz_local", I64),
                 ("sell_residual", I64), ("sell_local", I64), ("ntiles", I64), ("finalized", I32),
-                ("reserved", I32)]
+                ("z_format", I32)]
 
 
 class RasKernelTime(C.Structure):

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libras_b200.so")
-SOURCES = ["plan.cpp", "factor.cpp", "solver.cu", "async.cu"]
+SOURCES = ["plan.cpp", "factor.cpp", "zformat.cpp", "solver.cu", "async.cu"]
 
 
 def nccl_dir() -> str:

@@ -80,6 +80,8 @@ struct ras_ctx {
   int32_t* d_own_slot = nullptr;
   ras::Sell R{}, L{};
   int wR = 0, wL = 0;  // widest SELL slice of each matrix (kernel width dispatch)
+  bool z = false;      // SELL-Z compressed matrices + diagonal on the device
+  ras::Diag D{};
   ras::Tiles T{};
   double* d_x = nullptr;  // storage [owned | halo]
   double* d_r = nullptr;

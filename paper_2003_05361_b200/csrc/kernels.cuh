@@ -31,13 +31,35 @@ struct Tiles {
   const int4* tile;               // {row0, nrows, local subdomain, 0}
   const int64_t* sub_tile_begin;  // per local subdomain
   const int32_t* sub_ntiles;
+  int64_t ntiles;                 // all tiles of the rank (partials stride)
 };
 
+// SELL-32 matrix.  Plain: FP64 values + int32 columns.  Compressed (Z, see
+// zformat.cpp): uint8 value codes into `table` + per-(slice, k) int32 column
+// base + uint16 offsets.  Both decode to the same entries.
 struct Sell {
   const int64_t* sptr;
   const int32_t* col;
   const double* val;
+  const int32_t* kbase;  // Z: per slice column k (< 0: -(wide group) - 1)
+  const uint16_t* d16;   // Z: column = kbase + d16
+  const int32_t* wide;   // Z: int32 columns of wide groups
+  const uint8_t* code;   // Z: value = table[code]
+  const double* table;
 };
+
+// Diagonal of A_p: FP64, or (Z) uint8 codes into the shared value table.
+struct Diag {
+  const double* v;
+  const uint8_t* code;
+  const double* table;
+};
+
+template <bool Z>
+__device__ __forceinline__ double diag_at(const Diag& D, int64_t row) {
+  if (Z) return __ldg(&D.table[__ldcs(&D.code[row])]);
+  return __ldcs(&D.v[row]);
+}
 
 // Per local subdomain scalars (struct of arrays, one allocation each).
 struct Scal {
@@ -79,14 +101,25 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Each warp writes its NV partial sums of tile t (lane 0 after a shuffle tree).
+// The CTA's NV partial sums of tile t (shuffle trees, one CTA barrier, fixed
+// order), stored slot-major: partials[j * ntiles + t].  No fence, no atomic:
+// the per-subdomain k_finish kernel that follows in stream order reads them.
 template <int NV>
-__device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, double* partials) {
+__device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, int64_t ntiles, double* partials) {
+  __shared__ double sh[NV][kWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const double s = warp_sum(v[j]);
-    if (lane == 0) partials[(t * kWarps + w) * kNP + j] = s;
+    if (lane == 0) sh[j][w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const double s = warp_sum(lane < kWarps ? sh[j][lane] : 0.0);
+      if (lane == 0) partials[j * ntiles + t] = s;
+    }
   }
 }
 
@@ -95,15 +128,41 @@ __device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, 
 // the gathered vector keeps its L2 lines.
 // W > 0: every slice of the matrix is at most W wide (host-dispatched, fully
 // unrolled, predicated on the slice's own width); W == 0: generic loop.
-template <int W>
+template <int W, bool Z = false>
 __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const double* __restrict__ x) {
   const int64_t s = row >> 5;
   const int lane = (int)(row & 31);
   const int64_t base = __ldg(&M.sptr[s]);
   const int w = (int)((__ldg(&M.sptr[s + 1]) - base) >> 5);
+  double acc = 0.0;
+  if (Z) {
+    const uint8_t* vc = M.code + base + lane;
+    const uint16_t* dp = M.d16 + base + lane;
+    const int32_t* kb = M.kbase + (base >> 5);
+    if (W > 0) {
+      uint8_t v[W > 0 ? W : 1];
+      int32_t c[W > 0 ? W : 1];
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (k < w) {
+          v[k] = __ldcs(vc + 32 * k);
+          const int32_t b = __ldg(kb + k);  // warp-uniform
+          c[k] = b >= 0 ? b + (int32_t)__ldcs(dp + 32 * k) : __ldg(&M.wide[(-b - 1) * 32 + lane]);
+        }
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (k < w) acc += __ldg(&M.table[v[k]]) * __ldg(&x[c[k]]);
+    } else {
+      for (int k = 0; k < w; ++k) {
+        const int32_t b = __ldg(kb + k);
+        const int32_t c = b >= 0 ? b + (int32_t)__ldcs(dp + 32 * k) : __ldg(&M.wide[(-b - 1) * 32 + lane]);
+        acc += __ldg(&M.table[__ldcs(vc + 32 * k)]) * __ldg(&x[c]);
+      }
+    }
+    return acc;
+  }
   const double* vp = M.val + base + lane;
   const int32_t* cp = M.col + base + lane;
-  double acc = 0.0;
   if (W > 0) {
     double v[W > 0 ? W : 1];
     int32_t c[W > 0 ? W : 1];
@@ -131,10 +190,9 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
 //   r = b~ - [A_p|B_p] x (x read in place from owned/halo storage: restrict);
 //   JAC: z = D^-1 r, p = z.  Partials: r.z, ||r~||^2, owned ||r~||^2.
 // ---------------------------------------------------------------------------
-template <bool JAC, int W>
+template <bool JAC, int W, bool Z>
 static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base, Tiles T, Sell R,
-                                                              const double* __restrict__ b,
-                                                              const double* __restrict__ diag,
+                                                              const double* __restrict__ b, Diag D,
                                                               const int32_t* __restrict__ own_slot,
                                                               const double* __restrict__ x, double* __restrict__ r,
                                                               double* __restrict__ p, Scal S, Ctl C) {
@@ -147,10 +205,10 @@ static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base,
   int32_t os[kRPT];
   RAS_ROWS_LOOP(j) {
     bi[j] = __ldcs(&b[RAS_ROW(j)]);
-    if (JAC) di[j] = __ldcs(&diag[RAS_ROW(j)]);
+    if (JAC) di[j] = diag_at<Z>(D, RAS_ROW(j));
     os[j] = __ldcs(&own_slot[RAS_ROW(j)]);
   }
-  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W>(R, RAS_ROW(j), x);
+  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W, Z>(R, RAS_ROW(j), x);
   RAS_ROWS_LOOP(j) {
     const double ri = bi[j] - ax[j];
     r[RAS_ROW(j)] = ri;
@@ -162,13 +220,12 @@ static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base,
     v[1] += ri * ri;
     v[2] += os[j] >= 0 ? ri * ri : 0.0;
   }
-  warp_partials<3>(v, t, S.partials);
+  warp_partials<3>(v, t, T.ntiles, S.partials);
 }
 
 // a3 pass 1: q = A_p p (diag + SELL off-diagonal); partial p.q.
-template <int W>
-static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base, Tiles T, Sell L,
-                                                              const double* __restrict__ diag,
+template <int W, bool Z>
+static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base, Tiles T, Sell L, Diag D,
                                                               const double* __restrict__ p, double* __restrict__ q,
                                                               Scal S, Ctl C) {
   pdl_start();
@@ -179,15 +236,15 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base,
   double pi[kRPT], di[kRPT], ax[kRPT];
   RAS_ROWS_LOOP(j) {
     pi[j] = __ldg(&p[RAS_ROW(j)]);
-    di[j] = __ldcs(&diag[RAS_ROW(j)]);
+    di[j] = diag_at<Z>(D, RAS_ROW(j));
   }
-  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W>(L, RAS_ROW(j), p);
+  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W, Z>(L, RAS_ROW(j), p);
   RAS_ROWS_LOOP(j) {
     const double qi = di[j] * pi[j] + ax[j];
     q[RAS_ROW(j)] = qi;
     v[0] += pi[j] * qi;
   }
-  warp_partials<1>(v, t, S.partials);
+  warp_partials<1>(v, t, T.ntiles, S.partials);
 }
 
 // p_new = z + beta p_old, z = D^-1 r (Jacobi) or z from the trisolves (IC):
@@ -279,14 +336,13 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_pdot(int64_t tile_base
       v[0] += pi[j] * qi;
     }
   }
-  warp_partials<1>(v, t, S.partials);
+  warp_partials<1>(v, t, T.ntiles, S.partials);
 }
 
 // a3 pass 2: d += alpha p (d = alpha p on the first iteration), r -= alpha q;
 // JAC: z = D^-1 r, partials r.z, r.r.  !JAC: partial r.r only.
-template <bool JAC = true>
-static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T,
-                                                                const double* __restrict__ diag,
+template <bool JAC, bool Z>
+static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T, Diag D,
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ q, double* __restrict__ r,
                                                                 double* __restrict__ d, Scal S, Ctl C) {
@@ -303,7 +359,7 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
     pi[j] = __ldcs(&p[RAS_ROW(j)]);
     qi[j] = __ldcs(&q[RAS_ROW(j)]);
     ri[j] = __ldcs(&r[RAS_ROW(j)]);
-    if (JAC) gi[j] = __ldcs(&diag[RAS_ROW(j)]);
+    if (JAC) gi[j] = diag_at<Z>(D, RAS_ROW(j));
     di[j] = first ? 0.0 : __ldcs(&d[RAS_ROW(j)]);
   }
   RAS_ROWS_LOOP(j) {
@@ -314,12 +370,12 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
     if (JAC) v[0] += rn * (__drcp_rn(gi[j]) * rn);
     v[1] += rn * rn;
   }
-  warp_partials<2>(v, t, S.partials);
+  warp_partials<2>(v, t, T.ntiles, S.partials);
 }
 
 // a3 pass 3 (Jacobi): p = D^-1 r + beta p.
-static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, Tiles T,
-                                                             const double* __restrict__ diag,
+template <bool Z>
+static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, Tiles T, Diag D,
                                                              const double* __restrict__ r, double* __restrict__ p,
                                                              Scal S, Ctl C) {
   pdl_start();
@@ -330,7 +386,7 @@ static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, 
   const double beta = S.beta[lp];
   double gi[kRPT], ri[kRPT], pi[kRPT];
   RAS_ROWS_LOOP(j) {
-    gi[j] = __ldcs(&diag[RAS_ROW(j)]);
+    gi[j] = diag_at<Z>(D, RAS_ROW(j));
     ri[j] = __ldcs(&r[RAS_ROW(j)]);
     pi[j] = __ldcs(&p[RAS_ROW(j)]);
   }
@@ -363,8 +419,8 @@ static __global__ void __launch_bounds__(kFinThreads) k_finish(int lp_base, Tile
   pdl_start();
   if (stopped(C, lp)) return;
   if (OP != F_RES_JAC && OP != F_RES_IC && !S.active[lp]) return;
-  const int64_t base = T.sub_tile_begin[lp] * kWarps;
-  const int n = T.sub_ntiles[lp] * kWarps;
+  const int64_t base = T.sub_tile_begin[lp];
+  const int n = T.sub_ntiles[lp];
   double v[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) v[j] = 0.0;
@@ -374,7 +430,7 @@ static __global__ void __launch_bounds__(kFinThreads) k_finish(int lp_base, Tile
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kFinThreads;
 #pragma unroll
-      for (int j = 0; j < NV; ++j) a[u][j] = i < n ? __ldcg(&S.partials[(base + i) * kNP + j]) : 0.0;
+      for (int j = 0; j < NV; ++j) a[u][j] = i < n ? __ldcg(&S.partials[j * T.ntiles + base + i]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -519,7 +575,7 @@ static __global__ void __launch_bounds__(kThreads) k_zdot(int64_t tile_base, Til
     v[0] += ri[j] * zi[j];
     if (INIT) p[RAS_ROW(j)] = zi[j];
   }
-  warp_partials<1>(v, t, S.partials);
+  warp_partials<1>(v, t, T.ntiles, S.partials);
 }
 
 // IC path: p = z + beta p.

@@ -356,6 +356,7 @@ static void build_finalize(ras_plan* pl) {
       }
     }
   }
+  build_zformat(pl);
   pl->finalized = true;
 }
 
@@ -431,6 +432,7 @@ ras_status ras_plan_get_info(const ras_plan* pl, ras_plan_info* info) {
   info->sell_local = pl->L_sptr.empty() ? 0 : pl->L_sptr.back();
   info->ntiles = (int64_t)pl->tile_sub.size();
   info->finalized = pl->finalized;
+  info->z_format = pl->z_ok ? 1 : 0;
   return RAS_OK;
 }
 

@@ -92,6 +92,13 @@ struct ras_plan {
   std::vector<int32_t> Ap_col;   // subdomain-relative
   std::vector<double> Ap_val;
   int64_t nnz_residual = 0, nnz_local = 0;
+  // compressed SELL-Z copies of R, L and the diagonal (zformat.cpp); z_ok = usable
+  bool z_ok = false;
+  std::vector<double> z_table;
+  std::vector<uint8_t> R_code, L_code, D_code;
+  std::vector<int32_t> R_kbase, L_kbase;
+  std::vector<uint16_t> R_d16, L_d16;
+  std::vector<int32_t> R_wide, L_wide;  // int32 columns of the groups too wide for 16-bit offsets
   // tiles: CTA work units, never straddle subdomains
   std::vector<int32_t> tile_sub;
   std::vector<int64_t> tile_row0;
@@ -103,4 +110,6 @@ namespace ras {
 // IC(0) (kind = RAS_LS_IC0_PCG) or ILU(0) factors of every local A_p, in level
 // order: F = forward (L), B = backward (L^T or U).  Throws Fail on a pivot <= 0.
 void build_factors(ras_plan* pl, int kind, TriHost& F, TriHost& B);
+// Dictionary-coded values + base/offset columns of R, L, diag; false = not compressible.
+bool build_zformat(ras_plan* pl);
 }  // namespace ras

@@ -115,18 +115,22 @@ static void compute_model_bytes(ras_ctx* c) {
   const double rows = (double)pl->rows_local;
   int64_t owned = pl->n_own;
   const double nnz_off = (double)(pl->nnz_local - pl->rows_local);
-  // compulsory bytes, real (unpadded) rows and entries
-  c->mb.residual = rows * (8 /*b*/ + 8 /*diag*/ + 4 /*own_slot*/ + 8 /*x*/ + 8 /*r*/ + 8 /*p*/) +
-                   (double)pl->nnz_residual * 12.0;
+  // compulsory bytes, real (unpadded) rows and entries.  Plain
+  // SELL: 8 B value + 4 B column per entry, 8 B diagonal; SELL-Z: 1 B code +
+  // 2 B column offset (+ 4 B base per 32 entries), 1 B diagonal code.
+  const double eb = c->z ? (1.0 + 2.0 + 4.0 / 32.0) : 12.0;
+  const double db = c->z ? 1.0 : 8.0;
+  c->mb.residual = rows * (8 /*b*/ + db /*diag*/ + 4 /*own_slot*/ + 8 /*x*/ + 8 /*r*/ + 8 /*p*/) +
+                   (double)pl->nnz_residual * eb;
   if (c->fuse_p) {
     // pass 1 with the fused p update: r (or z), diag, p_old in; p_new, q out (+ off-diagonal entries)
     c->mb.spmv_dot = rows * (8 /*r|z*/ + 8 /*diag*/ + 8 /*p_old*/ + 8 /*p_new*/ + 8 /*q*/) + nnz_off * 12.0;
     c->mb.pupdate = 0.0;
   } else {
-    c->mb.spmv_dot = rows * (8 /*p*/ + 8 /*diag*/ + 8 /*q*/) + nnz_off * 12.0;
-    c->mb.pupdate = rows * (8 /*diag*/ + 8 /*r*/ + 16 /*p*/);
+    c->mb.spmv_dot = rows * (8 /*p*/ + db /*diag*/ + 8 /*q*/) + nnz_off * eb;
+    c->mb.pupdate = rows * (db /*diag*/ + 8 /*r*/ + 16 /*p*/);
   }
-  c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + 8 /*diag*/ + 16 /*r*/ + 16 /*d*/);
+  c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + db /*diag*/ + 16 /*r*/ + 16 /*d*/);
   c->mb.prolong = rows * 4.0 + (double)owned * (8 /*d*/ + 16 /*x*/);
   c->mb.pack = (double)c->n_send * (4 + 8 + 8);
 }
@@ -191,19 +195,48 @@ static ras_status upload_plan(ras_ctx* c) {
   c->ntiles = (int64_t)pl->tile_sub.size();
   c->nl = (int32_t)pl->subs.size();
   TRY(upload(c, &c->d_b, pl->b_loc));
-  TRY(upload(c, &c->d_diag, pl->diag));
   TRY(upload(c, &c->d_own_slot, pl->own_slot));
+  // SELL-Z (dictionary values, 16-bit column offsets) when requested
+  // (options.reserved_i[1] = 1) and the matrix allows it; the fused-p kernel
+  // reads the plain format.  Only one format lives on the device.  Measured on
+  // B200 (round 1): SELL-Z moves 2.3x fewer bytes but its extra dependent loads
+  // make the latency-bound kernels slower, so plain SELL is the default.
+  c->z = pl->z_ok && !c->fuse_p && c->opt.reserved_i[1] == 1;
   int64_t* sp;
-  int32_t* ci;
-  double* va;
-  TRY(upload(c, &sp, pl->R_sptr));
-  TRY(upload(c, &ci, pl->R_col, 1));
-  TRY(upload(c, &va, pl->R_val, 1));
-  c->R = Sell{sp, ci, va};
-  TRY(upload(c, &sp, pl->L_sptr));
-  TRY(upload(c, &ci, pl->L_col, 1));
-  TRY(upload(c, &va, pl->L_val, 1));
-  c->L = Sell{sp, ci, va};
+  if (c->z) {
+    double* tb;
+    uint8_t *rc, *lc, *dc;
+    int32_t *rk, *lk, *rw, *lw;
+    uint16_t *rd, *ld;
+    TRY(upload(c, &tb, pl->z_table, 1));
+    TRY(upload(c, &dc, pl->D_code, 1));
+    TRY(upload(c, &sp, pl->R_sptr));
+    TRY(upload(c, &rc, pl->R_code, 1));
+    TRY(upload(c, &rk, pl->R_kbase, 1));
+    TRY(upload(c, &rd, pl->R_d16, 1));
+    TRY(upload(c, &rw, pl->R_wide, 1));
+    c->R = Sell{sp, nullptr, nullptr, rk, rd, rw, rc, tb};
+    TRY(upload(c, &sp, pl->L_sptr));
+    TRY(upload(c, &lc, pl->L_code, 1));
+    TRY(upload(c, &lk, pl->L_kbase, 1));
+    TRY(upload(c, &ld, pl->L_d16, 1));
+    TRY(upload(c, &lw, pl->L_wide, 1));
+    c->L = Sell{sp, nullptr, nullptr, lk, ld, lw, lc, tb};
+    c->D = Diag{nullptr, dc, tb};
+  } else {
+    int32_t* ci;
+    double* va;
+    TRY(upload(c, &c->d_diag, pl->diag));
+    TRY(upload(c, &sp, pl->R_sptr));
+    TRY(upload(c, &ci, pl->R_col, 1));
+    TRY(upload(c, &va, pl->R_val, 1));
+    c->R = Sell{sp, ci, va, nullptr, nullptr, nullptr, nullptr, nullptr};
+    TRY(upload(c, &sp, pl->L_sptr));
+    TRY(upload(c, &ci, pl->L_col, 1));
+    TRY(upload(c, &va, pl->L_val, 1));
+    c->L = Sell{sp, ci, va, nullptr, nullptr, nullptr, nullptr, nullptr};
+    c->D = Diag{c->d_diag, nullptr, nullptr};
+  }
   c->wR = c->wL = 0;
   for (size_t s = 0; s + 1 < pl->R_sptr.size(); ++s) {
     c->wR = std::max<int>(c->wR, (int)((pl->R_sptr[s + 1] - pl->R_sptr[s]) / 32));
@@ -225,7 +258,7 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(upload(c, &ti, tiles));
   TRY(upload(c, &sb, stb));
   TRY(upload(c, &sn, snt));
-  c->T = Tiles{ti, sb, sn};
+  c->T = Tiles{ti, sb, sn, c->ntiles};
   c->d_x = (double*)dalloc_raw(c, (size_t)(c->n_own + c->n_halo) * 8);
   if (!c->d_x) return set_err(c, RAS_ENOMEM, "device allocation failed (x storage)");
   TRY(zalloc(c, &c->d_r, (size_t)c->rows_pad));
@@ -244,7 +277,7 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(zalloc(c, &c->S.its, nl));
   TRY(zalloc(c, &c->S.ticket, nl));
   TRY(zalloc(c, &c->S.inner_total, nl));
-  TRY(zalloc(c, &c->S.partials, (size_t)c->ntiles * kWarps * kNP));
+  TRY(zalloc(c, &c->S.partials, (size_t)c->ntiles * kNP));
   TRY(zalloc(c, &c->d_stop, 1));
   TRY(zalloc(c, &c->d_sync, 1));
   TRY(zalloc(c, &c->d_r2_local, 1));
@@ -443,20 +476,32 @@ static void enq_finish(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m 
   }
 
 ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
-#define RAS_RES(JAC, W)                                                                                         \
-  KL(s, K_RES, R.ntiles, kThreads, (k_residual<JAC, W>), R.tile_base, c->T, c->R, (const double*)c->d_b,       \
-     (const double*)c->d_diag, (const int32_t*)c->d_own_slot, (const double*)c->d_x, c->d_r, c->d_p, c->S, C)
-#define RAS_RES_J(W) RAS_RES(true, W)
-#define RAS_RES_I(W) RAS_RES(false, W)
+#define RAS_RES(JAC, W, Z)                                                                                  \
+  KL(s, K_RES, R.ntiles, kThreads, (k_residual<JAC, W, Z>), R.tile_base, c->T, c->R, (const double*)c->d_b, \
+     c->D, (const int32_t*)c->d_own_slot, (const double*)c->d_x, c->d_r, c->d_p, c->S, C)
+#define RAS_RES_J0(W) RAS_RES(true, W, false)
+#define RAS_RES_I0(W) RAS_RES(false, W, false)
+#define RAS_RES_JZ(W) RAS_RES(true, W, true)
+#define RAS_RES_IZ(W) RAS_RES(false, W, true)
   if (!c->ic) {
-    RAS_DISPATCH_W(c->wR, RAS_RES_J);
+    if (c->z) {
+      RAS_DISPATCH_W(c->wR, RAS_RES_JZ);
+    } else {
+      RAS_DISPATCH_W(c->wR, RAS_RES_J0);
+    }
     enq_finish<F_RES_JAC>(c, s, R, C);
   } else {
-    RAS_DISPATCH_W(c->wR, RAS_RES_I);
+    if (c->z) {
+      RAS_DISPATCH_W(c->wR, RAS_RES_IZ);
+    } else {
+      RAS_DISPATCH_W(c->wR, RAS_RES_I0);
+    }
     enq_finish<F_RES_IC>(c, s, R, C);
   }
-#undef RAS_RES_I
-#undef RAS_RES_J
+#undef RAS_RES_IZ
+#undef RAS_RES_JZ
+#undef RAS_RES_I0
+#undef RAS_RES_J0
 #undef RAS_RES
   return RAS_OK;
 }
@@ -521,12 +566,17 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 #define RAS_SPMV_JN(W) RAS_SPMV_V(W, false, false)
 #define RAS_SPMV_IF(W) RAS_SPMV_V(W, true, true)
 #define RAS_SPMV_IN(W) RAS_SPMV_V(W, true, false)
-#define RAS_SPMV_PLAIN(W)                                                                                      \
-  KL(s, K_SPMV, g, kThreads, (k_spmv_dot<W>), tb, c->T, c->L, (const double*)c->d_diag, (const double*)p_new, \
-     c->d_q, c->S, C)
+#define RAS_SPMV_P(W, Z) \
+  KL(s, K_SPMV, g, kThreads, (k_spmv_dot<W, Z>), tb, c->T, c->L, c->D, (const double*)p_new, c->d_q, c->S, C)
+#define RAS_SPMV_P0(W) RAS_SPMV_P(W, false)
+#define RAS_SPMV_PZ(W) RAS_SPMV_P(W, true)
     if (!c->fuse_p) {
       // p_new was written by the previous iteration's p update (or the PCG start)
-      RAS_DISPATCH_W(c->wL, RAS_SPMV_PLAIN);
+      if (c->z) {
+        RAS_DISPATCH_W(c->wL, RAS_SPMV_PZ);
+      } else {
+        RAS_DISPATCH_W(c->wL, RAS_SPMV_P0);
+      }
     } else if (!c->ic) {
       if (it == 1) {
         RAS_DISPATCH_W(c->wL, RAS_SPMV_JF);
@@ -540,7 +590,9 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
         RAS_DISPATCH_W(c->wL, RAS_SPMV_IN);
       }
     }
-#undef RAS_SPMV_PLAIN
+#undef RAS_SPMV_PZ
+#undef RAS_SPMV_P0
+#undef RAS_SPMV_P
 #undef RAS_SPMV_IN
 #undef RAS_SPMV_IF
 #undef RAS_SPMV_JN
@@ -548,14 +600,21 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 #undef RAS_SPMV_V
     enq_finish<F_SPMV>(c, s, R, C);
     if (!c->ic) {
-      KL(s, K_UPD, g, kThreads, k_update_dot<true>, tb, c->T, (const double*)c->d_diag, (const double*)p_new,
-         (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
+      if (c->z)
+        KL(s, K_UPD, g, kThreads, (k_update_dot<true, true>), tb, c->T, c->D, (const double*)p_new,
+           (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
+      else
+        KL(s, K_UPD, g, kThreads, (k_update_dot<true, false>), tb, c->T, c->D, (const double*)p_new,
+           (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
       enq_finish<F_UPD_JAC>(c, s, R, C, m, inner_tol);
-      if (!c->fuse_p && !last)
-        KL(s, K_PUPD, g, kThreads, k_pupdate, tb, c->T, (const double*)c->d_diag, (const double*)c->d_r, c->d_p, c->S,
-           C);
+      if (!c->fuse_p && !last) {
+        if (c->z)
+          KL(s, K_PUPD, g, kThreads, k_pupdate<true>, tb, c->T, c->D, (const double*)c->d_r, c->d_p, c->S, C);
+        else
+          KL(s, K_PUPD, g, kThreads, k_pupdate<false>, tb, c->T, c->D, (const double*)c->d_r, c->d_p, c->S, C);
+      }
     } else {
-      KL(s, K_UPD, g, kThreads, k_update_dot<false>, tb, c->T, (const double*)c->d_diag, (const double*)p_new,
+      KL(s, K_UPD, g, kThreads, (k_update_dot<false, false>), tb, c->T, c->D, (const double*)p_new,
          (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
       enq_finish<F_UPD_IC>(c, s, R, C, m, inner_tol);
       if (!last) {

@@ -59,9 +59,14 @@ _SOLVERS = {"jacobi": F.RAS_LS_JACOBI_PCG, "ic0": F.RAS_LS_IC0_PCG, "ilu0": F.RA
 _DETECTORS = {"central": F.RAS_DET_CENTRAL, "decentral": F.RAS_DET_DECENTRAL}
 
 
-def options(local_solver="jacobi", inner_iters=20, inner_tol=0.0, detector="decentral", **kw) -> F.RasOptions:
+def options(local_solver="jacobi", inner_iters=20, inner_tol=0.0, detector="decentral", fuse_p=False,
+            zfmt=False, **kw) -> F.RasOptions:
+    """ras_options.  fuse_p: fuse the PCG p update into the next SpMV (reserved_i[0]);
+    zfmt: use the compressed SELL-Z matrices when they apply (reserved_i[1])."""
     o = F.RasOptions()
     _check(F.lib().ras_options_default(C.byref(o)))
+    o.reserved_i[0] = 1 if fuse_p else 0
+    o.reserved_i[1] = 1 if zfmt else 0
     o.local_solver = _SOLVERS[local_solver] if isinstance(local_solver, str) else int(local_solver)
     o.inner_iters = int(inner_iters)
     o.inner_tol = float(inner_tol)

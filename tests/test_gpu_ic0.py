@@ -19,9 +19,10 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
+@pytest.mark.parametrize("fuse_p", [False, True])
 @pytest.mark.parametrize("kind", ["ic0", "ilu0"])
 @pytest.mark.parametrize("case", ["2d", "3d", "voronoi"])
-def test_ic_iterates_match_oracle(kind, case):
+def test_ic_iterates_match_oracle(kind, case, fuse_p):
     if case == "2d":
         A = ri.laplace_2d(48, 40)
         owner = O.partition_regular(48, 40, 1, 2, 2, 1)
@@ -39,7 +40,7 @@ def test_ic_iterates_match_oracle(kind, case):
     for s in subs:
         O.make_local_solver(s, kind, m)
     ref = O.ras_sync(A, b, subs, 1e-300, 4, record_iterates=True)
-    s = R.Solver(A, b, owner, gamma, R.options(kind, m))
+    s = R.Solver(A, b, owner, gamma, R.options(kind, m, fuse_p=fuse_p))
     for k in (1, 4):
         st, x = s.solve(1e-300, k, "sync")
         assert rel(x, ref.iterates[k]) <= 1e-10, (kind, case, k, rel(x, ref.iterates[k]))

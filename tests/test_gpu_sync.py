@@ -25,8 +25,9 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
+@pytest.mark.parametrize("fmt", ["z", "plain", "fuse_p"])
 @pytest.mark.parametrize("case", ["c1", "voronoi_ragged", "strips"])
-def test_sync_iterates_match_oracle(case):
+def test_sync_iterates_match_oracle(case, fmt):
     if case == "c1":
         nx = ny = 64
         A = ri.laplace_2d(nx)
@@ -45,7 +46,7 @@ def test_sync_iterates_match_oracle(case):
     b = ri.rhs(nx * ny, 0)
     K = 6
     ref = oracle_iterates(A, b, owner, gamma, "jacobi", m, K)
-    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m))
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", zfmt=fmt == "z"))
     for k in (1, 2, K):
         st, x = s.solve(1e-300, k, "sync")
         assert st == R._ffi.RAS_ENOCONV
@@ -139,3 +140,22 @@ def test_errors_are_reported():
     B.data[B.indptr[3]:B.indptr[4]] *= -1.0  # negative diagonal in row 3
     with pytest.raises(R.RasError, match="RAS_ENOTSPD.*subdomain 0"):
         R.Solver(B, b, np.zeros(N * N, np.int32), 1)
+
+
+def test_non_compressible_matrix_takes_plain_path():
+    # > 256 distinct values: the SELL-Z dictionary does not apply, plain FP64 SELL is used
+    N = 40
+    A = ri.laplace_2d(N)
+    rng = np.random.default_rng(3)
+    A.data = A.data * (1.0 + 0.01 * rng.random(A.nnz))
+    As = A.to_scipy()
+    As = ((As + As.T) * 0.5).tocsr()
+    As.sort_indices()
+    A2 = ri.CSR(As.indptr, As.indices, As.data, N * N)
+    owner = R.partition_regular(N, N, 1, 2, 2, 1)
+    s = R.Solver(A2, ri.rhs(N * N), owner, 2, R.options("jacobi", 8, zfmt=True))
+    assert s.plan().info()["z_format"] == 0
+    ref = oracle_iterates(A2, ri.rhs(N * N), owner, 2, "jacobi", 8, 3)
+    st, x = s.solve(1e-300, 3, "sync")
+    assert rel(x, ref.iterates[3]) <= 1e-10
+    s.close()
