@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libras_b200.so")
+LIB_PATH = os.environ.get("RAS_LIB_PATH") or os.path.join(HERE, "libras_b200.so")
 
 RAS_OK, RAS_EINVAL, RAS_ENOTSPD, RAS_ENOCONV, RAS_EVERIFY, RAS_ECUDA, RAS_ENCCL, RAS_ENOMEM, RAS_ESTATE = range(9)
 STATUS_NAMES = ["RAS_OK", "RAS_EINVAL", "RAS_ENOTSPD", "RAS_ENOCONV", "RAS_EVERIFY", "RAS_ECUDA", "RAS_ENCCL",

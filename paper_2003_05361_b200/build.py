@@ -22,14 +22,15 @@ def nccl_dir() -> str:
     return os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    OUT_ = out
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     hdrs += [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
-    if not force and os.path.exists(OUT):
-        t = os.path.getmtime(OUT)
+    if not force and os.path.exists(OUT_):
+        t = os.path.getmtime(OUT_)
         if all(os.path.getmtime(f) <= t for f in srcs + hdrs):
-            return OUT
+            return OUT_
     nd = nccl_dir()
     cmd = [
         "nvcc", "-O3", "-std=c++17", "-lineinfo",
@@ -37,7 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-Xcompiler", "-fPIC,-O3", "-shared",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(nd, "include"),
         "-Xptxas", "-v" if verbose else "-O3",
-        "-o", OUT + ".tmp", *srcs,
+        *["-D" + d for d in defines],
+        "-o", OUT_ + ".tmp", *srcs,
         "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
         "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
     ]
@@ -47,9 +49,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libras_b200.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(OUT_ + ".tmp", OUT_)
+    return OUT_
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH] [-DNAME=VAL ...]  (variants for tuning sweeps)
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else OUT
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args or bool(defs), verbose="-v" in args, out=out, defines=defs))

@@ -83,6 +83,7 @@ struct ras_ctx {
   bool z = false;      // SELL-Z compressed matrices + diagonal on the device
   ras::Diag D{};
   ras::Tiles T{};
+  int32_t dir = 0;  // tile walk direction of the last streaming launch
   double* d_x = nullptr;  // storage [owned | halo]
   double* d_r = nullptr;
   double* d_p = nullptr;

@@ -5,25 +5,60 @@
 // concatenated into one padded "row space"; matrices are SELL-32 (slice = 32
 // consecutive rows stored column-major, so lane i of a warp reads entry k of
 // row i at base + 32k + i: one coalesced 256 B value load + 128 B index load
-// per k).  A CTA (256 threads) processes one TILE of kRPT*256 rows that never
-// straddles subdomains; every thread owns kRPT rows (row0 + j*256 + tid) and
-// issues all their loads before using any (memory-level parallelism).
+// per k).  A CTA processes one TILE of kTileRows rows that never straddles
+// subdomains; each kernel has its own CTA size NT (tuned, see below) and every
+// thread owns RPT = kTileRows / NT rows (row0 + j*NT + tid), issuing all their
+// loads before using any (memory-level parallelism).  Consecutive streaming
+// launches walk the tiles in alternating directions (Tiles::rev) so each one
+// starts on the vectors the previous one left in the 126 MB L2.
 //
 // Per-subdomain dot products are reduced deterministically and without
-// atomics or CTA barriers in the streaming kernels: every WARP writes its
-// partial sums to partials[tile][warp][slot]; a small k_finish kernel (one CTA
-// per subdomain) sums them in fixed order and applies the PCG scalar update
-// (alpha, beta, stop tests) that the next streaming kernel reads.
+// atomics or fences in the streaming kernels: every CTA writes its partial
+// sums slot-major to partials[slot][tile]; a small k_finish kernel (one CTA per
+// subdomain) sums them in fixed order and applies the PCG scalar update
+// (alpha, beta, stop tests) that the next streaming kernel reads.  Kernels are
+// chained with programmatic dependent launch (pdl_start).
 #pragma once
 
 #include <cstdint>
 
 namespace ras {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;               // default CTA size (trisolve, finish helpers)
 constexpr int kWarps = kThreads / 32;
-constexpr int kRPT = 4;                     // rows per thread
-constexpr int kTileRows = kThreads * kRPT;  // rows per CTA tile (plan tile_rows)
+#ifndef RAS_RPT
+#define RAS_RPT 4
+#endif
+constexpr int kTileRows = 256 * RAS_RPT;    // rows per CTA tile (plan tile_rows)
+// Threads per CTA (and the minimum resident CTAs per SM, i.e. the register
+// budget) of each streaming kernel; rows per thread = kTileRows / threads.
+// Tuned on B200 (round 1 sweep): the gather kernels want more,
+// lighter threads (2 rows each), the pure streams 4 rows per thread.
+#ifndef RAS_NT_RES
+#define RAS_NT_RES 512
+#endif
+#ifndef RAS_MB_RES
+#define RAS_MB_RES 4
+#endif
+#ifndef RAS_NT_SPMV
+#define RAS_NT_SPMV 512
+#endif
+#ifndef RAS_MB_SPMV
+#define RAS_MB_SPMV 3
+#endif
+#ifndef RAS_NT_UPD
+#define RAS_NT_UPD 512
+#endif
+#ifndef RAS_MB_UPD
+#define RAS_MB_UPD 4
+#endif
+#ifndef RAS_NT_STREAM
+#define RAS_NT_STREAM 256
+#endif
+#ifndef RAS_MB_STREAM
+#define RAS_MB_STREAM 6
+#endif
+constexpr int kNT_RES = RAS_NT_RES, kNT_SPMV = RAS_NT_SPMV, kNT_UPD = RAS_NT_UPD, kNT_STREAM = RAS_NT_STREAM;
 constexpr int kNP = 4;                      // partial slots per warp
 constexpr int kMaxW = 8;                    // unrolled SELL width (wider slices take the loop path)
 
@@ -32,6 +67,8 @@ struct Tiles {
   const int64_t* sub_tile_begin;  // per local subdomain
   const int32_t* sub_ntiles;
   int64_t ntiles;                 // all tiles of the rank (partials stride)
+  int32_t rev;                    // walk the tiles backwards (alternates between launches so
+                                  // each kernel starts on the rows the previous one left in L2)
 };
 
 // SELL-32 matrix.  Plain: FP64 values + int32 columns.  Compressed (Z, see
@@ -104,9 +141,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // The CTA's NV partial sums of tile t (shuffle trees, one CTA barrier, fixed
 // order), stored slot-major: partials[j * ntiles + t].  No fence, no atomic:
 // the per-subdomain k_finish kernel that follows in stream order reads them.
-template <int NV>
+template <int NV, int NT>
 __device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, int64_t ntiles, double* partials) {
-  __shared__ double sh[NV][kWarps];
+  constexpr int NW = NT / 32;
+  __shared__ double sh[NV][NW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
@@ -117,7 +155,7 @@ __device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, 
   if (w == 0) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const double s = warp_sum(lane < kWarps ? sh[j][lane] : 0.0);
+      const double s = warp_sum(lane < NW ? sh[j][lane] : 0.0);
       if (lane == 0) partials[j * ntiles + t] = s;
     }
   }
@@ -181,9 +219,10 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
   return acc;
 }
 
+// each kernel defines NT (threads) and RPT = kTileRows / NT (rows per thread)
 #define RAS_ROWS_LOOP(j) \
-  _Pragma("unroll") for (int j = 0; j < kRPT; ++j) if (j * kThreads + (int)threadIdx.x < ti.y)
-#define RAS_ROW(j) ((int64_t)ti.x + j * kThreads + threadIdx.x)
+  _Pragma("unroll") for (int j = 0; j < RPT; ++j) if (j * NT + (int)threadIdx.x < ti.y)
+#define RAS_ROW(j) ((int64_t)ti.x + j * NT + threadIdx.x)
 
 // ---------------------------------------------------------------------------
 // a1+a2: restrict + residual (+ Jacobi PCG start).
@@ -191,18 +230,19 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
 //   JAC: z = D^-1 r, p = z.  Partials: r.z, ||r~||^2, owned ||r~||^2.
 // ---------------------------------------------------------------------------
 template <bool JAC, int W, bool Z>
-static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base, Tiles T, Sell R,
+static __global__ void __launch_bounds__(kNT_RES, RAS_MB_RES) k_residual(int64_t tile_base, Tiles T, Sell R,
                                                               const double* __restrict__ b, Diag D,
                                                               const int32_t* __restrict__ own_slot,
                                                               const double* __restrict__ x, double* __restrict__ r,
                                                               double* __restrict__ p, Scal S, Ctl C) {
+  constexpr int NT = kNT_RES, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   if (stopped(C, ti.z)) return;
   double v[3] = {0.0, 0.0, 0.0};
-  double bi[kRPT], di[kRPT], ax[kRPT];
-  int32_t os[kRPT];
+  double bi[RPT], di[RPT], ax[RPT];
+  int32_t os[RPT];
   RAS_ROWS_LOOP(j) {
     bi[j] = __ldcs(&b[RAS_ROW(j)]);
     if (JAC) di[j] = diag_at<Z>(D, RAS_ROW(j));
@@ -220,20 +260,21 @@ static __global__ void __launch_bounds__(kThreads) k_residual(int64_t tile_base,
     v[1] += ri * ri;
     v[2] += os[j] >= 0 ? ri * ri : 0.0;
   }
-  warp_partials<3>(v, t, T.ntiles, S.partials);
+  warp_partials<3, NT>(v, t, T.ntiles, S.partials);
 }
 
 // a3 pass 1: q = A_p p (diag + SELL off-diagonal); partial p.q.
 template <int W, bool Z>
-static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base, Tiles T, Sell L, Diag D,
+static __global__ void __launch_bounds__(kNT_SPMV, RAS_MB_SPMV) k_spmv_dot(int64_t tile_base, Tiles T, Sell L, Diag D,
                                                               const double* __restrict__ p, double* __restrict__ q,
                                                               Scal S, Ctl C) {
+  constexpr int NT = kNT_SPMV, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   if (stopped(C, ti.z) || !S.active[ti.z]) return;
   double v[1] = {0.0};
-  double pi[kRPT], di[kRPT], ax[kRPT];
+  double pi[RPT], di[RPT], ax[RPT];
   RAS_ROWS_LOOP(j) {
     pi[j] = __ldg(&p[RAS_ROW(j)]);
     di[j] = diag_at<Z>(D, RAS_ROW(j));
@@ -244,7 +285,7 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_dot(int64_t tile_base,
     q[RAS_ROW(j)] = qi;
     v[0] += pi[j] * qi;
   }
-  warp_partials<1>(v, t, T.ntiles, S.partials);
+  warp_partials<1, NT>(v, t, T.ntiles, S.partials);
 }
 
 // p_new = z + beta p_old, z = D^-1 r (Jacobi) or z from the trisolves (IC):
@@ -261,24 +302,25 @@ __device__ __forceinline__ double p_next(double g_or_z, double r, double po, dou
 // the fly, for every column it touches; q = A_p p_new; partial p_new.q.
 // FIRST (it = 1): p_new = z (beta and p_old unused).
 template <int W, bool IC, bool FIRST>
-static __global__ void __launch_bounds__(kThreads) k_spmv_pdot(int64_t tile_base, Tiles T, Sell L,
+static __global__ void __launch_bounds__(kThreads, 1) k_spmv_pdot(int64_t tile_base, Tiles T, Sell L,
                                                                const double* __restrict__ diag,
                                                                const double* __restrict__ zr,  // r (Jacobi) | z (IC)
                                                                const double* __restrict__ p_old,
                                                                double* __restrict__ p_new, double* __restrict__ q,
                                                                Scal S, Ctl C) {
+  constexpr int NT = kThreads, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
   const double beta = FIRST ? 0.0 : S.beta[lp];
   double v[1] = {0.0};
-  double pi[kRPT], di[kRPT], ax[kRPT];
+  double pi[RPT], di[RPT], ax[RPT];
   // the gathered arrays stay in L1 (ld.global.nc, L1-allocating): neighbours in
   // the same slice hit the lines this warp just loaded
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = j * NT + threadIdx.x;
     if (lr < ti.y) {
       const int64_t row = ti.x + lr;
       di[j] = __ldg(&diag[row]);
@@ -287,8 +329,8 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_pdot(int64_t tile_base
     }
   }
 #pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = j * NT + threadIdx.x;
     if (lr < ti.y) {
       const int64_t row = ti.x + lr;
       const int64_t s = row >> 5;
@@ -326,8 +368,8 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_pdot(int64_t tile_base
     }
   }
 #pragma unroll
-  for (int j = 0; j < kRPT; ++j) {
-    const int lr = j * kThreads + threadIdx.x;
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = j * NT + threadIdx.x;
     if (lr < ti.y) {
       const int64_t row = ti.x + lr;
       const double qi = di[j] * pi[j] + ax[j];
@@ -336,25 +378,26 @@ static __global__ void __launch_bounds__(kThreads) k_spmv_pdot(int64_t tile_base
       v[0] += pi[j] * qi;
     }
   }
-  warp_partials<1>(v, t, T.ntiles, S.partials);
+  warp_partials<1, NT>(v, t, T.ntiles, S.partials);
 }
 
 // a3 pass 2: d += alpha p (d = alpha p on the first iteration), r -= alpha q;
 // JAC: z = D^-1 r, partials r.z, r.r.  !JAC: partial r.r only.
 template <bool JAC, bool Z>
-static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_base, Tiles T, Diag D,
+static __global__ void __launch_bounds__(kNT_UPD, RAS_MB_UPD) k_update_dot(int64_t tile_base, Tiles T, Diag D,
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ q, double* __restrict__ r,
                                                                 double* __restrict__ d, Scal S, Ctl C) {
+  constexpr int NT = kNT_UPD, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
   const double alpha = S.alpha[lp];
   const bool first = S.its[lp] == 1;
   double v[2] = {0.0, 0.0};
-  double pi[kRPT], qi[kRPT], ri[kRPT], di[kRPT], gi[kRPT];
+  double pi[RPT], qi[RPT], ri[RPT], di[RPT], gi[RPT];
   RAS_ROWS_LOOP(j) {
     pi[j] = __ldcs(&p[RAS_ROW(j)]);
     qi[j] = __ldcs(&q[RAS_ROW(j)]);
@@ -370,21 +413,22 @@ static __global__ void __launch_bounds__(kThreads) k_update_dot(int64_t tile_bas
     if (JAC) v[0] += rn * (__drcp_rn(gi[j]) * rn);
     v[1] += rn * rn;
   }
-  warp_partials<2>(v, t, T.ntiles, S.partials);
+  warp_partials<2, NT>(v, t, T.ntiles, S.partials);
 }
 
 // a3 pass 3 (Jacobi): p = D^-1 r + beta p.
 template <bool Z>
-static __global__ void __launch_bounds__(kThreads) k_pupdate(int64_t tile_base, Tiles T, Diag D,
+static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_pupdate(int64_t tile_base, Tiles T, Diag D,
                                                              const double* __restrict__ r, double* __restrict__ p,
                                                              Scal S, Ctl C) {
+  constexpr int NT = kNT_STREAM, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
   const double beta = S.beta[lp];
-  double gi[kRPT], ri[kRPT], pi[kRPT];
+  double gi[RPT], ri[RPT], pi[RPT];
   RAS_ROWS_LOOP(j) {
     gi[j] = diag_at<Z>(D, RAS_ROW(j));
     ri[j] = __ldcs(&r[RAS_ROW(j)]);
@@ -558,15 +602,16 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
 
 // IC path, after z = M^-1 r: partial r.z (INIT: also p = z).
 template <bool INIT>
-static __global__ void __launch_bounds__(kThreads) k_zdot(int64_t tile_base, Tiles T, const double* __restrict__ r,
+static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_zdot(int64_t tile_base, Tiles T, const double* __restrict__ r,
                                                           const double* __restrict__ z, double* __restrict__ p, Scal S,
                                                           Ctl C) {
+  constexpr int NT = kNT_STREAM, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   if (stopped(C, ti.z) || !S.active[ti.z]) return;
   double v[1] = {0.0};
-  double ri[kRPT], zi[kRPT];
+  double ri[RPT], zi[RPT];
   RAS_ROWS_LOOP(j) {
     ri[j] = __ldcs(&r[RAS_ROW(j)]);
     zi[j] = __ldcs(&z[RAS_ROW(j)]);
@@ -575,20 +620,21 @@ static __global__ void __launch_bounds__(kThreads) k_zdot(int64_t tile_base, Til
     v[0] += ri[j] * zi[j];
     if (INIT) p[RAS_ROW(j)] = zi[j];
   }
-  warp_partials<1>(v, t, T.ntiles, S.partials);
+  warp_partials<1, NT>(v, t, T.ntiles, S.partials);
 }
 
 // IC path: p = z + beta p.
-static __global__ void __launch_bounds__(kThreads) k_pupdate_z(int64_t tile_base, Tiles T,
+static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_pupdate_z(int64_t tile_base, Tiles T,
                                                                const double* __restrict__ z, double* __restrict__ p,
                                                                Scal S, Ctl C) {
+  constexpr int NT = kNT_STREAM, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   const int lp = ti.z;
   if (stopped(C, lp) || !S.active[lp]) return;
   const double beta = S.beta[lp];
-  double zi[kRPT], pi[kRPT];
+  double zi[RPT], pi[RPT];
   RAS_ROWS_LOOP(j) {
     zi[j] = __ldcs(&z[RAS_ROW(j)]);
     pi[j] = __ldcs(&p[RAS_ROW(j)]);
@@ -597,16 +643,17 @@ static __global__ void __launch_bounds__(kThreads) k_pupdate_z(int64_t tile_base
 }
 
 // a4: restricted prolongation x[S_p] += d[S_p] (overlap part of d discarded).
-static __global__ void __launch_bounds__(kThreads) k_prolong(int64_t tile_base, Tiles T,
+static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_prolong(int64_t tile_base, Tiles T,
                                                              const int32_t* __restrict__ own_slot,
                                                              const double* __restrict__ d, double* __restrict__ x,
                                                              Scal S, Ctl C) {
+  constexpr int NT = kNT_STREAM, RPT = kTileRows / NT;
   pdl_start();
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   if (stopped(C, ti.z) || S.its[ti.z] == 0) return;  // no PCG step taken: d == 0
-  int32_t os[kRPT];
-  double di[kRPT];
+  int32_t os[RPT];
+  double di[RPT];
   RAS_ROWS_LOOP(j) {
     os[j] = __ldcs(&own_slot[RAS_ROW(j)]);
     di[j] = __ldcs(&d[RAS_ROW(j)]);

@@ -53,7 +53,10 @@ struct SubPlan {
 struct ras_plan {
   int64_t n = 0;
   int32_t P = 0, rank = 0, world = 1, gamma = 0;
-  int32_t tile_rows = 1024;  // must equal ras::kTileRows (kernels.cuh)
+#ifndef RAS_RPT
+#define RAS_RPT 4
+#endif
+  int32_t tile_rows = 256 * RAS_RPT;  // must equal ras::kTileRows (kernels.cuh)
   std::vector<int32_t> sub_to_rank;
   std::vector<ras::SubPlan> subs;  // local subdomains, ascending global id
   int64_t n_own = 0, n_halo = 0;

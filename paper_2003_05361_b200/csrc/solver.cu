@@ -464,6 +464,19 @@ static void enq_finish(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m 
   KL(s, K_CTRL, nsub, kFinThreads, k_finish<OP>, R.lp < 0 ? 0 : R.lp, c->T, c->S, C, m, inner_tol);
 }
 
+// Streaming kernels walk the tiles alternately forwards and backwards, so each
+// starts on the rows whose vectors the previous kernel left in L2.
+static Tiles tiles_next(ras_ctx* c) {
+  Tiles t = c->T;
+  c->dir ^= 1;
+#ifdef RAS_NOREV
+  t.rev = 0;
+#else
+  t.rev = c->dir;
+#endif
+  return t;
+}
+
 // SELL width dispatch: the smallest unrolled width >= the matrix's widest slice
 #define RAS_DISPATCH_W(w, CALL) \
   switch ((w) <= 4 ? 4 : (w) <= 5 ? 5 : (w) <= 6 ? 6 : (w) <= 7 ? 7 : (w) <= 8 ? 8 : 0) { \
@@ -477,7 +490,7 @@ static void enq_finish(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m 
 
 ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
 #define RAS_RES(JAC, W, Z)                                                                                  \
-  KL(s, K_RES, R.ntiles, kThreads, (k_residual<JAC, W, Z>), R.tile_base, c->T, c->R, (const double*)c->d_b, \
+  KL(s, K_RES, R.ntiles, kNT_RES, (k_residual<JAC, W, Z>), R.tile_base, tiles_next(c), c->R, (const double*)c->d_b, \
      c->D, (const int32_t*)c->d_own_slot, (const double*)c->d_x, c->d_r, c->d_p, c->S, C)
 #define RAS_RES_J0(W) RAS_RES(true, W, false)
 #define RAS_RES_I0(W) RAS_RES(false, W, false)
@@ -550,7 +563,7 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
   const int64_t tb = R.tile_base;
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
     TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
-    KL(s, K_ZDOT, g, kThreads, k_zdot<true>, tb, c->T, (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
+    KL(s, K_ZDOT, g, kNT_STREAM, k_zdot<true>, tb, tiles_next(c), (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
     enq_finish<F_ZDOT0>(c, s, R, C);
   }
   for (int it = 1; it <= m; ++it) {
@@ -560,14 +573,14 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
     const double* p_old = c->fuse_p ? ((it & 1) ? c->d_p2 : c->d_p) : c->d_p;
     const double* zr = c->ic ? c->d_z : c->d_r;
 #define RAS_SPMV_V(W, IC, FIRST)                                                                                  \
-  KL(s, K_SPMV, g, kThreads, (k_spmv_pdot<W, IC, FIRST>), tb, c->T, c->L, (const double*)c->d_diag, zr, p_old, \
+  KL(s, K_SPMV, g, kThreads, (k_spmv_pdot<W, IC, FIRST>), tb, tiles_next(c), c->L, (const double*)c->d_diag, zr, p_old, \
      p_new, c->d_q, c->S, C)
 #define RAS_SPMV_JF(W) RAS_SPMV_V(W, false, true)
 #define RAS_SPMV_JN(W) RAS_SPMV_V(W, false, false)
 #define RAS_SPMV_IF(W) RAS_SPMV_V(W, true, true)
 #define RAS_SPMV_IN(W) RAS_SPMV_V(W, true, false)
 #define RAS_SPMV_P(W, Z) \
-  KL(s, K_SPMV, g, kThreads, (k_spmv_dot<W, Z>), tb, c->T, c->L, c->D, (const double*)p_new, c->d_q, c->S, C)
+  KL(s, K_SPMV, g, kNT_SPMV, (k_spmv_dot<W, Z>), tb, tiles_next(c), c->L, c->D, (const double*)p_new, c->d_q, c->S, C)
 #define RAS_SPMV_P0(W) RAS_SPMV_P(W, false)
 #define RAS_SPMV_PZ(W) RAS_SPMV_P(W, true)
     if (!c->fuse_p) {
@@ -601,27 +614,27 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
     enq_finish<F_SPMV>(c, s, R, C);
     if (!c->ic) {
       if (c->z)
-        KL(s, K_UPD, g, kThreads, (k_update_dot<true, true>), tb, c->T, c->D, (const double*)p_new,
+        KL(s, K_UPD, g, kNT_UPD, (k_update_dot<true, true>), tb, tiles_next(c), c->D, (const double*)p_new,
            (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
       else
-        KL(s, K_UPD, g, kThreads, (k_update_dot<true, false>), tb, c->T, c->D, (const double*)p_new,
+        KL(s, K_UPD, g, kNT_UPD, (k_update_dot<true, false>), tb, tiles_next(c), c->D, (const double*)p_new,
            (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
       enq_finish<F_UPD_JAC>(c, s, R, C, m, inner_tol);
       if (!c->fuse_p && !last) {
         if (c->z)
-          KL(s, K_PUPD, g, kThreads, k_pupdate<true>, tb, c->T, c->D, (const double*)c->d_r, c->d_p, c->S, C);
+          KL(s, K_PUPD, g, kNT_STREAM, k_pupdate<true>, tb, tiles_next(c), c->D, (const double*)c->d_r, c->d_p, c->S, C);
         else
-          KL(s, K_PUPD, g, kThreads, k_pupdate<false>, tb, c->T, c->D, (const double*)c->d_r, c->d_p, c->S, C);
+          KL(s, K_PUPD, g, kNT_STREAM, k_pupdate<false>, tb, tiles_next(c), c->D, (const double*)c->d_r, c->d_p, c->S, C);
       }
     } else {
-      KL(s, K_UPD, g, kThreads, (k_update_dot<false, false>), tb, c->T, c->D, (const double*)p_new,
+      KL(s, K_UPD, g, kNT_UPD, (k_update_dot<false, false>), tb, tiles_next(c), c->D, (const double*)p_new,
          (const double*)c->d_q, c->d_r, c->d_d, c->S, C);
       enq_finish<F_UPD_IC>(c, s, R, C, m, inner_tol);
       if (!last) {
         TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
-        KL(s, K_ZDOT, g, kThreads, k_zdot<false>, tb, c->T, (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
+        KL(s, K_ZDOT, g, kNT_STREAM, k_zdot<false>, tb, tiles_next(c), (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
         enq_finish<F_ZDOT>(c, s, R, C);
-        if (!c->fuse_p) KL(s, K_PUPD, g, kThreads, k_pupdate_z, tb, c->T, (const double*)c->d_z, c->d_p, c->S, C);
+        if (!c->fuse_p) KL(s, K_PUPD, g, kNT_STREAM, k_pupdate_z, tb, tiles_next(c), (const double*)c->d_z, c->d_p, c->S, C);
       }
     }
     if (exact && it % 16 == 0) {
@@ -635,7 +648,7 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 
 // a4
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
-  KL(s, K_PROL, R.ntiles, kThreads, k_prolong, R.tile_base, c->T, (const int32_t*)c->d_own_slot, (const double*)c->d_d,
+  KL(s, K_PROL, R.ntiles, kNT_STREAM, k_prolong, R.tile_base, tiles_next(c), (const int32_t*)c->d_own_slot, (const double*)c->d_d,
      c->d_x, c->S, C);
   return RAS_OK;
 }
