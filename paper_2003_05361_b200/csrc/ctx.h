@@ -81,14 +81,17 @@ struct ras_ctx {
   ras::Sell R{}, L{};
   int wR = 0, wL = 0;  // widest SELL slice of each matrix (kernel width dispatch)
   bool z = false;      // SELL-Z compressed matrices + diagonal on the device
+  int zwR = 0, zwL = 0;  // SELL-Z packed widths
   ras::Diag D{};
   ras::Tiles T{};
+  int2* d_cspan = nullptr;  // per tile {first column, span} of the local matrix (SpMV smem staging)
   int32_t dir = 0;  // tile walk direction of the last streaming launch
   double* d_x = nullptr;  // storage [owned | halo]
   double* d_r = nullptr;
   double* d_p = nullptr;
   double* d_p2 = nullptr;  // p double buffer (fused p update + SpMV)
   bool fuse_p = false;     // options.reserved_i[0]: fuse pass 3 into the next pass 1
+  bool stage = false;      // options.reserved_i[2]: shared-memory staging of p in the SpMV
   double* d_q = nullptr;
   double* d_d = nullptr;
   // IC(0)/ILU(0) path (a3')

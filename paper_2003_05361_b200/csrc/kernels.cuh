@@ -61,6 +61,7 @@ constexpr int kTileRows = 256 * RAS_RPT;    // rows per CTA tile (plan tile_rows
 constexpr int kNT_RES = RAS_NT_RES, kNT_SPMV = RAS_NT_SPMV, kNT_UPD = RAS_NT_UPD, kNT_STREAM = RAS_NT_STREAM;
 constexpr int kNP = 4;                      // partial slots per warp
 constexpr int kMaxW = 8;                    // unrolled SELL width (wider slices take the loop path)
+constexpr int kStageMax = 4096;             // max p span staged in shared memory by k_spmv_dot (32 KB)
 
 struct Tiles {
   const int4* tile;               // {row0, nrows, local subdomain, 0}
@@ -166,39 +167,49 @@ __device__ __forceinline__ void warp_partials(const double (&v)[NV], int64_t t, 
 // the gathered vector keeps its L2 lines.
 // W > 0: every slice of the matrix is at most W wide (host-dispatched, fully
 // unrolled, predicated on the slice's own width); W == 0: generic loop.
-template <int W, bool Z = false>
-__device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const double* __restrict__ x) {
+// SMX: x is a shared-memory copy of the columns [xoff, xoff + span).
+template <int W, bool Z = false, bool SMX = false>
+__device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const double* x, int32_t xoff = 0) {
   const int64_t s = row >> 5;
   const int lane = (int)(row & 31);
-  const int64_t base = __ldg(&M.sptr[s]);
-  const int w = (int)((__ldg(&M.sptr[s + 1]) - base) >> 5);
   double acc = 0.0;
   if (Z) {
-    const uint8_t* vc = M.code + base + lane;
-    const uint16_t* dp = M.d16 + base + lane;
-    const int32_t* kb = M.kbase + (base >> 5);
-    if (W > 0) {
-      uint8_t v[W > 0 ? W : 1];
-      int32_t c[W > 0 ? W : 1];
-#pragma unroll
-      for (int k = 0; k < W; ++k)
-        if (k < w) {
-          v[k] = __ldcs(vc + 32 * k);
-          const int32_t b = __ldg(kb + k);  // warp-uniform
-          c[k] = b >= 0 ? b + (int32_t)__ldcs(dp + 32 * k) : __ldg(&M.wide[(-b - 1) * 32 + lane]);
-        }
-#pragma unroll
-      for (int k = 0; k < W; ++k)
-        if (k < w) acc += __ldg(&M.table[v[k]]) * __ldg(&x[c[k]]);
+    // lane-packed SELL-Z (zformat.cpp): W in {4, 8} is the matrix's packed width;
+    // one vector load of the row's W codes, one of its W column offsets, and
+    // the slice's W column bases (warp-uniform, L1 broadcast).
+    static_assert(!Z || W == 4 || W == 8, "SELL-Z widths are 4 or 8");
+    uint32_t cw[W / 4 > 0 ? W / 4 : 1];
+    uint32_t dw[W / 2 > 0 ? W / 2 : 1];
+    int32_t kb[W > 0 ? W : 1];
+    if (W == 4) {
+      cw[0] = __ldcs(reinterpret_cast<const unsigned int*>(M.code) + row);
+      const uint2 d = __ldcs(reinterpret_cast<const uint2*>(M.d16) + row);
+      dw[0] = d.x;
+      dw[1] = d.y;
+      const int4 b = __ldg(reinterpret_cast<const int4*>(M.kbase) + s);
+      kb[0] = b.x, kb[1] = b.y, kb[2] = b.z, kb[3] = b.w;
     } else {
-      for (int k = 0; k < w; ++k) {
-        const int32_t b = __ldg(kb + k);
-        const int32_t c = b >= 0 ? b + (int32_t)__ldcs(dp + 32 * k) : __ldg(&M.wide[(-b - 1) * 32 + lane]);
-        acc += __ldg(&M.table[__ldcs(vc + 32 * k)]) * __ldg(&x[c]);
-      }
+      const uint2 c = __ldcs(reinterpret_cast<const uint2*>(M.code) + row);
+      cw[0] = c.x;
+      cw[W / 4 - 1] = c.y;
+      const uint4 d = __ldcs(reinterpret_cast<const uint4*>(M.d16) + row);
+      dw[0] = d.x, dw[1] = d.y, dw[2] = d.z, dw[W / 2 - 1] = d.w;
+      const int4 b0 = __ldg(reinterpret_cast<const int4*>(M.kbase) + 2 * s);
+      const int4 b1 = __ldg(reinterpret_cast<const int4*>(M.kbase) + 2 * s + 1);
+      kb[0] = b0.x, kb[1] = b0.y, kb[2] = b0.z, kb[3] = b0.w;
+      kb[W - 4] = b1.x, kb[W - 3] = b1.y, kb[W - 2] = b1.z, kb[W - 1] = b1.w;
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint32_t code = (cw[k / 4] >> (8 * (k % 4))) & 0xffu;
+      const uint32_t off = (dw[k / 2] >> (16 * (k % 2))) & 0xffffu;
+      const int32_t c = kb[k] >= 0 ? kb[k] + (int32_t)off : __ldg(&M.wide[(-kb[k] - 1) * 32 + lane]);
+      acc += __ldg(&M.table[code]) * (SMX ? x[c - xoff] : __ldg(&x[c]));
     }
     return acc;
   }
+  const int64_t base = __ldg(&M.sptr[s]);
+  const int w = (int)((__ldg(&M.sptr[s + 1]) - base) >> 5);
   const double* vp = M.val + base + lane;
   const int32_t* cp = M.col + base + lane;
   if (W > 0) {
@@ -212,9 +223,12 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
       }
 #pragma unroll
     for (int k = 0; k < W; ++k)
-      if (k < w) acc += v[k] * __ldg(&x[c[k]]);
+      if (k < w) acc += v[k] * (SMX ? x[c[k] - xoff] : __ldg(&x[c[k]]));
   } else {
-    for (int k = 0; k < w; ++k) acc += __ldcs(vp + 32 * k) * __ldg(&x[__ldcs(cp + 32 * k)]);
+    for (int k = 0; k < w; ++k) {
+      const int32_t c = __ldcs(cp + 32 * k);
+      acc += __ldcs(vp + 32 * k) * (SMX ? x[c - xoff] : __ldg(&x[c]));
+    }
   }
   return acc;
 }
@@ -264,22 +278,41 @@ static __global__ void __launch_bounds__(kNT_RES, RAS_MB_RES) k_residual(int64_t
 }
 
 // a3 pass 1: q = A_p p (diag + SELL off-diagonal); partial p.q.
-template <int W, bool Z>
+template <int W, bool Z, bool STG>
 static __global__ void __launch_bounds__(kNT_SPMV, RAS_MB_SPMV) k_spmv_dot(int64_t tile_base, Tiles T, Sell L, Diag D,
                                                               const double* __restrict__ p, double* __restrict__ q,
-                                                              Scal S, Ctl C) {
+                                                              Scal S, Ctl C, const int2* __restrict__ cspan) {
   constexpr int NT = kNT_SPMV, RPT = kTileRows / NT;
+  // shared-memory staging of p: a tile whose columns span <= kStageMax rows
+  // (2D natural ordering: the tile +- one Omega width) first copies that span of
+  // p with coalesced loads, then gathers from shared memory (no dependent L2
+  // round trip per neighbour); wider tiles gather from global memory.
+  // Measured on B200 (round 1): the barrier after the staging copy serialises
+  // the span load and the matrix stream and the halo triples the L2 traffic, so
+  // the global-gather path (STG = false) is faster and the default.
+  __shared__ double sp[STG ? kStageMax : 1];
   pdl_start();
   const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];
   if (stopped(C, ti.z) || !S.active[ti.z]) return;
+  const int2 cs = STG ? cspan[t] : make_int2(0, -1);
+  const bool staged = STG && cs.y > 0;
+  if (STG) {
+    if (staged)
+      for (int i = threadIdx.x; i < cs.y; i += NT) sp[i] = __ldg(&p[cs.x + i]);
+    __syncthreads();
+  }
   double v[1] = {0.0};
   double pi[RPT], di[RPT], ax[RPT];
   RAS_ROWS_LOOP(j) {
-    pi[j] = __ldg(&p[RAS_ROW(j)]);
+    pi[j] = staged ? sp[RAS_ROW(j) - cs.x] : __ldg(&p[RAS_ROW(j)]);
     di[j] = diag_at<Z>(D, RAS_ROW(j));
   }
-  RAS_ROWS_LOOP(j) ax[j] = sell_dot<W, Z>(L, RAS_ROW(j), p);
+  if (staged) {
+    RAS_ROWS_LOOP(j) ax[j] = sell_dot<W, Z, true>(L, RAS_ROW(j), sp, cs.x);
+  } else {
+    RAS_ROWS_LOOP(j) ax[j] = sell_dot<W, Z>(L, RAS_ROW(j), p);
+  }
   RAS_ROWS_LOOP(j) {
     const double qi = di[j] * pi[j] + ax[j];
     q[RAS_ROW(j)] = qi;

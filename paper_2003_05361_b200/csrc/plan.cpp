@@ -356,6 +356,20 @@ static void build_finalize(ras_plan* pl) {
       }
     }
   }
+  // per tile: the span of local-matrix columns it reads (its rows included),
+  // staged in shared memory by the SpMV when it fits (kernels.cuh kStageMax)
+  pl->tile_cmin.assign(pl->tile_row0.size(), 0);
+  pl->tile_clen.assign(pl->tile_row0.size(), -1);
+  for (size_t t = 0; t < pl->tile_row0.size(); ++t) {
+    int64_t lo = pl->tile_row0[t], hi = pl->tile_row0[t] + pl->tile_nrows[t] - 1;
+    for (int64_t sl = lo / kSlice; sl <= hi / kSlice; ++sl)
+      for (int64_t e = pl->L_sptr[sl]; e < pl->L_sptr[sl + 1]; ++e) {
+        lo = std::min<int64_t>(lo, pl->L_col[e]);
+        hi = std::max<int64_t>(hi, pl->L_col[e]);
+      }
+    pl->tile_cmin[t] = (int32_t)lo;
+    if (hi - lo + 1 <= pl->stage_max) pl->tile_clen[t] = (int32_t)(hi - lo + 1);
+  }
   build_zformat(pl);
   pl->finalized = true;
 }

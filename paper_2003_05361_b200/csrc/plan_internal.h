@@ -97,6 +97,7 @@ struct ras_plan {
   int64_t nnz_residual = 0, nnz_local = 0;
   // compressed SELL-Z copies of R, L and the diagonal (zformat.cpp); z_ok = usable
   bool z_ok = false;
+  int32_t zR_w = 0, zL_w = 0;  // packed widths (4 or 8)
   std::vector<double> z_table;
   std::vector<uint8_t> R_code, L_code, D_code;
   std::vector<int32_t> R_kbase, L_kbase;
@@ -106,6 +107,8 @@ struct ras_plan {
   std::vector<int32_t> tile_sub;
   std::vector<int64_t> tile_row0;
   std::vector<int32_t> tile_nrows;
+  std::vector<int32_t> tile_cmin, tile_clen;  // local-matrix column span per tile (-1 = wider than stage_max)
+  int32_t stage_max = 4096;                   // must equal ras::kStageMax (kernels.cuh)
   double b2_global_local = 0.0;  // sum over this rank's owned rows of b^2
 };
 

@@ -118,16 +118,18 @@ static void compute_model_bytes(ras_ctx* c) {
   // compulsory bytes, real (unpadded) rows and entries.  Plain
   // SELL: 8 B value + 4 B column per entry, 8 B diagonal; SELL-Z: 1 B code +
   // 2 B column offset (+ 4 B base per 32 entries), 1 B diagonal code.
+  // SELL-Z is lane-packed to the padded width: every row moves Wp entries.
   const double eb = c->z ? (1.0 + 2.0 + 4.0 / 32.0) : 12.0;
   const double db = c->z ? 1.0 : 8.0;
-  c->mb.residual = rows * (8 /*b*/ + db /*diag*/ + 4 /*own_slot*/ + 8 /*x*/ + 8 /*r*/ + 8 /*p*/) +
-                   (double)pl->nnz_residual * eb;
+  const double ent_R = c->z ? rows * pl->zR_w : (double)pl->nnz_residual;
+  const double ent_L = c->z ? rows * pl->zL_w : nnz_off;
+  c->mb.residual = rows * (8 /*b*/ + db /*diag*/ + 4 /*own_slot*/ + 8 /*x*/ + 8 /*r*/ + 8 /*p*/) + ent_R * eb;
   if (c->fuse_p) {
     // pass 1 with the fused p update: r (or z), diag, p_old in; p_new, q out (+ off-diagonal entries)
     c->mb.spmv_dot = rows * (8 /*r|z*/ + 8 /*diag*/ + 8 /*p_old*/ + 8 /*p_new*/ + 8 /*q*/) + nnz_off * 12.0;
     c->mb.pupdate = 0.0;
   } else {
-    c->mb.spmv_dot = rows * (8 /*p*/ + db /*diag*/ + 8 /*q*/) + nnz_off * eb;
+    c->mb.spmv_dot = rows * (8 /*p*/ + db /*diag*/ + 8 /*q*/) + ent_L * eb;
     c->mb.pupdate = rows * (db /*diag*/ + 8 /*r*/ + 16 /*p*/);
   }
   c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + db /*diag*/ + 16 /*r*/ + 16 /*d*/);
@@ -223,6 +225,8 @@ static ras_status upload_plan(ras_ctx* c) {
     TRY(upload(c, &lw, pl->L_wide, 1));
     c->L = Sell{sp, nullptr, nullptr, lk, ld, lw, lc, tb};
     c->D = Diag{nullptr, dc, tb};
+    c->zwR = pl->zR_w;
+    c->zwL = pl->zL_w;
   } else {
     int32_t* ci;
     double* va;
@@ -259,6 +263,10 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(upload(c, &sb, stb));
   TRY(upload(c, &sn, snt));
   c->T = Tiles{ti, sb, sn, c->ntiles};
+  if (pl->stage_max != kStageMax) return set_err(c, RAS_ESTATE, "plan stage_max != kernel kStageMax");
+  std::vector<int2> cspan(pl->tile_cmin.size());
+  for (size_t i = 0; i < cspan.size(); ++i) cspan[i] = make_int2(pl->tile_cmin[i], pl->tile_clen[i]);
+  TRY(upload(c, &c->d_cspan, cspan, 1));
   c->d_x = (double*)dalloc_raw(c, (size_t)(c->n_own + c->n_halo) * 8);
   if (!c->d_x) return set_err(c, RAS_ENOMEM, "device allocation failed (x storage)");
   TRY(zalloc(c, &c->d_r, (size_t)c->rows_pad));
@@ -488,6 +496,14 @@ static Tiles tiles_next(ras_ctx* c) {
     default: CALL(0); break;                                                               \
   }
 
+// SELL-Z packed widths are 4 or 8
+#define RAS_DISPATCH_ZW(w, CALL) \
+  if ((w) == 4) {                \
+    CALL(4);                     \
+  } else {                       \
+    CALL(8);                     \
+  }
+
 ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
 #define RAS_RES(JAC, W, Z)                                                                                  \
   KL(s, K_RES, R.ntiles, kNT_RES, (k_residual<JAC, W, Z>), R.tile_base, tiles_next(c), c->R, (const double*)c->d_b, \
@@ -498,14 +514,14 @@ ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
 #define RAS_RES_IZ(W) RAS_RES(false, W, true)
   if (!c->ic) {
     if (c->z) {
-      RAS_DISPATCH_W(c->wR, RAS_RES_JZ);
+      RAS_DISPATCH_ZW(c->zwR, RAS_RES_JZ);
     } else {
       RAS_DISPATCH_W(c->wR, RAS_RES_J0);
     }
     enq_finish<F_RES_JAC>(c, s, R, C);
   } else {
     if (c->z) {
-      RAS_DISPATCH_W(c->wR, RAS_RES_IZ);
+      RAS_DISPATCH_ZW(c->zwR, RAS_RES_IZ);
     } else {
       RAS_DISPATCH_W(c->wR, RAS_RES_I0);
     }
@@ -579,16 +595,27 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 #define RAS_SPMV_JN(W) RAS_SPMV_V(W, false, false)
 #define RAS_SPMV_IF(W) RAS_SPMV_V(W, true, true)
 #define RAS_SPMV_IN(W) RAS_SPMV_V(W, true, false)
-#define RAS_SPMV_P(W, Z) \
-  KL(s, K_SPMV, g, kNT_SPMV, (k_spmv_dot<W, Z>), tb, tiles_next(c), c->L, c->D, (const double*)p_new, c->d_q, c->S, C)
-#define RAS_SPMV_P0(W) RAS_SPMV_P(W, false)
-#define RAS_SPMV_PZ(W) RAS_SPMV_P(W, true)
+#define RAS_SPMV_P(W, Z, STG)                                                                                     \
+  KL(s, K_SPMV, g, kNT_SPMV, (k_spmv_dot<W, Z, STG>), tb, tiles_next(c), c->L, c->D, (const double*)p_new, c->d_q, \
+     c->S, C, (const int2*)c->d_cspan)
+#define RAS_SPMV_P0(W) RAS_SPMV_P(W, false, false)
+#define RAS_SPMV_PZ(W) RAS_SPMV_P(W, true, false)
+#define RAS_SPMV_S0(W) RAS_SPMV_P(W, false, true)
+#define RAS_SPMV_SZ(W) RAS_SPMV_P(W, true, true)
     if (!c->fuse_p) {
       // p_new was written by the previous iteration's p update (or the PCG start)
       if (c->z) {
-        RAS_DISPATCH_W(c->wL, RAS_SPMV_PZ);
+        if (c->stage) {
+          RAS_DISPATCH_ZW(c->zwL, RAS_SPMV_SZ);
+        } else {
+          RAS_DISPATCH_ZW(c->zwL, RAS_SPMV_PZ);
+        }
       } else {
-        RAS_DISPATCH_W(c->wL, RAS_SPMV_P0);
+        if (c->stage) {
+          RAS_DISPATCH_W(c->wL, RAS_SPMV_S0);
+        } else {
+          RAS_DISPATCH_W(c->wL, RAS_SPMV_P0);
+        }
       }
     } else if (!c->ic) {
       if (it == 1) {
@@ -603,6 +630,8 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
         RAS_DISPATCH_W(c->wL, RAS_SPMV_IN);
       }
     }
+#undef RAS_SPMV_SZ
+#undef RAS_SPMV_S0
 #undef RAS_SPMV_PZ
 #undef RAS_SPMV_P0
 #undef RAS_SPMV_P
@@ -859,6 +888,7 @@ ras_status ras_setup(ras_ctx** out, const ras_csr* A, const double* b, const ras
   if (opt) c->opt = *opt;
   if (c->opt.inner_iters < 1) c->opt.inner_iters = 1;
   c->fuse_p = c->opt.reserved_i[0] != 0;
+  c->stage = c->opt.reserved_i[2] != 0;
   if (c->opt.inner_tol < 0) {
     set_tls_error("inner_tol must be >= 0");
     delete c;

@@ -1,15 +1,20 @@
-// Compressed SELL-32 ("SELL-Z") of the residual and local matrices: the same
-// entries in the same order, stored with fewer bytes when the matrix allows it.
+// Compressed, lane-packed SELL-32 ("SELL-Z") of the residual and local
+// matrices: the same entries as the plain SELL-32, stored with fewer bytes and
+// packed so that a thread fetches all entries of its row with one vector load.
 //
+//  * width: every slice padded to one width Wp in {4, 8} (the matrix's widest
+//    slice rounded up; wider matrices keep the plain format);
 //  * values: dictionary coded (CSR-VI style) — one uint8 code per entry into a
 //    table of <= 256 distinct FP64 values shared by the residual matrix, the
-//    local off-diagonal matrix and the diagonal;
-//  * columns: per (slice, k) column of 32 entries an int32 base (the smallest
-//    column) plus a uint16 offset per entry.
+//    local off-diagonal matrix and the diagonal (padding entries code 0.0);
+//  * columns: per (slice, k) an int32 base (the smallest column of the 32 rows)
+//    plus a uint16 offset per entry; a (slice, k) group spanning more than
+//    65535 columns keeps its 32 int32 columns in `wide` (base = -(group) - 1);
+//  * packing: entry k of lane l of slice s at (s*32 + l)*Wp + k, so lane l reads
+//    its Wp codes as one 4/8-byte load and its Wp offsets as one 8/16-byte load
+//    and a warp's loads are contiguous.
 // Decoding is exact (table[code] is the original double, base + offset the
-// original column), so results are bitwise those of the plain SELL path.  A
-// matrix that does not fit (more than 256 distinct values, or a slice column
-// spanning more than 65535 indices) keeps the plain FP64 / int32 format.
+// original column), so results are bitwise those of the plain SELL path.
 #include <algorithm>
 #include <cstring>
 #include <unordered_map>
@@ -19,37 +24,12 @@
 
 namespace ras {
 
-// Groups whose 32 columns span more than 65535 (e.g. a slice straddling the
-// owned / overlap boundary of the residual matrix, whose columns then point
-// into two subdomains' storage) keep their int32 columns in `wide`;
-// kbase = -(wide group index) - 1 marks them.
-static void encode_cols(const std::vector<int32_t>& col, std::vector<int32_t>& kbase, std::vector<uint16_t>& d16,
-                        std::vector<int32_t>& wide) {
-  const size_t ne = col.size();
-  kbase.assign(ne / 32, 0);
-  d16.assign(ne, 0);
-  wide.clear();
-  for (size_t g = 0; g < ne / 32; ++g) {
-    int32_t lo = col[g * 32], hi = col[g * 32];
-    for (int l = 1; l < 32; ++l) {
-      lo = std::min(lo, col[g * 32 + l]);
-      hi = std::max(hi, col[g * 32 + l]);
-    }
-    if ((int64_t)hi - lo > 65535) {
-      kbase[g] = -(int32_t)(wide.size() / 32) - 1;
-      wide.insert(wide.end(), col.begin() + g * 32, col.begin() + g * 32 + 32);
-      continue;
-    }
-    kbase[g] = lo;
-    for (int l = 0; l < 32; ++l) d16[g * 32 + l] = (uint16_t)(col[g * 32 + l] - lo);
-  }
-}
+namespace {
 
-bool build_zformat(ras_plan* pl) {
-  pl->z_ok = false;
+struct Coder {
   std::unordered_map<uint64_t, uint8_t> code;
   std::vector<double> table;
-  auto enc = [&](double v, uint8_t* out) -> bool {
+  bool enc(double v, uint8_t* out) {
     uint64_t b;
     std::memcpy(&b, &v, 8);
     auto it = code.find(b);
@@ -62,23 +42,76 @@ bool build_zformat(ras_plan* pl) {
     *out = (uint8_t)table.size();
     table.push_back(v);
     return true;
-  };
-  std::vector<uint8_t> rc(pl->R_val.size()), lc(pl->L_val.size()), dc(pl->diag.size());
-  for (size_t i = 0; i < rc.size(); ++i)
-    if (!enc(pl->R_val[i], &rc[i])) return false;
-  for (size_t i = 0; i < lc.size(); ++i)
-    if (!enc(pl->L_val[i], &lc[i])) return false;
-  for (size_t i = 0; i < dc.size(); ++i)
-    if (!enc(pl->diag[i], &dc[i])) return false;
+  }
+};
+
+int padded_width(const std::vector<int64_t>& sptr) {
+  int64_t w = 0;
+  for (size_t s = 0; s + 1 < sptr.size(); ++s) w = std::max(w, (sptr[s + 1] - sptr[s]) / 32);
+  if (w <= 4) return 4;
+  if (w <= 8) return 8;
+  return 0;
+}
+
+// plain SELL-32 (sptr, col, val) -> packed Z arrays; false if a value does not fit the table
+bool pack(const std::vector<int64_t>& sptr, const std::vector<int32_t>& col, const std::vector<double>& val, int Wp,
+          Coder& C, std::vector<uint8_t>& code, std::vector<int32_t>& kbase, std::vector<uint16_t>& d16,
+          std::vector<int32_t>& wide) {
+  const int64_t nsl = (int64_t)sptr.size() - 1;
+  code.assign((size_t)nsl * 32 * Wp, 0);
+  d16.assign((size_t)nsl * 32 * Wp, 0);
+  kbase.assign((size_t)nsl * Wp, 0);
+  wide.clear();
+  uint8_t zero;
+  if (!C.enc(0.0, &zero)) return false;
+  std::vector<int32_t> cg(32);
+  for (int64_t s = 0; s < nsl; ++s) {
+    const int64_t w = (sptr[s + 1] - sptr[s]) / 32;
+    for (int k = 0; k < Wp; ++k) {
+      for (int l = 0; l < 32; ++l) {
+        const size_t z = ((size_t)s * 32 + l) * Wp + k;
+        if (k < w) {
+          const int64_t e = sptr[s] + (int64_t)k * 32 + l;
+          if (!C.enc(val[e], &code[z])) return false;
+          cg[l] = col[e];
+        } else {
+          code[z] = zero;  // padding: value 0 at a valid column (the lane's first entry, or 0)
+          cg[l] = w > 0 ? col[sptr[s] + l] : 0;
+        }
+      }
+      const int32_t lo = *std::min_element(cg.begin(), cg.end());
+      const int32_t hi = *std::max_element(cg.begin(), cg.end());
+      if ((int64_t)hi - lo > 65535) {
+        kbase[(size_t)s * Wp + k] = -(int32_t)(wide.size() / 32) - 1;
+        wide.insert(wide.end(), cg.begin(), cg.end());
+      } else {
+        kbase[(size_t)s * Wp + k] = lo;
+        for (int l = 0; l < 32; ++l) d16[((size_t)s * 32 + l) * Wp + k] = (uint16_t)(cg[l] - lo);
+      }
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+bool build_zformat(ras_plan* pl) {
+  pl->z_ok = false;
+  const int wR = padded_width(pl->R_sptr), wL = padded_width(pl->L_sptr);
+  if (!wR || !wL) return false;
+  Coder C;
+  std::vector<uint8_t> rc, lc, dc(pl->diag.size());
   std::vector<int32_t> rkb, lkb, rw, lw;
   std::vector<uint16_t> rd, ld;
-  encode_cols(pl->R_col, rkb, rd, rw);
-  encode_cols(pl->L_col, lkb, ld, lw);
+  if (!pack(pl->R_sptr, pl->R_col, pl->R_val, wR, C, rc, rkb, rd, rw)) return false;
+  if (!pack(pl->L_sptr, pl->L_col, pl->L_val, wL, C, lc, lkb, ld, lw)) return false;
+  for (size_t i = 0; i < dc.size(); ++i)
+    if (!C.enc(pl->diag[i], &dc[i])) return false;
   // worth it only if the wide groups stay rare
-  if (rw.size() * 8 > pl->R_col.size() || lw.size() * 8 > pl->L_col.size()) return false;
-  pl->R_wide = std::move(rw);
-  pl->L_wide = std::move(lw);
-  pl->z_table = std::move(table);
+  if (rw.size() * 8 > rc.size() || lw.size() * 8 > lc.size()) return false;
+  pl->z_table = std::move(C.table);
+  pl->zR_w = wR;
+  pl->zL_w = wL;
   pl->R_code = std::move(rc);
   pl->L_code = std::move(lc);
   pl->D_code = std::move(dc);
@@ -86,6 +119,8 @@ bool build_zformat(ras_plan* pl) {
   pl->L_kbase = std::move(lkb);
   pl->R_d16 = std::move(rd);
   pl->L_d16 = std::move(ld);
+  pl->R_wide = std::move(rw);
+  pl->L_wide = std::move(lw);
   pl->z_ok = true;
   return true;
 }

@@ -25,7 +25,7 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-@pytest.mark.parametrize("fmt", ["z", "plain", "fuse_p"])
+@pytest.mark.parametrize("fmt", ["plain", "z", "fuse_p", "stage", "z_stage"])
 @pytest.mark.parametrize("case", ["c1", "voronoi_ragged", "strips"])
 def test_sync_iterates_match_oracle(case, fmt):
     if case == "c1":
@@ -46,7 +46,7 @@ def test_sync_iterates_match_oracle(case, fmt):
     b = ri.rhs(nx * ny, 0)
     K = 6
     ref = oracle_iterates(A, b, owner, gamma, "jacobi", m, K)
-    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", zfmt=fmt == "z"))
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", zfmt=fmt.startswith("z"), stage=fmt.endswith("stage")))
     for k in (1, 2, K):
         st, x = s.solve(1e-300, k, "sync")
         assert st == R._ffi.RAS_ENOCONV
