@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--tts", action="store_true", help="also run to rel. residual 1e-8 (long)")
     ap.add_argument("--scale", type=int, default=SUB, help="owned side per subdomain (debug)")
-    ap.add_argument("--zfmt", action="store_true", help="compressed SELL-Z matrices (opt-in format)")
+    ap.add_argument("--plain", action="store_true", help="force plain FP64/int32 SELL (default: SELL-Z when it applies)")
     ap.add_argument("--fuse-p", action="store_true", help="fuse the PCG p update into the next SpMV")
     return ap.parse_args()
 
@@ -292,7 +292,7 @@ def main():
         nccl_id = obj[0]
     t_setup0 = time.perf_counter()
     prob = build_rank_problem(N, rank, args.scale)
-    opts = R.options("jacobi", M_INNER, zfmt=args.zfmt, fuse_p=args.fuse_p)
+    opts = R.options("jacobi", M_INNER, plain=args.plain, fuse_p=args.fuse_p)
     solver = R.Solver(prob["A"], prob["b"], prob["owner"], GAMMA, opts,
                       comm={"rank": rank, "world": world, "device": local, "nccl_id": nccl_id,
                             "stream": stream.cuda_stream})

@@ -44,7 +44,7 @@ constexpr int kTileRows = 256 * RAS_RPT;    // rows per CTA tile (plan tile_rows
 #define RAS_NT_SPMV 512
 #endif
 #ifndef RAS_MB_SPMV
-#define RAS_MB_SPMV 3
+#define RAS_MB_SPMV 4
 #endif
 #ifndef RAS_NT_UPD
 #define RAS_NT_UPD 512

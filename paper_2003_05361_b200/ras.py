@@ -60,15 +60,15 @@ _DETECTORS = {"central": F.RAS_DET_CENTRAL, "decentral": F.RAS_DET_DECENTRAL}
 
 
 def options(local_solver="jacobi", inner_iters=20, inner_tol=0.0, detector="decentral", fuse_p=False,
-            zfmt=False, stage=False, **kw) -> F.RasOptions:
+            plain=False, stage=False, **kw) -> F.RasOptions:
     """ras_options.  Kernel-variant switches (all bitwise-equivalent paths):
     fuse_p: fuse the PCG p update into the next SpMV (reserved_i[0]);
-    zfmt: compressed lane-packed SELL-Z matrices when they apply (reserved_i[1]);
+    plain: force FP64/int32 SELL instead of the default lane-packed SELL-Z (reserved_i[1] = 2);
     stage: shared-memory staging of p in the SpMV (reserved_i[2])."""
     o = F.RasOptions()
     _check(F.lib().ras_options_default(C.byref(o)))
     o.reserved_i[0] = 1 if fuse_p else 0
-    o.reserved_i[1] = 1 if zfmt else 0
+    o.reserved_i[1] = 2 if plain else 0
     o.reserved_i[2] = 1 if stage else 0
     o.local_solver = _SOLVERS[local_solver] if isinstance(local_solver, str) else int(local_solver)
     o.inner_iters = int(inner_iters)

@@ -46,7 +46,8 @@ def test_sync_iterates_match_oracle(case, fmt):
     b = ri.rhs(nx * ny, 0)
     K = 6
     ref = oracle_iterates(A, b, owner, gamma, "jacobi", m, K)
-    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", zfmt=fmt.startswith("z"), stage=fmt.endswith("stage")))
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", plain=fmt in ("plain", "stage"),
+                                              stage=fmt.endswith("stage")))
     for k in (1, 2, K):
         st, x = s.solve(1e-300, k, "sync")
         assert st == R._ffi.RAS_ENOCONV
@@ -153,7 +154,7 @@ def test_non_compressible_matrix_takes_plain_path():
     As.sort_indices()
     A2 = ri.CSR(As.indptr, As.indices, As.data, N * N)
     owner = R.partition_regular(N, N, 1, 2, 2, 1)
-    s = R.Solver(A2, ri.rhs(N * N), owner, 2, R.options("jacobi", 8, zfmt=True))
+    s = R.Solver(A2, ri.rhs(N * N), owner, 2, R.options("jacobi", 8))
     assert s.plan().info()["z_format"] == 0
     ref = oracle_iterates(A2, ri.rhs(N * N), owner, 2, "jacobi", 8, 3)
     st, x = s.solve(1e-300, 3, "sync")
