@@ -361,8 +361,9 @@ static void build_finalize(ras_plan* pl) {
   pl->tile_cmin.assign(pl->tile_row0.size(), 0);
   pl->tile_clen.assign(pl->tile_row0.size(), -1);
   for (size_t t = 0; t < pl->tile_row0.size(); ++t) {
-    int64_t lo = pl->tile_row0[t], hi = pl->tile_row0[t] + pl->tile_nrows[t] - 1;
-    for (int64_t sl = lo / kSlice; sl <= hi / kSlice; ++sl)
+    const int64_t r0 = pl->tile_row0[t], r1 = pl->tile_row0[t] + pl->tile_nrows[t] - 1;
+    int64_t lo = r0, hi = r1;
+    for (int64_t sl = r0 / kSlice; sl <= r1 / kSlice; ++sl)
       for (int64_t e = pl->L_sptr[sl]; e < pl->L_sptr[sl + 1]; ++e) {
         lo = std::min<int64_t>(lo, pl->L_col[e]);
         hi = std::max<int64_t>(hi, pl->L_col[e]);

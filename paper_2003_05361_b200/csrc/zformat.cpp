@@ -26,21 +26,31 @@ namespace ras {
 
 namespace {
 
+// Value dictionary keyed by the bit pattern (exact; -0.0 != 0.0).  Matrices
+// that fit have few distinct values, so a linear scan with a last-hit cache is
+// faster than hashing; the scan length is capped by the 256-entry limit.
 struct Coder {
-  std::unordered_map<uint64_t, uint8_t> code;
+  std::vector<uint64_t> bits;
   std::vector<double> table;
+  size_t last = 0;
   bool enc(double v, uint8_t* out) {
     uint64_t b;
     std::memcpy(&b, &v, 8);
-    auto it = code.find(b);
-    if (it != code.end()) {
-      *out = it->second;
+    if (last < bits.size() && bits[last] == b) {
+      *out = (uint8_t)last;
       return true;
     }
+    for (size_t i = 0; i < bits.size(); ++i)
+      if (bits[i] == b) {
+        last = i;
+        *out = (uint8_t)i;
+        return true;
+      }
     if (table.size() >= 256) return false;
-    code.emplace(b, (uint8_t)table.size());
-    *out = (uint8_t)table.size();
+    last = bits.size();
+    bits.push_back(b);
     table.push_back(v);
+    *out = (uint8_t)last;
     return true;
   }
 };
