@@ -92,6 +92,9 @@ struct ras_ctx {
   double* d_p2 = nullptr;  // p double buffer (fused p update + SpMV)
   bool fuse_p = false;     // options.reserved_i[0]: fuse pass 3 into the next pass 1
   bool stage = false;      // options.reserved_i[2]: shared-memory staging of p in the SpMV
+  bool small = false;      // f2: one CTA per subdomain runs the whole local PCG (k_small_pcg)
+  int small_nmax = 0;
+  ras::SmallSubs SS{};
   double* d_q = nullptr;
   double* d_d = nullptr;
   // IC(0)/ILU(0) path (a3')

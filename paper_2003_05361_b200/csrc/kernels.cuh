@@ -675,6 +675,122 @@ static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_pupdate_z(
   RAS_ROWS_LOOP(j) p[RAS_ROW(j)] = zi[j] + beta * pi[j];
 }
 
+// ---------------------------------------------------------------------------
+// Small-subdomain regime (thousands of unknowns per subdomain,
+// many subdomains per GPU; the paper's own runs use 4096 per subdomain).  One
+// CTA of kNT_SMALL threads runs the WHOLE Jacobi-PCG local solve of one
+// subdomain (all m iterations, or to the inner tolerance in exact mode) plus the
+// restricted prolongation, with p, r, d in shared memory, q in registers and
+// block-level reductions: no per-iteration launches, no host polling.  Same
+// recurrences as the tiled path; only summation order differs.
+// ---------------------------------------------------------------------------
+constexpr int kNT_SMALL = 1024;
+constexpr int kSmallMaxRows = 9216;  // 24 B of shared memory per row (p, r, d) <= 216 KB
+
+struct SmallSubs {
+  const int32_t* row_off;  // per local subdomain: first row-space row
+  const int32_t* nrows;    // padded rows (multiple of 32)
+};
+
+// Deterministic block sum of NV values over kNT_SMALL threads; every thread gets the result.
+template <int NV>
+__device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[kNT_SMALL / 32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double s = warp_sum(v[j]);
+    if (lane == 0) sh[j][w] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double s = lane < kNT_SMALL / 32 ? sh[j][lane] : 0.0;
+    s = warp_sum(s);
+    v[j] = __shfl_sync(0xffffffffu, s, 0);
+  }
+  __syncthreads();
+}
+
+// Runs after k_residual<JAC>/k_finish<F_RES_JAC> (r, p = z, rho, rt2, active set).
+template <int RPT, int W, bool Z>
+static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, SmallSubs SS, Sell L, Diag D,
+                                                                   const double* __restrict__ r_in,
+                                                                   const double* __restrict__ p_in,
+                                                                   const int32_t* __restrict__ own_slot,
+                                                                   double* __restrict__ x, Scal S, Ctl C, int32_t m,
+                                                                   double inner_tol) {
+  extern __shared__ double smem[];
+  __shared__ double red[2][kNT_SMALL / 32];
+  pdl_start();
+  const int lp = lp_base + blockIdx.x;
+  if (stopped(C, lp) || !S.active[lp]) return;  // uniform per CTA
+  const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+  double* sp = smem;           // p
+  double* sr = smem + n;       // r
+  double* sd = smem + 2 * n;   // d (correction)
+  for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
+    sp[i] = __ldg(&p_in[r0 + i]);
+    sr[i] = __ldg(&r_in[r0 + i]);
+    sd[i] = 0.0;
+  }
+  double rho = S.rho[lp];
+  const double rt2 = S.rt2[lp];
+  int its = 0;
+  __syncthreads();
+  for (;;) {
+    // pass 1: q = A_p p, sigma = p.q
+    double q[RPT];
+    double v1[1] = {0.0};
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int i = j * kNT_SMALL + threadIdx.x;
+      if (i < n) {
+        const int64_t row = (int64_t)r0 + i;
+        q[j] = diag_at<Z>(D, row) * sp[i] + sell_dot<W, Z, true>(L, row, sp, r0);
+        v1[0] += sp[i] * q[j];
+      }
+    }
+    block_allsum<1>(v1, red);
+    const double sigma = v1[0];
+    if (sigma == 0.0) break;  // R7
+    const double alpha = rho / sigma;
+    ++its;
+    // pass 2: d += alpha p, r -= alpha q, z = D^-1 r; r.z, r.r
+    double v2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int i = j * kNT_SMALL + threadIdx.x;
+      if (i < n) {
+        sd[i] = its == 1 ? alpha * sp[i] : sd[i] + alpha * sp[i];
+        const double rn = sr[i] - alpha * q[j];
+        sr[i] = rn;
+        v2[0] += rn * (__drcp_rn(diag_at<Z>(D, (int64_t)r0 + i)) * rn);
+        v2[1] += rn * rn;
+      }
+    }
+    block_allsum<2>(v2, red);
+    if (inner_tol > 0.0 && sqrt(v2[1]) <= inner_tol * sqrt(rt2)) break;  // exact mode / eta
+    const double beta = v2[0] / rho;
+    rho = v2[0];
+    if (its >= m || rho == 0.0) break;
+    // pass 3: p = z + beta p (own rows only; the previous barrier ended all p reads)
+    for (int i = threadIdx.x; i < n; i += kNT_SMALL)
+      sp[i] = __drcp_rn(diag_at<Z>(D, (int64_t)r0 + i)) * sr[i] + beta * sp[i];
+    __syncthreads();
+  }
+  // a4: restricted prolongation of the owned rows
+  if (its > 0)
+    for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
+      const int32_t s = __ldg(&own_slot[r0 + i]);
+      if (s >= 0) x[s] = x[s] + sd[i];
+    }
+  if (threadIdx.x == 0) {
+    S.its[lp] = its;
+    S.inner_total[lp] += its;
+    S.active[lp] = 0;
+  }
+}
+
 // a4: restricted prolongation x[S_p] += d[S_p] (overlap part of d discarded).
 static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_prolong(int64_t tile_base, Tiles T,
                                                              const int32_t* __restrict__ own_slot,

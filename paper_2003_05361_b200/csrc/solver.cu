@@ -240,6 +240,24 @@ static ras_status upload_plan(ras_ctx* c) {
     c->L = Sell{sp, ci, va, nullptr, nullptr, nullptr, nullptr, nullptr};
     c->D = Diag{c->d_diag, nullptr, nullptr};
   }
+  // f2 small-subdomain mode: every local Omega_p fits one CTA's shared memory
+  // (Jacobi / exact PCG; options.reserved_i[3] = 2 forces the tiled path)
+  {
+    int nmax = 0;
+    std::vector<int32_t> ro(pl->subs.size()), nr(pl->subs.size());
+    for (size_t i = 0; i < pl->subs.size(); ++i) {
+      ro[i] = (int32_t)pl->subs[i].row_off;
+      nr[i] = (int32_t)pl->subs[i].nrows_pad;
+      nmax = std::max(nmax, nr[i]);
+    }
+    const bool jac = c->opt.local_solver == RAS_LS_JACOBI_PCG || c->opt.local_solver == RAS_LS_EXACT_PCG;
+    c->small = jac && !c->fuse_p && nmax <= kSmallMaxRows && c->opt.reserved_i[3] != 2;
+    c->small_nmax = nmax;
+    int32_t *dro, *dnr;
+    TRY(upload(c, &dro, ro));
+    TRY(upload(c, &dnr, nr));
+    c->SS = SmallSubs{dro, dnr};
+  }
   c->wR = c->wL = 0;
   for (size_t s = 0; s + 1 < pl->R_sptr.size(); ++s) {
     c->wR = std::max<int>(c->wR, (int)((pl->R_sptr[s + 1] - pl->R_sptr[s]) / 32));
@@ -430,12 +448,14 @@ static void kt_collect(ras_ctx* c) {
 // scheduled while the previous one drains; every kernel starts with
 // griddepcontrol.launch_dependents + griddepcontrol.wait (kernels.cuh), so
 // the data dependence is still the full completion of the predecessor.
+static thread_local size_t g_launch_smem = 0;  // dynamic shared memory of the next KL launch
 template <typename Kern, typename... Args>
 static void pdl_launch(cudaStream_t s, unsigned grid, unsigned block, Kern k, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = g_launch_smem;
+  g_launch_smem = 0;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -573,9 +593,54 @@ static ras_status poll_inactive(ras_ctx* c, cudaStream_t s, const Range& R, bool
 }
 
 // a3: local PCG solve (m iterations; exact mode polls every 16 iterations)
+template <int RPT, int W, bool Z>
+static void small_attr(size_t smem) {
+  static size_t set = 0;  // per instantiation: raise the dynamic shared-memory limit once
+  if (smem > set) {
+    cudaFuncSetAttribute((const void*)k_small_pcg<RPT, W, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+}
+
+// f2 regime: one CTA runs a subdomain's whole PCG + prolongation (k_small_pcg)
+static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol) {
+  const unsigned nsub = R.lp < 0 ? (unsigned)c->nl : 1u;
+  const int lp0 = R.lp < 0 ? 0 : R.lp;
+  const size_t smem = (size_t)3 * c->small_nmax * sizeof(double);
+  const int rpt = (c->small_nmax + kNT_SMALL - 1) / kNT_SMALL;
+#define RAS_SMALL(RPT, W, Z)                                                                                     \
+  small_attr<RPT, W, Z>(smem);                                                                                   \
+  g_launch_smem = smem;                                                                                          \
+  KL(s, K_SPMV, nsub, kNT_SMALL, (k_small_pcg<RPT, W, Z>), lp0, c->SS, c->L, c->D, (const double*)c->d_r,      \
+     (const double*)c->d_p, (const int32_t*)c->d_own_slot, c->d_x, c->S, C, m, inner_tol)
+#define RAS_SMALL_R(W, Z)              \
+  if (rpt <= 2) {                      \
+    RAS_SMALL(2, W, Z);                \
+  } else if (rpt <= 4) {               \
+    RAS_SMALL(4, W, Z);                \
+  } else if (rpt <= 6) {               \
+    RAS_SMALL(6, W, Z);                \
+  } else {                             \
+    RAS_SMALL(9, W, Z);                \
+  }
+#define RAS_SMALL_Z(W) RAS_SMALL_R(W, true)
+#define RAS_SMALL_0(W) RAS_SMALL_R(W, false)
+  if (c->z) {
+    RAS_DISPATCH_ZW(c->zwL, RAS_SMALL_Z);
+  } else {
+    RAS_DISPATCH_W(c->wL, RAS_SMALL_0);
+  }
+#undef RAS_SMALL_0
+#undef RAS_SMALL_Z
+#undef RAS_SMALL_R
+#undef RAS_SMALL
+  return RAS_OK;
+}
+
 ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol, bool exact) {
   const unsigned g = R.ntiles;
   const int64_t tb = R.tile_base;
+  if (c->small) return enq_small_pcg(c, s, R, C, m, inner_tol);
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
     TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
     KL(s, K_ZDOT, g, kNT_STREAM, k_zdot<true>, tb, tiles_next(c), (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
@@ -676,12 +741,16 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 
 // a4
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
+  if (c->small) return RAS_OK;  // k_small_pcg prolongs in the same kernel
   KL(s, K_PROL, R.ntiles, kNT_STREAM, k_prolong, R.tile_base, tiles_next(c), (const int32_t*)c->d_own_slot, (const double*)c->d_d,
      c->d_x, c->S, C);
   return RAS_OK;
 }
 
-static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact, int slot) {
+// check_only: the sweep at k == max_iters only evaluates x^{max_iters} (the
+// device stops there whatever the residual), so its local solve is not enqueued.
+static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact, int slot,
+                             bool check_only) {
   Ctl C{c->d_stop, 0};
   const Range R = range_all(c);
   // a1+a2
@@ -695,6 +764,7 @@ static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, d
   }
   LAUNCH(K_CTRL, k_sync_check<<<1, 32, 0, c->stream>>>(r2g, c->b2_global, tol, max_iters, c->d_sync, c->d_stop,
                                                        c->h_stop_dev + slot));
+  if (check_only) return RAS_OK;
   // a3
   TRY(enq_pcg(c, c->stream, R, C, m, inner_tol, exact));
   // a4
@@ -846,7 +916,7 @@ static ras_status solve_sync(ras_ctx* c, double tol, int64_t max_iters) {
       if (((volatile int32_t*)c->h_stop)[slot]) break;
     }
     if (k > max_iters) break;  // sweep max_iters only checks x^{max_iters}; the device stops there
-    st = sync_sweep(c, tol, max_iters, m, inner_tol, exact, slot);
+    st = sync_sweep(c, tol, max_iters, m, inner_tol, exact, slot, k == max_iters);
     if (st != RAS_OK) break;
     RAS_CUDA(c, cudaEventRecord(ev[slot], c->stream));
   }

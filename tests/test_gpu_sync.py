@@ -25,7 +25,7 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-@pytest.mark.parametrize("fmt", ["plain", "z", "fuse_p", "stage", "z_stage"])
+@pytest.mark.parametrize("fmt", ["plain", "z", "fuse_p", "stage", "z_stage", "tiled", "plain_tiled"])
 @pytest.mark.parametrize("case", ["c1", "voronoi_ragged", "strips"])
 def test_sync_iterates_match_oracle(case, fmt):
     if case == "c1":
@@ -46,8 +46,8 @@ def test_sync_iterates_match_oracle(case, fmt):
     b = ri.rhs(nx * ny, 0)
     K = 6
     ref = oracle_iterates(A, b, owner, gamma, "jacobi", m, K)
-    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", plain=fmt in ("plain", "stage"),
-                                              stage=fmt.endswith("stage")))
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", plain=fmt.startswith("plain") or fmt == "stage",
+                                              stage=fmt.endswith("stage"), tiled=fmt.endswith("tiled") or "stage" in fmt))
     for k in (1, 2, K):
         st, x = s.solve(1e-300, k, "sync")
         assert st == R._ffi.RAS_ENOCONV
@@ -79,7 +79,8 @@ def test_sync_converges_to_tolerance_and_matches_oracle_solution():
     s.close()
 
 
-def test_exact_mode_c1_sweeps_and_solution():
+@pytest.mark.parametrize("tiled", [False, True])
+def test_exact_mode_c1_sweeps_and_solution(tiled):
     # C1: 64x64, 2x2, overlap 2, "exact" local solve (PCG to 1e-14, R6): 106 sweeps (oracle)
     N = 64
     A = ri.laplace_2d(N)
@@ -90,7 +91,7 @@ def test_exact_mode_c1_sweeps_and_solution():
         O.make_local_solver(sb, "exact")
     ref = O.ras_sync(A, b, subs, 1e-8, 1000, record_iterates=True)
     assert ref.sweeps == 106
-    s = R.Solver(A, b, owner, 2, R.options("exact"))
+    s = R.Solver(A, b, owner, 2, R.options("exact", tiled=tiled))
     for k in (1, 5):
         st, x = s.solve(1e-300, k, "sync")
         assert rel(x, ref.iterates[k]) <= 1e-10

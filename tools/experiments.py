@@ -1,0 +1,86 @@
+#!/usr/bin/env python
+"""B200 analogues of the paper's experiments (PAPER §4), one JSON
+line per configuration, through the C ABI:
+
+  overlap   E4/E5 (P574-598): sweeps / updates and time-to-solution vs overlap
+  regime    E3/E9 + NEXT f2 (P527-546, P716-735): the paper's latency regime, 4096
+            unknowns per subdomain, many subdomains per GPU: sync vs async
+  detector  E8 (P678-691): centralized vs decentralized detection (async)
+
+  python tools/experiments.py overlap|regime|detector [--tol 1e-8] [--out FILE]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import ras_inputs as ri  # noqa: E402
+
+
+def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decentral", max_iters=200000, reps=1):
+    import paper_2003_05361_b200 as R
+
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 0)
+    owner = R.partition_regular(nx, ny, 1, px, py, 1)
+    s = R.Solver(A, b, owner, gamma, R.options(solver, m, detector=detector))
+    out = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        st, x = s.solve(tol, max_iters, mode, gather=False)
+        wall = time.perf_counter() - t0
+        d = s.stats()
+        out.append({"status": int(st), "wall_s": wall, "tts_s": d["time_to_solution_s"], "sweeps": d["sweeps"],
+                    "updates_min": d["updates_min"], "updates_median": d["updates_median"],
+                    "updates_max": d["updates_max"], "inner_iters": d["inner_iters_total"],
+                    "rel_residual": d["final_rel_residual"], "resumes": d["resumes"],
+                    "launches": d["kernel_launches"]})
+    s.close()
+    rec = {"grid": [nx, ny], "subdomains": px * py, "tiles": [px, py], "unknowns_per_subdomain": nx * ny // (px * py),
+           "overlap": gamma, "mode": mode, "tol": tol, "local_solver": f"{solver}-PCG m={m}", "detector": detector,
+           "runs": out}
+    if reps > 1:
+        t = [r["tts_s"] for r in out]
+        rec["tts_mean_s"], rec["tts_sd_s"] = float(np.mean(t)), float(np.std(t))
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", choices=["overlap", "regime", "detector"])
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    recs = []
+    if a.which == "overlap":
+        # 1024^2, 4x4 subdomains of 256^2 (E4 shape: few subdomains, growing overlap)
+        for g in (1, 2, 4, 8, 16):
+            for mode in ("sync", "async"):
+                recs.append(run(1024, 1024, 4, 4, g, mode, a.tol, reps=1 if mode == "sync" else a.reps))
+    elif a.which == "regime":
+        # 64^2 = 4096 unknowns per subdomain, overlap 16 (the paper's best async overlap, P594-598)
+        for (px, py) in ((2, 2), (4, 4), (6, 6), (8, 8), (12, 8), (12, 12)):
+            for mode in ("sync", "async"):
+                recs.append(run(64 * px, 64 * py, px, py, 16, mode, a.tol, reps=1 if mode == "sync" else a.reps))
+    else:
+        for det in ("central", "decentral"):
+            recs.append(run(512, 512, 8, 8, 16, "async", a.tol, detector=det, reps=a.reps))
+    lines = [json.dumps({"experiment": a.which, **r}) for r in recs]
+    for ln in lines:
+        print(ln, flush=True)
+    if a.out:
+        with open(a.out, "a") as f:
+            f.write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
