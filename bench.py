@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=SUB, help="owned side per subdomain (debug)")
     ap.add_argument("--plain", action="store_true", help="force plain FP64/int32 SELL (default: SELL-Z when it applies)")
     ap.add_argument("--fuse-p", action="store_true", help="fuse the PCG p update into the next SpMV")
+    ap.add_argument("--path", default="auto", choices=["auto", "tiled", "block", "resident"],
+                    help="local-PCG execution path (ras_pcg_path)")
     return ap.parse_args()
 
 
@@ -292,7 +294,7 @@ def main():
         nccl_id = obj[0]
     t_setup0 = time.perf_counter()
     prob = build_rank_problem(N, rank, args.scale)
-    opts = R.options("jacobi", M_INNER, plain=args.plain, fuse_p=args.fuse_p)
+    opts = R.options("jacobi", M_INNER, plain=args.plain, fuse_p=args.fuse_p, path=args.path)
     solver = R.Solver(prob["A"], prob["b"], prob["owner"], GAMMA, opts,
                       comm={"rank": rank, "world": world, "device": local, "nccl_id": nccl_id,
                             "stream": stream.cuda_stream})
@@ -415,6 +417,7 @@ def main():
             "ras_iters_per_s": args.steps / (ms / 1e3),
             "sweeps_done": sweeps,
             "inner_iters_total": stats["inner_iters_total"],
+            "pcg_path": ["auto", "tiled", "block", "resident"][stats["pcg_path"]],
             "roofline": roof,
             "pcg_path_gbs": pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms else None,
             "kernels": kern,

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RAS_ABI_VERSION 1
+#define RAS_ABI_VERSION 2
 
 typedef struct ras_ctx ras_ctx; /* opaque; one per rank (process) */
 
@@ -67,6 +67,19 @@ typedef enum {
 } ras_local_solver;
 
 typedef enum { RAS_DET_CENTRAL = 0, RAS_DET_DECENTRAL = 1 } ras_detector;
+
+/* How the Jacobi / exact local PCG (a3) is executed on the GPU.  All paths run
+ * the same recurrences; only the summation order of the dot
+ * products differs.  IC(0)/ILU(0) always use TILED.
+ *   TILED    one streaming launch per PCG pass over every subdomain's rows
+ *   BLOCK    one CTA per subdomain runs the whole local solve in shared memory
+ *            (|Omega_p| <= 9216 rows; the paper's 4096-unknown regime)
+ *   RESIDENT a cooperative grid, one CTA per SM, runs each subdomain's whole
+ *            local solve with p, r in shared memory and q, d in registers
+ *            (|Omega_p| <= 24 * 512 rows per CTA of its group); sync mode only,
+ *            async solves fall back to TILED
+ *   AUTO     BLOCK if it applies, else RESIDENT if it applies, else TILED */
+typedef enum { RAS_PCG_AUTO = 0, RAS_PCG_TILED = 1, RAS_PCG_BLOCK = 2, RAS_PCG_RESIDENT = 3 } ras_pcg_path;
 
 /* Sparse matrix A in CSR, possibly a window of rows [row_begin, row_begin+nrows)
  * of the global n x n matrix (so a rank need not hold all of A).  row_ptr is
@@ -103,7 +116,12 @@ typedef struct {
   int32_t poll_interval;         /* sweeps between host polls of the device stop flag (default 4) */
   double async_timeout_s;        /* async wall-clock watchdog, default 1800 s */
   int32_t scripted_flags;        /* test hook: Eq. 2 flags come from ras_set_scripted_flags */
-  int32_t reserved_i[7];
+  /* kernel variants (bitwise-equivalent results up to summation order) */
+  int32_t fuse_p;                /* 1: fuse the PCG p update into the next SpMV (tiled path, plain SELL) */
+  int32_t matrix_format;         /* 0: lane-packed SELL-Z when the matrix allows it; 1: plain SELL-32 */
+  int32_t stage_p;               /* 1: stage p in shared memory in the tiled SpMV */
+  ras_pcg_path pcg_path;         /* default RAS_PCG_AUTO */
+  int32_t reserved_i[3];
   double reserved_d[4];
 } ras_options;
 
@@ -132,7 +150,8 @@ typedef struct {
   double t_residual, t_local_solve, t_prolong, t_exchange, t_convcheck; /* per-phase seconds (Figs. 3a-7a) */
   double model_bytes;          /* algorithmic HBM bytes moved by this rank's kernels */
   int32_t num_subdomains, world;
-  int32_t local_subdomains, reserved0;
+  int32_t local_subdomains;
+  int32_t pcg_path;            /* ras_pcg_path the Jacobi/exact local solves of a sync solve ran on */
   int64_t rows_local;          /* sum |Omega_p| on this rank */
   int64_t halo_values;         /* halo slots on this rank (values received per exchange) */
   int64_t kernel_launches;     /* kernels launched by the last ras_solve on this rank */

@@ -17,6 +17,8 @@ STATUS_NAMES = ["RAS_OK", "RAS_EINVAL", "RAS_ENOTSPD", "RAS_ENOCONV", "RAS_EVERI
 RAS_SYNC, RAS_ASYNC = 0, 1
 RAS_LS_JACOBI_PCG, RAS_LS_IC0_PCG, RAS_LS_ILU0_PCG, RAS_LS_EXACT_PCG = range(4)
 RAS_DET_CENTRAL, RAS_DET_DECENTRAL = 0, 1
+RAS_PCG_AUTO, RAS_PCG_TILED, RAS_PCG_BLOCK, RAS_PCG_RESIDENT = range(4)
+ABI_VERSION = 2  # include/ras.h RAS_ABI_VERSION
 
 I32, I64, F64, U8 = C.c_int32, C.c_int64, C.c_double, C.c_uint8
 P = C.POINTER
@@ -34,7 +36,8 @@ class RasPartition(C.Structure):
 class RasOptions(C.Structure):
     _fields_ = [("local_solver", I32), ("inner_iters", I32), ("inner_tol", F64), ("detector", I32),
                 ("local_crit_owned_only", I32), ("max_resumes", I32), ("use_graphs", I32), ("poll_interval", I32),
-                ("async_timeout_s", F64), ("scripted_flags", I32), ("reserved_i", I32 * 7), ("reserved_d", F64 * 4)]
+                ("async_timeout_s", F64), ("scripted_flags", I32), ("fuse_p", I32), ("matrix_format", I32), ("stage_p", I32),
+                ("pcg_path", I32), ("reserved_i", I32 * 3), ("reserved_d", F64 * 4)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -54,7 +57,7 @@ class RasStats(C.Structure):
                 ("inner_iters_total", I64), ("final_rel_residual", F64),
                 ("t_residual", F64), ("t_local_solve", F64), ("t_prolong", F64), ("t_exchange", F64),
                 ("t_convcheck", F64), ("model_bytes", F64), ("num_subdomains", I32), ("world", I32),
-                ("local_subdomains", I32), ("reserved0", I32), ("rows_local", I64), ("halo_values", I64),
+                ("local_subdomains", I32), ("pcg_path", I32), ("rows_local", I64), ("halo_values", I64),
                 ("kernel_launches", I64), ("fresh_halo_reads", I64)]
 
     def as_dict(self):
@@ -123,6 +126,8 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.ras_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"{LIB_PATH} has ABI {L.ras_abi_version()}, the binding expects {ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 

@@ -23,7 +23,7 @@ struct DevBuf {
 
 struct AsyncRt;  // async-mode runtime (async.cu)
 
-enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_ZDOT, K_NKINDS };
+enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_ZDOT, K_SMALL, K_RESID, K_NKINDS };
 
 // A range of tiles: every local subdomain (lp < 0) or one subdomain.
 struct Range {
@@ -53,6 +53,7 @@ struct KTimer {
 
 struct ModelBytes {  // algorithmic bytes per launch over the whole row space
   double residual, spmv_dot, update_dot, pupdate, prolong, pack, trsv, zdot;
+  double local_solve;  // BLOCK / RESIDENT: compulsory HBM bytes of one whole local-solve launch
 };
 
 }  // namespace ras
@@ -90,11 +91,18 @@ struct ras_ctx {
   double* d_r = nullptr;
   double* d_p = nullptr;
   double* d_p2 = nullptr;  // p double buffer (fused p update + SpMV)
-  bool fuse_p = false;     // options.reserved_i[0]: fuse pass 3 into the next pass 1
-  bool stage = false;      // options.reserved_i[2]: shared-memory staging of p in the SpMV
-  bool small = false;      // f2: one CTA per subdomain runs the whole local PCG (k_small_pcg)
+  bool fuse_p = false;     // options.fuse_p: fuse pass 3 into the next pass 1
+  bool stage = false;      // options.stage_p: shared-memory staging of p in the SpMV
+  int path = RAS_PCG_TILED;  // local-PCG path of batched (sync) solves, ras_pcg_path
+  bool small = false;      // path == BLOCK: one CTA per subdomain runs the whole local PCG (k_small_pcg)
   int small_nmax = 0;
   ras::SmallSubs SS{};
+  // path == RESIDENT (k_resident_pcg): cooperative grid of ngroups * gs CTAs
+  ras::ResidentCtl RC{};
+  int resid_rpt = 0;        // rows-per-thread instantiation
+  size_t resid_smem = 0;    // dynamic shared memory per CTA (p, r of the largest chunk)
+  int resid_chunk = 0;      // rows per CTA of the largest subdomain
+  unsigned long long* d_resid_slots = nullptr;
   double* d_q = nullptr;
   double* d_d = nullptr;
   // IC(0)/ILU(0) path (a3')

@@ -791,6 +791,413 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Grid-resident regime (subdomains of up to ~1.4M rows, e.g. C2's 1024^2 tiles
+// + overlap): a persistent cooperative grid, one CTA per SM, split into groups
+// of gs CTAs; a group runs the WHOLE Jacobi-PCG local solve of one subdomain
+// (then the next one: subdomains lp_base + g, + ngroups, ...) with its rows
+// partitioned into contiguous chunks, one per CTA, resident on chip for all m
+// iterations: p, r and the diagonal in shared memory, q and d in registers.
+// HBM is touched once per sweep (r, p in; x[S_p] out; the matrix streams from
+// L2/L1), instead of three passes per iteration.
+//
+// Reductions: two group-wide sums per iteration.  No atomics: every CTA
+// release-stores its partial into its own slot of a 3-deep ring (slot of
+// barrier k+1 reset to a sentinel before the store of barrier k), and warp 0 of
+// every CTA polls the group's slots until none holds the sentinel, then sums
+// them in fixed order -- bitwise-identical alpha / beta / stop decisions in all
+// CTAs.  The ring is safe because a CTA stores for barrier k only after every
+// CTA has finished reading the slots of barrier k-2 (it passed barrier k-1).
+//
+// Halo: a row's neighbours owned by another CTA of the group are read from L2.
+// The p update of iteration it-1 is fused into the SpMV of iteration it: each
+// CTA publishes, for its export band only (rows other CTAs reference, host-
+// computed), z = D^-1 r (pass 2) and p (pass 3) of every iteration; a reader
+// recomputes p_it(c) = fma(beta, p_{it-1}(c), z(c)) with the same expression
+// the owner uses, so only the two reductions synchronise CTAs.  p_it lives in
+// pbuf[(it-1) & 1] (pbuf[0] = the p written by k_residual, all rows).
+// ---------------------------------------------------------------------------
+#ifndef RAS_NT_RESID
+#define RAS_NT_RESID 1024
+#endif
+#ifndef RAS_PD_RESID
+#define RAS_PD_RESID 1
+#endif
+constexpr int kNT_RESID = RAS_NT_RESID;
+constexpr int kResidMaxRPT = kNT_RESID >= 1024 ? 8 : 16;  // rows per thread: q in registers (2 * RPT registers)
+constexpr unsigned long long kSlotEmpty = 0xffffffffffffffffull;  // NaN pattern never stored (see group_allsum)
+constexpr int kMaxGroupCTAs = 160;  // >= SMs of a B200 (148): CTAs of one group
+
+struct ResidentCtl {
+  const int2* band;           // per (local subdomain, CTA of group): chunk-relative export band
+                              // {lo_end, hi_begin}: rows i < lo_end or i >= hi_begin are read by others
+  unsigned long long* slots;  // per group [3 ring][2 values][gs] partial sums, kSlotEmpty before launch
+  double* pbuf0;              // p_1 (k_residual output) / odd iterations' p, export rows
+  double* pbuf1;              // even iterations' p, export rows
+  double* zg;                 // z of the export rows
+  int32_t ngroups, gs;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// all 32 lanes end with the same bitwise value (xor butterfly: each stage adds
+// the same two operands on both partner lanes)
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Group-wide sum of NV values; every thread of every CTA of the group returns
+// the identical result.  The CTA's earlier global stores (export band) are
+// published by the release store (ordered after them by the CTA barrier);
+// readers poll with acquire loads, and the CTA barrier after the poll orders
+// every thread's later halo loads after them.  seq = reductions completed.
+template <int NV>
+__device__ __forceinline__ void group_allsum(double (&v)[NV], double (*red)[kNT_RESID / 32], double* bc,
+                                             unsigned long long* slots, int gs, int c, unsigned& seq) {
+  constexpr int NW = kNT_RESID / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double s = warp_sum(v[j]);
+    if (lane == 0) red[j][w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const unsigned ring = seq % 3, nxt = (seq + 1) % 3;
+    double s[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) s[j] = warp_sum(lane < NW ? red[j][lane] : 0.0);
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) st_relaxed_gpu_u64(&slots[(nxt * 2 + j) * gs + c], kSlotEmpty);
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        unsigned long long u = (unsigned long long)__double_as_longlong(s[j]);
+        if (u == kSlotEmpty) u = 0x7ff8000000000000ull;  // a NaN partial stays a NaN, never the sentinel
+        st_release_gpu_u64(&slots[(ring * 2 + j) * gs + c], u);
+      }
+    }
+    // poll: each lane owns slots lane, lane + 32, ... (<= kMaxSlotsPerLane) and
+    // re-loads only the ones still empty, all in flight together
+    constexpr int KS = (kMaxGroupCTAs + 31) / 32;
+    unsigned long long u[NV][KS];
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int t = 0; t < KS; ++t) u[j][t] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
+    for (;;) {
+      bool done = true;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int t = 0; t < KS; ++t)
+          if (u[j][t] == kSlotEmpty) u[j][t] = ld_acquire_gpu_u64(&slots[(ring * 2 + j) * gs + lane + 32 * t]);
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int t = 0; t < KS; ++t) done = done && u[j][t] != kSlotEmpty;
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+    double acc[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      acc[j] = 0.0;
+#pragma unroll
+      for (int t = 0; t < KS; ++t) acc[j] += __longlong_as_double((long long)u[j][t]);  // lane + 32t order
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      acc[j] = warp_allsum(acc[j]);
+      if (lane == 0) bc[j] = acc[j];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = bc[j];
+  ++seq;
+}
+
+// Off-diagonal part of row `row` of the local matrix: sum_k a_k * P(col_k) (SELL-Z
+// lane-packed width W in {4, 8}, or plain SELL with W > 0 unrolled / W == 0 loop).
+// Z values come from the shared-memory copy of the dictionary `tab`.
+template <int W, bool Z, class G>
+__device__ __forceinline__ double resident_row(const Sell& L, int64_t row, const double* tab, G P) {
+  double acc = 0.0;
+  const int64_t sl = row >> 5;
+  if (Z) {
+    uint32_t cw[W / 4 > 0 ? W / 4 : 1];
+    uint32_t dw[W / 2 > 0 ? W / 2 : 1];
+    int32_t kb[W > 0 ? W : 1];
+    if (W == 4) {
+      cw[0] = __ldg(reinterpret_cast<const unsigned int*>(L.code) + row);
+      const uint2 dd = __ldg(reinterpret_cast<const uint2*>(L.d16) + row);
+      dw[0] = dd.x;
+      dw[1] = dd.y;
+      const int4 b4 = __ldg(reinterpret_cast<const int4*>(L.kbase) + sl);
+      kb[0] = b4.x, kb[1] = b4.y, kb[2] = b4.z, kb[3] = b4.w;
+    } else {
+      const uint2 cc = __ldg(reinterpret_cast<const uint2*>(L.code) + row);
+      cw[0] = cc.x;
+      cw[W / 4 - 1] = cc.y;
+      const uint4 dd = __ldg(reinterpret_cast<const uint4*>(L.d16) + row);
+      dw[0] = dd.x, dw[1] = dd.y, dw[2] = dd.z, dw[W / 2 - 1] = dd.w;
+      const int4 b0 = __ldg(reinterpret_cast<const int4*>(L.kbase) + 2 * sl);
+      const int4 b1 = __ldg(reinterpret_cast<const int4*>(L.kbase) + 2 * sl + 1);
+      kb[0] = b0.x, kb[1] = b0.y, kb[2] = b0.z, kb[3] = b0.w;
+      kb[W - 4] = b1.x, kb[W - 3] = b1.y, kb[W - 2] = b1.z, kb[W - 1] = b1.w;
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint32_t code = (cw[k / 4] >> (8 * (k % 4))) & 0xffu;
+      const uint32_t off = (dw[k / 2] >> (16 * (k % 2))) & 0xffffu;
+      const int32_t col = kb[k] >= 0 ? kb[k] + (int32_t)off : __ldg(&L.wide[(-kb[k] - 1) * 32 + (row & 31)]);
+      acc += tab[code] * P(col);
+    }
+  } else {
+    const int64_t base = __ldg(&L.sptr[sl]);
+    const int w = (int)((__ldg(&L.sptr[sl + 1]) - base) >> 5);
+    const double* vp = L.val + base + (row & 31);
+    const int32_t* cp = L.col + base + (row & 31);
+    if (W > 0) {
+      double vv[W > 0 ? W : 1];
+      int32_t cc[W > 0 ? W : 1];
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (k < w) {
+          vv[k] = __ldg(vp + 32 * k);
+          cc[k] = __ldg(cp + 32 * k);
+        }
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (k < w) acc += vv[k] * P(cc[k]);
+    } else {
+      for (int k = 0; k < w; ++k) acc += __ldg(vp + 32 * k) * P(__ldg(cp + 32 * k));
+    }
+  }
+  return acc;
+}
+
+// Runs after k_residual<JAC>/k_finish<F_RES_JAC> (r, p = z, rho, rt2, active set).
+// Launched cooperatively with grid = ngroups * gs CTAs (all co-resident).
+// Dynamic shared memory per chunk row: p, r, d (FP64) + the diagonal (Z: uint8
+// code into the dictionary and its reciprocals, both copied to shared memory;
+// plain: FP64); q lives in registers.  Rows of the export band are the only
+// ones with off-chunk columns (A_p is symmetric), so every other row gathers p
+// from shared memory without range checks.
+template <int RPT, int W, bool Z>
+static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_base, int nsub, SmallSubs SS,
+                                                                      ResidentCtl RC, Sell L, Diag D,
+                                                                      const double* __restrict__ r_in,
+                                                                      const int32_t* __restrict__ own_slot,
+                                                                      double* __restrict__ x, Scal S, Ctl C,
+                                                                      int32_t m, double inner_tol, int32_t chunk_max,
+                                                                      int32_t ntable) {
+  constexpr int NT = kNT_RESID;
+  extern __shared__ double smem[];
+  __shared__ double red[2][NT / 32];
+  __shared__ double bc[2];
+  double* sp = smem;                  // p of the chunk
+  double* sr = sp + chunk_max;        // r
+  double* sd = sr + chunk_max;        // d (the correction)
+  double* stab = sd + chunk_max;      // Z: dictionary values [256]
+  double* sinv = stab + 256;          // Z: __drcp_rn of every dictionary value [256]
+  uint8_t* sdc = reinterpret_cast<uint8_t*>(sinv + 256);  // Z: diagonal codes of the chunk
+  double* sdg = stab;                 // plain: diagonal of the chunk
+  const int gs = RC.gs;
+  const int g = blockIdx.x / gs, c = blockIdx.x - g * gs;
+  unsigned long long* slots = RC.slots + (size_t)6 * gs * g;
+  unsigned seq = 0;
+  if (Z)
+    for (int i = threadIdx.x; i < ntable; i += NT) {
+      const double v = __ldg(&D.table[i]);
+      stab[i] = v;
+      sinv[i] = __drcp_rn(v);
+    }
+  for (int lp = lp_base + g; lp < lp_base + nsub; lp += RC.ngroups) {
+    if (stopped(C, lp) || !S.active[lp]) continue;  // uniform over the group
+    const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+    const int chunk = ((n / 32 + gs - 1) / gs) * 32;
+    const int a = min(n, c * chunk), nr = min(n, a + chunk) - a;
+    const int2 band = RC.band[lp * gs + c];
+    // chunk row i is row-space row rb + i (rb is a multiple of 32: slice aligned);
+    // every array below is re-based to the chunk so indices stay 32-bit
+    const int32_t rb = r0 + a;
+    double* const zg = RC.zg + rb;
+    const double* const pb0 = RC.pbuf0 + rb;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr; i += NT) {
+      sp[i] = __ldcg(&pb0[i]);
+      sr[i] = __ldcg(&r_in[rb + i]);
+      if (Z)
+        sdc[i] = __ldg(&D.code[rb + i]);
+      else
+        sdg[i] = __ldg(&D.v[rb + i]);
+    }
+    double q[RPT];
+    double rho = S.rho[lp];
+    const double rt2 = S.rt2[lp];
+    double beta = 0.0;
+    int its = 0;
+    __syncthreads();
+    auto diag = [&](int i) -> double { return Z ? stab[sdc[i]] : sdg[i]; };
+    auto dinv_r = [&](int i, double r) -> double {  // z = D^-1 r, bitwise as __drcp_rn(diag) * r
+      return __dmul_rn(Z ? sinv[sdc[i]] : __drcp_rn(sdg[i]), r);
+    };
+    for (;;) {
+      // pass 1 (+ the fused pass 3 of the previous iteration for halo columns):
+      // q = A_p p_it, sigma = p_it . q.  li = chunk-relative column.
+      const double* const pold = ((its & 1) ? RC.pbuf0 : RC.pbuf1) + rb;  // p_{it-1} = pbuf[(it-2) & 1]
+      const bool first = its == 0;
+      const double bt = beta;
+      auto Pb = [&](int li) -> double {  // row of the export band: the column may be another CTA's
+        if ((unsigned)li < (unsigned)nr) return sp[li];
+        if (first) return __ldcg(&pb0[li]);
+        return __fma_rn(bt, __ldcg(&pold[li]), __ldcg(&zg[li]));
+      };
+      double v1 = 0.0;
+      if (Z) {
+        // SELL-Z rows software-pipelined: the codes / offsets / slice bases of
+        // row j + PD are in flight while row j is computed (L2 latency hiding)
+        constexpr int PD = RPT < RAS_PD_RESID ? RPT : RAS_PD_RESID;
+        constexpr int W4 = W / 4 > 0 ? W / 4 : 1, W2 = W / 2 > 0 ? W / 2 : 1, WW = W > 0 ? W : 1;
+        const uint8_t* const codeb = L.code + (size_t)rb * W;
+        const uint16_t* const d16b = L.d16 + (size_t)rb * W;
+        const int32_t* const kbb = L.kbase + (size_t)(rb >> 5) * W;
+        uint32_t bcw[PD][W4], bdw[PD][W2];
+        int32_t bkb[PD][WW];
+        auto zload = [&](int j, int bi) {
+          const int i = j * NT + threadIdx.x;
+          if (i < nr) {
+            if (W == 4) {
+              bcw[bi][0] = __ldg(reinterpret_cast<const unsigned int*>(codeb) + i);
+              const uint2 dd = __ldg(reinterpret_cast<const uint2*>(d16b) + i);
+              bdw[bi][0] = dd.x;
+              bdw[bi][W2 - 1] = dd.y;
+              const int4 b4 = __ldg(reinterpret_cast<const int4*>(kbb) + (i >> 5));
+              bkb[bi][0] = b4.x, bkb[bi][1] = b4.y, bkb[bi][2] = b4.z, bkb[bi][WW - 1] = b4.w;
+            } else {
+              const uint2 cc = __ldg(reinterpret_cast<const uint2*>(codeb) + i);
+              bcw[bi][0] = cc.x;
+              bcw[bi][W4 - 1] = cc.y;
+              const uint4 dd = __ldg(reinterpret_cast<const uint4*>(d16b) + i);
+              bdw[bi][0] = dd.x, bdw[bi][1] = dd.y, bdw[bi][2] = dd.z, bdw[bi][W2 - 1] = dd.w;
+              const int4 b0 = __ldg(reinterpret_cast<const int4*>(kbb) + 2 * (i >> 5));
+              const int4 b1 = __ldg(reinterpret_cast<const int4*>(kbb) + 2 * (i >> 5) + 1);
+              bkb[bi][0] = b0.x, bkb[bi][1] = b0.y, bkb[bi][2] = b0.z, bkb[bi][3] = b0.w;
+              bkb[bi][WW - 4] = b1.x, bkb[bi][WW - 3] = b1.y, bkb[bi][WW - 2] = b1.z, bkb[bi][WW - 1] = b1.w;
+            }
+          }
+        };
+#pragma unroll
+        for (int j = 0; j < PD; ++j) zload(j, j);
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const int i = j * NT + threadIdx.x;
+          const int bi = j % PD;
+          if (i < nr) {
+            const double pi = sp[i];
+            const bool inner = i >= band.x && i < band.y;
+            // a slice with a wide group (base < 0: int32 columns) takes the generic decoder
+            bool wide = false;
+#pragma unroll
+            for (int k = 0; k < W; ++k) wide = wide || bkb[bi][k] < 0;
+            double off = 0.0;
+            if (!wide) {
+#pragma unroll
+              for (int k = 0; k < W; ++k) {
+                const uint32_t code = (bcw[bi][k / 4] >> (8 * (k % 4))) & 0xffu;
+                const int li = bkb[bi][k] - rb + (int)((bdw[bi][k / 2] >> (16 * (k % 2))) & 0xffffu);
+                off += stab[code] * (inner ? sp[li] : Pb(li));
+              }
+            } else {
+              off = resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return Pb(col - rb); });
+            }
+            q[j] = diag(i) * pi + off;
+            v1 += pi * q[j];
+          }
+          if (j + PD < RPT) zload(j + PD, bi);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const int i = j * NT + threadIdx.x;
+          if (i < nr) {
+            const double pi = sp[i];
+            const double off = (i >= band.x && i < band.y)
+                                   ? resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return sp[col - rb]; })
+                                   : resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return Pb(col - rb); });
+            q[j] = diag(i) * pi + off;
+            v1 += pi * q[j];
+          }
+        }
+      }
+      double s1[1] = {v1};
+      group_allsum<1>(s1, red, bc, slots, gs, c, seq);
+      const double sigma = s1[0];
+      if (sigma == 0.0) break;  // R7
+      const double alpha = rho / sigma;
+      ++its;
+      // pass 2: d += alpha p, r -= alpha q, z = D^-1 r (published for the export band); r.z, r.r
+      double v2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int i = j * NT + threadIdx.x;
+        if (i < nr) {
+          const double pi = sp[i];
+          sd[i] = its == 1 ? alpha * pi : sd[i] + alpha * pi;
+          const double rn = sr[i] - alpha * q[j];
+          sr[i] = rn;
+          const double z = dinv_r(i, rn);
+          if (i < band.x || i >= band.y) __stcg(&zg[i], z);
+          v2[0] += rn * z;
+          v2[1] += rn * rn;
+        }
+      }
+      group_allsum<2>(v2, red, bc, slots, gs, c, seq);
+      if (inner_tol > 0.0 && sqrt(v2[1]) <= inner_tol * sqrt(rt2)) break;  // exact mode / eta
+      beta = v2[0] / rho;
+      rho = v2[0];
+      if (its >= m || rho == 0.0) break;
+      // pass 3 (own rows): p_{its+1} = z + beta p_its -> shared memory, export band -> pbuf[its & 1]
+      double* const pw = ((its & 1) ? RC.pbuf1 : RC.pbuf0) + rb;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int i = j * NT + threadIdx.x;
+        if (i < nr) {
+          const double pn = __fma_rn(beta, sp[i], dinv_r(i, sr[i]));
+          sp[i] = pn;
+          if (i < band.x || i >= band.y) __stcg(&pw[i], pn);
+        }
+      }
+      __syncthreads();
+    }
+    // a4: restricted prolongation of the chunk's owned rows
+    if (its > 0) {
+      for (int i = threadIdx.x; i < nr; i += NT) {
+        const int32_t s = __ldg(&own_slot[rb + i]);
+        if (s >= 0) x[s] = x[s] + sd[i];
+      }
+    }
+    if (c == 0 && threadIdx.x == 0) {
+      S.its[lp] = its;
+      S.inner_total[lp] += its;
+      S.active[lp] = 0;
+    }
+  }
+}
+
 // a4: restricted prolongation x[S_p] += d[S_p] (overlap part of d discarded).
 static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_prolong(int64_t tile_base, Tiles T,
                                                              const int32_t* __restrict__ own_slot,

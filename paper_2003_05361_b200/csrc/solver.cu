@@ -135,6 +135,96 @@ static void compute_model_bytes(ras_ctx* c) {
   c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + db /*diag*/ + 16 /*r*/ + 16 /*d*/);
   c->mb.prolong = rows * 4.0 + (double)owned * (8 /*d*/ + 16 /*x*/);
   c->mb.pack = (double)c->n_send * (4 + 8 + 8);
+  // BLOCK / RESIDENT: one launch = the whole local solve of every subdomain; its
+  // compulsory HBM traffic is r, p (from k_residual), the local matrix and
+  // diagonal once, the prolong map, and x[S_p] read + written.  Every further
+  // PCG iteration runs from shared memory / registers / L2.
+  c->mb.local_solve = rows * (8 /*r*/ + 8 /*p*/ + db /*diag*/ + 4 /*own_slot*/) + ent_L * eb + (double)owned * 16.0;
+}
+
+// RESIDENT path setup (k_resident_pcg): group count / size, rows per thread,
+// export bands, barrier counters and partial-sum slots.  Leaves c->path alone
+// when no configuration fits (the caller falls back to TILED).
+static const void* resident_kernel(int rpt, bool z, int w) {
+#define RAS_RK(RPT)                                                                             \
+  if (z) return w == 4 ? (const void*)k_resident_pcg<RPT, 4, true> : (const void*)k_resident_pcg<RPT, 8, true>; \
+  return w <= 8 ? (const void*)k_resident_pcg<RPT, 8, false> : (const void*)k_resident_pcg<RPT, 0, false>;
+  // only the rows-per-thread counts the register budget allows are instantiated
+  if (rpt <= 4) {
+    RAS_RK(4)
+  } else if (rpt <= 8 || kResidMaxRPT == 8) {
+    RAS_RK(8)
+  } else if (rpt <= 12) {
+    RAS_RK(kResidMaxRPT >= 12 ? 12 : 8)
+  } else {
+    RAS_RK(kResidMaxRPT)
+  }
+#undef RAS_RK
+}
+
+static ras_status setup_resident(ras_ctx* c, int nmax) {
+  const ras_plan* pl = c->plan;
+  int sms = 0, smem_optin = 0;
+  RAS_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  RAS_CUDA(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  // shared memory per chunk row: p, r, d (24 B) + diagonal (SELL-Z: 1 B code, plain: 8 B);
+  // + the dictionary and its reciprocals (4 KB)
+  const int row_b = c->z ? 25 : 32;
+  const int cap = std::min(kResidMaxRPT * kNT_RESID, ((smem_optin - 4096 - 2048) / row_b) / 32 * 32);
+  auto chunk_of = [](int n, int gs) { return ((n / 32 + gs - 1) / gs) * 32; };
+  const int nl = c->nl;
+  int kfit = 0;  // most groups (concurrent subdomains) whose chunks still fit
+  for (int k = 1; k <= std::min(nl, sms); ++k)
+    if (chunk_of(nmax, sms / k) <= cap) kfit = k;
+  if (kfit == 0) return RAS_OK;
+  const int waves = (nl + kfit - 1) / kfit;
+  int k = kfit;  // fewest groups with the same number of waves = most CTAs per subdomain
+  while (k > 1 && (nl + k - 2) / (k - 1) == waves) --k;
+  const int gs = std::min(sms / k, kMaxGroupCTAs);
+  const int chunk = chunk_of(nmax, gs);
+  if (chunk > cap) return RAS_OK;
+  const int need = (chunk + kNT_RESID - 1) / kNT_RESID;
+  const int rpt = need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : 16;
+  const size_t smem = (size_t)24 * chunk + (c->z ? 4096 + (size_t)chunk : (size_t)8 * chunk);
+  const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL);
+  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_RESID, smem));
+  if (per_sm < 1) return RAS_OK;
+  // export bands: chunk rows other CTAs of the group read (Ap columns, subdomain-relative)
+  std::vector<int2> band((size_t)nl * gs);
+  for (int lp = 0; lp < nl; ++lp) {
+    const auto& S = pl->subs[lp];
+    const int n = (int)S.nrows_pad, ch = chunk_of(n, gs);
+    std::vector<int> lo(gs, 0), hi(gs), len(gs);
+    for (int cc = 0; cc < gs; ++cc) {
+      const int a = std::min(n, cc * ch);
+      len[cc] = std::min(n, a + ch) - a;
+      hi[cc] = len[cc];
+    }
+    for (int i = 0; i < n; ++i) {
+      const int ci = i / ch;
+      for (int64_t e = pl->Ap_ptr[S.row_off + i]; e < pl->Ap_ptr[S.row_off + i + 1]; ++e) {
+        const int j = pl->Ap_col[e], cj = j / ch;
+        if (cj == ci) continue;
+        const int lj = j - cj * ch;
+        if (lj < len[cj] / 2)
+          lo[cj] = std::max(lo[cj], lj + 1);
+        else
+          hi[cj] = std::min(hi[cj], lj);
+      }
+    }
+    for (int cc = 0; cc < gs; ++cc) band[(size_t)lp * gs + cc] = make_int2(lo[cc], hi[cc]);
+  }
+  int2* dband;
+  TRY(upload(c, &dband, band));
+  TRY(zalloc(c, &c->d_resid_slots, (size_t)k * 6 * gs));
+  c->RC = ResidentCtl{dband, c->d_resid_slots, c->d_p, c->d_p2, c->d_q, k, gs};
+  c->resid_rpt = rpt;
+  c->resid_chunk = chunk;
+  c->resid_smem = smem;
+  c->path = RAS_PCG_RESIDENT;
+  return RAS_OK;
 }
 
 // a3' setup: IC(0)/ILU(0) factors + level sets on the host (factor.cpp), uploaded once
@@ -199,10 +289,10 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(upload(c, &c->d_b, pl->b_loc));
   TRY(upload(c, &c->d_own_slot, pl->own_slot));
   // Lane-packed SELL-Z (dictionary values, 16-bit column offsets) whenever the
-  // matrix allows it, unless plain SELL is forced (options.reserved_i[1] = 2);
+  // matrix allows it, unless plain SELL is forced (options.matrix_format = 1);
   // the fused-p kernel reads the plain format.  Only one format lives on the
   // device.  Measured on B200 (round 1, C2): 7.9 ms/sweep SELL-Z vs 9.3 plain.
-  c->z = pl->z_ok && !c->fuse_p && c->opt.reserved_i[1] != 2;
+  c->z = pl->z_ok && !c->fuse_p && c->opt.matrix_format != 1;
   int64_t* sp;
   if (c->z) {
     double* tb;
@@ -240,24 +330,6 @@ static ras_status upload_plan(ras_ctx* c) {
     c->L = Sell{sp, ci, va, nullptr, nullptr, nullptr, nullptr, nullptr};
     c->D = Diag{c->d_diag, nullptr, nullptr};
   }
-  // f2 small-subdomain mode: every local Omega_p fits one CTA's shared memory
-  // (Jacobi / exact PCG; options.reserved_i[3] = 2 forces the tiled path)
-  {
-    int nmax = 0;
-    std::vector<int32_t> ro(pl->subs.size()), nr(pl->subs.size());
-    for (size_t i = 0; i < pl->subs.size(); ++i) {
-      ro[i] = (int32_t)pl->subs[i].row_off;
-      nr[i] = (int32_t)pl->subs[i].nrows_pad;
-      nmax = std::max(nmax, nr[i]);
-    }
-    const bool jac = c->opt.local_solver == RAS_LS_JACOBI_PCG || c->opt.local_solver == RAS_LS_EXACT_PCG;
-    c->small = jac && !c->fuse_p && nmax <= kSmallMaxRows && c->opt.reserved_i[3] != 2;
-    c->small_nmax = nmax;
-    int32_t *dro, *dnr;
-    TRY(upload(c, &dro, ro));
-    TRY(upload(c, &dnr, nr));
-    c->SS = SmallSubs{dro, dnr};
-  }
   c->wR = c->wL = 0;
   for (size_t s = 0; s + 1 < pl->R_sptr.size(); ++s) {
     c->wR = std::max<int>(c->wR, (int)((pl->R_sptr[s + 1] - pl->R_sptr[s]) / 32));
@@ -291,6 +363,36 @@ static ras_status upload_plan(ras_ctx* c) {
   TRY(zalloc(c, &c->d_p2, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_q, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_d, (size_t)c->rows_pad));
+  // Local-PCG execution path (ras_pcg_path): BLOCK when every local Omega_p fits
+  // one CTA's shared memory (the paper's 4096-unknown regime, NEXT f2), else
+  // RESIDENT when a cooperative grid can keep every subdomain on chip, else TILED.
+  {
+    int nmax = 0;
+    std::vector<int32_t> ro(pl->subs.size()), nr(pl->subs.size());
+    for (size_t i = 0; i < pl->subs.size(); ++i) {
+      ro[i] = (int32_t)pl->subs[i].row_off;
+      nr[i] = (int32_t)pl->subs[i].nrows_pad;
+      nmax = std::max(nmax, nr[i]);
+    }
+    const int req = c->opt.pcg_path;
+    if (req < RAS_PCG_AUTO || req > RAS_PCG_RESIDENT) return set_err(c, RAS_EINVAL, "unknown pcg_path");
+    const bool jac = c->opt.local_solver == RAS_LS_JACOBI_PCG || c->opt.local_solver == RAS_LS_EXACT_PCG;
+    const bool eligible = jac && !c->fuse_p && !c->stage;
+    if (req != RAS_PCG_AUTO && req != RAS_PCG_TILED && !eligible)
+      return set_err(c, RAS_EINVAL, "pcg_path BLOCK/RESIDENT need Jacobi or exact PCG without fuse_p/stage_p");
+    c->small = eligible && nmax <= kSmallMaxRows && (req == RAS_PCG_AUTO || req == RAS_PCG_BLOCK);
+    if (req == RAS_PCG_BLOCK && !c->small)
+      return set_err(c, RAS_EINVAL, "pcg_path BLOCK needs every |Omega_p| <= 9216 rows (padded)");
+    c->small_nmax = nmax;
+    c->path = c->small ? RAS_PCG_BLOCK : RAS_PCG_TILED;
+    int32_t *dro, *dnr;
+    TRY(upload(c, &dro, ro));
+    TRY(upload(c, &dnr, nr));
+    c->SS = SmallSubs{dro, dnr};
+    if (!c->small && eligible && (req == RAS_PCG_AUTO || req == RAS_PCG_RESIDENT)) TRY(setup_resident(c, nmax));
+    if (req == RAS_PCG_RESIDENT && c->path != RAS_PCG_RESIDENT)
+      return set_err(c, RAS_EINVAL, "pcg_path RESIDENT: a subdomain is too large for the cooperative grid");
+  }
   const int nl = c->nl;
   TRY(zalloc(c, &c->S.rt2, nl));
   TRY(zalloc(c, &c->S.rho, nl));
@@ -611,7 +713,7 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
 #define RAS_SMALL(RPT, W, Z)                                                                                     \
   small_attr<RPT, W, Z>(smem);                                                                                   \
   g_launch_smem = smem;                                                                                          \
-  KL(s, K_SPMV, nsub, kNT_SMALL, (k_small_pcg<RPT, W, Z>), lp0, c->SS, c->L, c->D, (const double*)c->d_r,      \
+  KL(s, K_SMALL, nsub, kNT_SMALL, (k_small_pcg<RPT, W, Z>), lp0, c->SS, c->L, c->D, (const double*)c->d_r,      \
      (const double*)c->d_p, (const int32_t*)c->d_own_slot, c->d_x, c->S, C, m, inner_tol)
 #define RAS_SMALL_R(W, Z)              \
   if (rpt <= 2) {                      \
@@ -637,10 +739,41 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
   return RAS_OK;
 }
 
+// RESIDENT path: one cooperative launch runs every local subdomain's whole PCG
+// + prolongation (k_resident_pcg), batched (sync) solves only.
+static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m, double inner_tol) {
+  // every reduction slot starts empty (kSlotEmpty = all ones)
+  RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff, (size_t)c->RC.ngroups * 6 * c->RC.gs * 8, s));
+  const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL);
+  int lp0 = 0, nsub = c->nl;
+  const double* r_in = c->d_r;
+  const int32_t* own = c->d_own_slot;
+  double* x = c->d_x;
+  int32_t chunk_max = c->resid_chunk;
+  int32_t ntable = c->z ? (int32_t)c->plan->z_table.size() : 0;
+  void* args[] = {&lp0,  &nsub, &c->SS, &c->RC, &c->L,      &c->D,      &r_in,  &own,
+                  &x,    &c->S, &C,     &m,     &inner_tol, &chunk_max, &ntable};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(c->RC.ngroups * c->RC.gs));
+  cfg.blockDim = dim3(kNT_RESID);
+  cfg.dynamicSmemBytes = c->resid_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int ti = kt_begin(c, s);
+  RAS_CUDA(c, cudaLaunchKernelExC(&cfg, fn, args));
+  kt_end(c, s, K_RESID, ti);
+  return RAS_OK;
+}
+
 ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol, bool exact) {
   const unsigned g = R.ntiles;
   const int64_t tb = R.tile_base;
   if (c->small) return enq_small_pcg(c, s, R, C, m, inner_tol);
+  if (c->path == RAS_PCG_RESIDENT && R.lp < 0) return enq_resident_pcg(c, s, C, m, inner_tol);
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
     TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
     KL(s, K_ZDOT, g, kNT_STREAM, k_zdot<true>, tb, tiles_next(c), (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
@@ -742,6 +875,7 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 // a4
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
   if (c->small) return RAS_OK;  // k_small_pcg prolongs in the same kernel
+  if (c->path == RAS_PCG_RESIDENT && R.lp < 0) return RAS_OK;  // so does k_resident_pcg
   KL(s, K_PROL, R.ntiles, kNT_STREAM, k_prolong, R.tile_base, tiles_next(c), (const int32_t*)c->d_own_slot, (const double*)c->d_d,
      c->d_x, c->S, C);
   return RAS_OK;
@@ -956,8 +1090,8 @@ ras_status ras_setup(ras_ctx** out, const ras_csr* A, const double* b, const ras
   ras_options_default(&c->opt);
   if (opt) c->opt = *opt;
   if (c->opt.inner_iters < 1) c->opt.inner_iters = 1;
-  c->fuse_p = c->opt.reserved_i[0] != 0;
-  c->stage = c->opt.reserved_i[2] != 0;
+  c->fuse_p = c->opt.fuse_p != 0;
+  c->stage = c->opt.stage_p != 0;
   if (c->opt.inner_tol < 0) {
     set_tls_error("inner_tol must be >= 0");
     delete c;
@@ -1036,6 +1170,7 @@ static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   c->st.num_subdomains = c->plan->P;
   c->st.world = c->world;
   c->st.local_subdomains = c->nl;
+  c->st.pcg_path = c->ic ? RAS_PCG_TILED : c->small ? RAS_PCG_BLOCK : mode == RAS_SYNC ? c->path : RAS_PCG_TILED;
   c->st.rows_local = c->plan->rows_local;
   c->st.halo_values = c->n_halo;
   c->st.kernel_launches = c->launches;
@@ -1108,11 +1243,12 @@ ras_status ras_kernel_timing(ras_ctx* c, int32_t enable) {
 
 ras_status ras_kernel_times(const ras_ctx* c, ras_kernel_time_t* out, int32_t max_entries, int32_t* n_out) {
   if (!c || !n_out) return RAS_EINVAL;
-  static const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", c->ic ? "k_update_dot<ic>" : "k_update_dot",
-                                        c->ic ? "k_pupdate_z" : "k_pupdate", "k_prolong", "k_pack", "control",
-                                        "k_trsv", "k_zdot"};
-  const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate, c->mb.prolong,
-                                  c->mb.pack,     0.0,            c->mb.trsv,       c->mb.zdot};
+  const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", c->ic ? "k_update_dot<ic>" : "k_update_dot",
+                                 c->ic ? "k_pupdate_z" : "k_pupdate", "k_prolong", "k_pack", "control",
+                                 "k_trsv", "k_zdot", "k_small_pcg", "k_resident_pcg"};
+  const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate,
+                                  c->mb.prolong,  c->mb.pack,     0.0,              c->mb.trsv,
+                                  c->mb.zdot,     c->mb.local_solve, c->mb.local_solve};
   int n = 0;
   for (int k = 0; k < K_NKINDS && n < max_entries; ++k) {
     if (!out) break;

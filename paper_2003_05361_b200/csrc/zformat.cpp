@@ -64,9 +64,12 @@ int padded_width(const std::vector<int64_t>& sptr) {
 }
 
 // plain SELL-32 (sptr, col, val) -> packed Z arrays; false if a value does not fit the table
+// self_pad: the padding column of an empty slice is the lane's own row (the
+// local matrix, whose columns are row-space rows) instead of 0, so every column
+// of the local matrix lies in its subdomain's rows.
 bool pack(const std::vector<int64_t>& sptr, const std::vector<int32_t>& col, const std::vector<double>& val, int Wp,
           Coder& C, std::vector<uint8_t>& code, std::vector<int32_t>& kbase, std::vector<uint16_t>& d16,
-          std::vector<int32_t>& wide) {
+          std::vector<int32_t>& wide, bool self_pad) {
   const int64_t nsl = (int64_t)sptr.size() - 1;
   code.assign((size_t)nsl * 32 * Wp, 0);
   d16.assign((size_t)nsl * 32 * Wp, 0);
@@ -85,8 +88,8 @@ bool pack(const std::vector<int64_t>& sptr, const std::vector<int32_t>& col, con
           if (!C.enc(val[e], &code[z])) return false;
           cg[l] = col[e];
         } else {
-          code[z] = zero;  // padding: value 0 at a valid column (the lane's first entry, or 0)
-          cg[l] = w > 0 ? col[sptr[s] + l] : 0;
+          code[z] = zero;  // padding: value 0 at a valid column (the lane's first entry, or 0 / own row)
+          cg[l] = w > 0 ? col[sptr[s] + l] : self_pad ? (int32_t)(s * 32 + l) : 0;
         }
       }
       const int32_t lo = *std::min_element(cg.begin(), cg.end());
@@ -113,8 +116,8 @@ bool build_zformat(ras_plan* pl) {
   std::vector<uint8_t> rc, lc, dc(pl->diag.size());
   std::vector<int32_t> rkb, lkb, rw, lw;
   std::vector<uint16_t> rd, ld;
-  if (!pack(pl->R_sptr, pl->R_col, pl->R_val, wR, C, rc, rkb, rd, rw)) return false;
-  if (!pack(pl->L_sptr, pl->L_col, pl->L_val, wL, C, lc, lkb, ld, lw)) return false;
+  if (!pack(pl->R_sptr, pl->R_col, pl->R_val, wR, C, rc, rkb, rd, rw, false)) return false;
+  if (!pack(pl->L_sptr, pl->L_col, pl->L_val, wL, C, lc, lkb, ld, lw, true)) return false;
   for (size_t i = 0; i < dc.size(); ++i)
     if (!C.enc(pl->diag[i], &dc[i])) return false;
   // worth it only if the wide groups stay rare

@@ -58,7 +58,7 @@ def test_solve_device_owned_order_and_kernel_timing():
     import torch
 
     A, b, owner, gamma, m = setup()
-    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m))
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, path="tiled"))
     gids = s.owned_gids()
     assert sorted(gids.tolist()) == list(range(A.n))
     x = torch.zeros(len(gids), dtype=torch.float64, device="cuda")
@@ -69,11 +69,25 @@ def test_solve_device_owned_order_and_kernel_timing():
     st2, xh = s.solve(1e-300, 5, "sync")
     assert np.array_equal(x.cpu().numpy(), xh[gids])  # deterministic: bitwise reproducible
     assert kt["k_spmv_dot"][0] == 5 * m and kt["k_spmv_dot"][1] > 0  # the check-only sweep 5 launches no PCG
+    assert kt["k_small_pcg"][0] == 0 and kt["k_resident_pcg"][0] == 0
     # start from a device x0 = the 5-sweep result: 5 more sweeps = 10 sweeps from zero
     y = torch.zeros_like(x)
     s.solve_device(1e-300, 5, "sync", x.data_ptr(), y.data_ptr())
     _, x10 = s.solve(1e-300, 10, "sync")
     assert rel(y.cpu().numpy(), x10[gids]) <= 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("path", ["block", "resident"])
+def test_whole_solve_kernels_are_timed(path):
+    A, b, owner, gamma, m = setup()
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, path=path))
+    s.kernel_timing(True)
+    s.solve(1e-300, 4, "sync")
+    kt = s.kernel_times()
+    name = "k_small_pcg" if path == "block" else "k_resident_pcg"
+    assert kt[name][0] == 4 and kt[name][1] > 0 and kt["k_spmv_dot"][0] == 0 and kt["k_prolong"][0] == 0
+    assert s.stats()["pcg_path"] == getattr(R._ffi, "RAS_PCG_" + path.upper())
     s.close()
 
 

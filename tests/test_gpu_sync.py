@@ -25,7 +25,8 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-@pytest.mark.parametrize("fmt", ["plain", "z", "fuse_p", "stage", "z_stage", "tiled", "plain_tiled"])
+@pytest.mark.parametrize("fmt", ["plain", "z", "fuse_p", "stage", "z_stage", "tiled", "plain_tiled", "resident",
+                                 "plain_resident"])
 @pytest.mark.parametrize("case", ["c1", "voronoi_ragged", "strips"])
 def test_sync_iterates_match_oracle(case, fmt):
     if case == "c1":
@@ -46,12 +47,15 @@ def test_sync_iterates_match_oracle(case, fmt):
     b = ri.rhs(nx * ny, 0)
     K = 6
     ref = oracle_iterates(A, b, owner, gamma, "jacobi", m, K)
+    path = "resident" if fmt.endswith("resident") else "tiled" if fmt.endswith("tiled") or "stage" in fmt else "auto"
     s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, fuse_p=fmt == "fuse_p", plain=fmt.startswith("plain") or fmt == "stage",
-                                              stage=fmt.endswith("stage"), tiled=fmt.endswith("tiled") or "stage" in fmt))
+                                              stage=fmt.endswith("stage"), path=path))
     for k in (1, 2, K):
         st, x = s.solve(1e-300, k, "sync")
         assert st == R._ffi.RAS_ENOCONV
         assert s.stats()["sweeps"] == k
+        if path != "auto":
+            assert s.stats()["pcg_path"] == getattr(R._ffi, "RAS_PCG_" + path.upper())
         assert rel(x, ref.iterates[k]) <= 1e-10, (case, k, rel(x, ref.iterates[k]))
     s.close()
 
@@ -79,8 +83,8 @@ def test_sync_converges_to_tolerance_and_matches_oracle_solution():
     s.close()
 
 
-@pytest.mark.parametrize("tiled", [False, True])
-def test_exact_mode_c1_sweeps_and_solution(tiled):
+@pytest.mark.parametrize("path", ["auto", "tiled", "resident"])
+def test_exact_mode_c1_sweeps_and_solution(path):
     # C1: 64x64, 2x2, overlap 2, "exact" local solve (PCG to 1e-14, R6): 106 sweeps (oracle)
     N = 64
     A = ri.laplace_2d(N)
@@ -91,7 +95,7 @@ def test_exact_mode_c1_sweeps_and_solution(tiled):
         O.make_local_solver(sb, "exact")
     ref = O.ras_sync(A, b, subs, 1e-8, 1000, record_iterates=True)
     assert ref.sweeps == 106
-    s = R.Solver(A, b, owner, 2, R.options("exact", tiled=tiled))
+    s = R.Solver(A, b, owner, 2, R.options("exact", path=path))
     for k in (1, 5):
         st, x = s.solve(1e-300, k, "sync")
         assert rel(x, ref.iterates[k]) <= 1e-10
@@ -100,6 +104,36 @@ def test_exact_mode_c1_sweeps_and_solution(tiled):
     assert s.stats()["sweeps"] == 106
     assert rel(x, ref.x) <= 1e-10
     s.close()
+
+
+@pytest.mark.parametrize("plain", [False, True])
+def test_resident_path_is_auto_for_medium_subdomains(plain):
+    # 2x2 subdomains of ~134^2 rows (> the one-CTA limit of 9216): AUTO picks the
+    # grid-resident kernel (one group of all SMs per subdomain, ragged last chunk)
+    nx, ny = 262, 250
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 2)
+    owner = R.partition_regular(nx, ny, 1, 2, 2, 1)
+    ref = oracle_iterates(A, b, owner, 4, "jacobi", 12, 3)
+    s = R.Solver(A, b, owner, 4, R.options("jacobi", 12, plain=plain))
+    for k in (1, 3):
+        st, x = s.solve(1e-300, k, "sync")
+        assert s.stats()["pcg_path"] == R._ffi.RAS_PCG_RESIDENT
+        assert s.stats()["inner_iters_total"] == 12 * 4 * k
+        assert rel(x, ref.iterates[k]) <= 1e-10, (k, rel(x, ref.iterates[k]))
+    s.close()
+
+
+def test_forced_paths_that_do_not_apply_are_errors():
+    N = 40
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N)
+    owner = R.partition_regular(N, N, 1, 2, 2, 1)
+    with pytest.raises(R.RasError, match="pcg_path"):
+        R.Solver(A, b, owner, 1, R.options("ic0", 5, path="resident"))
+    big = ri.laplace_2d(200)
+    with pytest.raises(R.RasError, match="BLOCK"):
+        R.Solver(big, ri.rhs(200 * 200), np.zeros(200 * 200, np.int32), 0, R.options("jacobi", 5, path="block"))
 
 
 def test_edge_cases():

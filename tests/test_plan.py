@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert {n for n, _, _ in R._ffi.SIGNATURES} == names
-    assert lib.ras_abi_version() == 1
+    assert lib.ras_abi_version() == R._ffi.ABI_VERSION == 2
 
 
 @pytest.mark.parametrize("dims,parts", [((10, 1, 1), (3, 1, 1)), ((64, 64, 1), (2, 2, 1)), ((17, 9, 1), (4, 3, 1)),
