@@ -792,59 +792,90 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
 }
 
 // ---------------------------------------------------------------------------
-// Grid-resident regime (subdomains of up to ~1.4M rows, e.g. C2's 1024^2 tiles
+// Grid-resident regime (subdomains of up to ~1.2M rows, e.g. C2's 1024^2 tiles
 // + overlap): a persistent cooperative grid, one CTA per SM, split into groups
 // of gs CTAs; a group runs the WHOLE Jacobi-PCG local solve of one subdomain
 // (then the next one: subdomains lp_base + g, + ngroups, ...) with its rows
 // partitioned into contiguous chunks, one per CTA, resident on chip for all m
-// iterations: p, r and the diagonal in shared memory, q and d in registers.
+// iterations: p, r, d and the diagonal codes in shared memory, q in registers.
 // HBM is touched once per sweep (r, p in; x[S_p] out; the matrix streams from
-// L2/L1), instead of three passes per iteration.
+// L2), instead of three passes per iteration.
 //
-// Reductions: two group-wide sums per iteration.  No atomics: every CTA
-// release-stores its partial into its own slot of a 3-deep ring (slot of
-// barrier k+1 reset to a sentinel before the store of barrier k), and warp 0 of
-// every CTA polls the group's slots until none holds the sentinel, then sums
-// them in fixed order -- bitwise-identical alpha / beta / stop decisions in all
-// CTAs.  The ring is safe because a CTA stores for barrier k only after every
-// CTA has finished reading the slots of barrier k-2 (it passed barrier k-1).
+// One group-wide reduction per iteration.  PCG's second dot product is taken
+// from quantities known before the update (Jacobi, z = D^-1 r):
+//   rho' = (r - a q, D^-1 (r - a q)) = rho - 2a (z, q) + a^2 (q, D^-1 q)
+//   |r'|^2 = |r|^2 - 2a (r, q) + a^2 (q, q)        (inner tolerance only)
+// so sigma = (p, q), (z, q), (q, D^-1 q) [, (r, q), (q, q)] are reduced
+// together after the SpMV; the expansion has no cancellation beyond the
+// per-iteration ratio rho'/rho (R28).  Same alpha / beta / stop rules
+// as the tiled path (R7, R6).
 //
-// Halo: a row's neighbours owned by another CTA of the group are read from L2.
-// The p update of iteration it-1 is fused into the SpMV of iteration it: each
-// CTA publishes, for its export band only (rows other CTAs reference, host-
-// computed), z = D^-1 r (pass 2) and p (pass 3) of every iteration; a reader
-// recomputes p_it(c) = fma(beta, p_{it-1}(c), z(c)) with the same expression
-// the owner uses, so only the two reductions synchronise CTAs.  p_it lives in
-// pbuf[(it-1) & 1] (pbuf[0] = the p written by k_residual, all rows).
+// Reductions: no atomics: every CTA stores its partials (after one release
+// fence) into its own 32-byte sector of a 3-deep slot ring (the sector of
+// reduction k+1 reset to a sentinel before the stores of reduction k), and warp
+// 0 of every CTA polls the group's slots with relaxed loads until none holds
+// the sentinel, fences once (acquire), then sums them in fixed order -- bitwise-identical
+// alpha / beta / stop decisions in all CTAs.  The ring is safe because a CTA
+// stores for reduction k only after every CTA finished reading the slots of
+// reduction k-2 (it passed reduction k-1).
+//
+// Halo: the columns of a chunk's rows lie in [-glo, nr + ghi) (host-computed
+// ghost zones; only export-band rows reach outside [0, nr): A_p is symmetric).
+// At the start of every pass A the ghost rows of p are staged next to the
+// chunk's own p in shared memory, so the SpMV gathers from shared memory only.
+// A ghost value is recomputed by the reader from values the owner published
+// for its export band before the reduction:
+//   p_it(c) = fma(beta, p_{it-1}(c), D^-1(c) * fma(-alpha, q_{it-1}(c), r_{it-2}(c)))
+// -- the owner's own expression -- so no CTA waits for its neighbours' update.
+// Published arrays (export rows only, double-buffered by iteration parity):
+// p_it in pub_p[it & 1] (pub_p[1] = k_residual's p = p_1, all rows), r_it in
+// pub_r[it & 1] (pub_r[0] = k_residual's r = r_0, all rows), q_it in pub_q[it & 1].
 // ---------------------------------------------------------------------------
 #ifndef RAS_NT_RESID
-#define RAS_NT_RESID 1024
+#define RAS_NT_RESID 768
 #endif
 #ifndef RAS_PD_RESID
 #define RAS_PD_RESID 1
 #endif
 constexpr int kNT_RESID = RAS_NT_RESID;
-constexpr int kResidMaxRPT = kNT_RESID >= 1024 ? 8 : 16;  // rows per thread: q in registers (2 * RPT registers)
+constexpr int kResidMaxRPT = kNT_RESID >= 1024 ? 8 : kNT_RESID >= 768 ? 12 : 16;  // rows per thread: q in registers (2 * RPT registers)
 constexpr unsigned long long kSlotEmpty = 0xffffffffffffffffull;  // NaN pattern never stored (see group_allsum)
 constexpr int kMaxGroupCTAs = 160;  // >= SMs of a B200 (148): CTAs of one group
+constexpr int kResidNV = 4;         // slot sector per CTA: up to 4 values per reduction (3 used)
+
+#ifdef RAS_RESID_TRACE
+// timing experiment: per CTA, per iteration of the first traced subdomain:
+// globaltimer at pass-A start, before the reduction, after it, after pass B
+__device__ unsigned long long g_resid_trace[160][64][4];
+__device__ unsigned long long g_red_trace[160][64][4];  // per CTA, per reduction: arrive, stored, polled, released
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RAS_TRACE(slot)                                                                   \
+  __syncthreads();                                                                         \
+  if (threadIdx.x == 0 && lp == lp_base + 1 && it <= 64) g_resid_trace[blockIdx.x][it - 1][slot] = gtimer();
+#else
+#define RAS_TRACE(slot)
+#endif
 
 struct ResidentCtl {
-  const int2* band;           // per (local subdomain, CTA of group): chunk-relative export band
-                              // {lo_end, hi_begin}: rows i < lo_end or i >= hi_begin are read by others
-  unsigned long long* slots;  // per group [3 ring][2 values][gs] partial sums, kSlotEmpty before launch
-  double* pbuf0;              // p_1 (k_residual output) / odd iterations' p, export rows
-  double* pbuf1;              // even iterations' p, export rows
-  double* zg;                 // z of the export rows
+  const int4* band;           // per (local subdomain, CTA of group), chunk-relative:
+                              // {lo_end, hi_begin, glo, ghi}: rows i < lo_end or i >= hi_begin are read
+                              // by other CTAs (export band); the chunk's rows reference columns in
+                              // [-glo, nr + ghi) (ghost zones, staged in shared memory every iteration)
+  unsigned long long* slots;  // per group [3 ring][gs][kResidNV] partial sums, kSlotEmpty before launch
+  double* pub_p[2];           // [1] = k_residual's p (p_1)
+  double* pub_r[2];           // [0] = k_residual's r (r_0)
+  double* pub_q[2];
   int32_t ngroups, gs;
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
-}
-__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -863,9 +894,16 @@ __device__ __forceinline__ double warp_allsum(double v) {
 // published by the release store (ordered after them by the CTA barrier);
 // readers poll with acquire loads, and the CTA barrier after the poll orders
 // every thread's later halo loads after them.  seq = reductions completed.
+#ifdef RAS_RESID_TRACE
+#define RAS_RTR(k) \
+  if (threadIdx.x == 0 && seq < 64) g_red_trace[blockIdx.x][seq][k] = gtimer();
+#else
+#define RAS_RTR(k)
+#endif
 template <int NV>
 __device__ __forceinline__ void group_allsum(double (&v)[NV], double (*red)[kNT_RESID / 32], double* bc,
                                              unsigned long long* slots, int gs, int c, unsigned& seq) {
+  static_assert(NV <= kResidNV, "slot ring holds kResidNV values per CTA");
   constexpr int NW = kNT_RESID / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -874,56 +912,65 @@ __device__ __forceinline__ void group_allsum(double (&v)[NV], double (*red)[kNT_
     if (lane == 0) red[j][w] = s;
   }
   __syncthreads();
+  RAS_RTR(0)
   if (w == 0) {
-    const unsigned ring = seq % 3, nxt = (seq + 1) % 3;
+    // slots: [3 ring][gs CTAs][4] -- a CTA's values share one 32-byte sector
+    unsigned long long* const ring = slots + (size_t)(seq % 3) * gs * 4;
+    unsigned long long* const nxt = slots + (size_t)((seq + 1) % 3) * gs * 4;
     double s[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) s[j] = warp_sum(lane < NW ? red[j][lane] : 0.0);
     if (lane == 0) {
 #pragma unroll
-      for (int j = 0; j < NV; ++j) st_relaxed_gpu_u64(&slots[(nxt * 2 + j) * gs + c], kSlotEmpty);
+      for (int j = 0; j < NV; ++j) st_relaxed_gpu_u64(&nxt[c * 4 + j], kSlotEmpty);
+      // release: one fence orders the CTA's earlier stores (export band, ordered
+      // before this thread by the CTA barrier) before the value stores
+#ifndef RAS_EXP_NOWFENCE  // timing experiment only (unsafe ordering)
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         unsigned long long u = (unsigned long long)__double_as_longlong(s[j]);
         if (u == kSlotEmpty) u = 0x7ff8000000000000ull;  // a NaN partial stays a NaN, never the sentinel
-        st_release_gpu_u64(&slots[(ring * 2 + j) * gs + c], u);
+        st_relaxed_gpu_u64(&ring[c * 4 + j], u);
       }
     }
-    // poll: each lane owns slots lane, lane + 32, ... (<= kMaxSlotsPerLane) and
-    // re-loads only the ones still empty, all in flight together
+    RAS_RTR(1)
+    // poll: each lane owns CTAs lane, lane + 32, ... and re-loads only the values
+    // still empty, all in flight together (relaxed loads; one acquire fence after)
     constexpr int KS = (kMaxGroupCTAs + 31) / 32;
-    unsigned long long u[NV][KS];
+    unsigned long long u[KS][NV];
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
+    for (int t = 0; t < KS; ++t)
 #pragma unroll
-      for (int t = 0; t < KS; ++t) u[j][t] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
+      for (int j = 0; j < NV; ++j) u[t][j] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
     for (;;) {
       bool done = true;
 #pragma unroll
-      for (int j = 0; j < NV; ++j)
+      for (int t = 0; t < KS; ++t)
 #pragma unroll
-        for (int t = 0; t < KS; ++t)
-          if (u[j][t] == kSlotEmpty) u[j][t] = ld_acquire_gpu_u64(&slots[(ring * 2 + j) * gs + lane + 32 * t]);
+        for (int j = 0; j < NV; ++j)
+          if (u[t][j] == kSlotEmpty) u[t][j] = ld_relaxed_gpu_u64(&ring[(lane + 32 * t) * 4 + j]);
 #pragma unroll
-      for (int j = 0; j < NV; ++j)
+      for (int t = 0; t < KS; ++t)
 #pragma unroll
-        for (int t = 0; t < KS; ++t) done = done && u[j][t] != kSlotEmpty;
+        for (int j = 0; j < NV; ++j) done = done && u[t][j] != kSlotEmpty;
       if (__all_sync(0xffffffffu, done)) break;
     }
+    RAS_RTR(2)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the peers' export-band stores
     double acc[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       acc[j] = 0.0;
 #pragma unroll
-      for (int t = 0; t < KS; ++t) acc[j] += __longlong_as_double((long long)u[j][t]);  // lane + 32t order
-    }
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
+      for (int t = 0; t < KS; ++t) acc[j] += __longlong_as_double((long long)u[t][j]);  // CTA lane + 32t order
       acc[j] = warp_allsum(acc[j]);
       if (lane == 0) bc[j] = acc[j];
     }
   }
   __syncthreads();
+  RAS_RTR(3)
 #pragma unroll
   for (int j = 0; j < NV; ++j) v[j] = bc[j];
   ++seq;
@@ -989,6 +1036,14 @@ __device__ __forceinline__ double resident_row(const Sell& L, int64_t row, const
   return acc;
 }
 
+// Row-slot order of pass A: 0, RPT-1, 1, RPT-2, ... -- the export bands sit at
+// both ends of a chunk, so their published q stores are issued first and have
+// completed by the time the reduction's release fence waits for them.
+template <int RPT>
+__device__ __forceinline__ constexpr int band_first(int jo) {
+  return (jo & 1) ? RPT - 1 - (jo >> 1) : (jo >> 1);
+}
+
 // Runs after k_residual<JAC>/k_finish<F_RES_JAC> (r, p = z, rho, rt2, active set).
 // Launched cooperatively with grid = ngroups * gs CTAs (all co-resident).
 // Dynamic shared memory per chunk row: p, r, d (FP64) + the diagonal (Z: uint8
@@ -996,20 +1051,19 @@ __device__ __forceinline__ double resident_row(const Sell& L, int64_t row, const
 // plain: FP64); q lives in registers.  Rows of the export band are the only
 // ones with off-chunk columns (A_p is symmetric), so every other row gathers p
 // from shared memory without range checks.
-template <int RPT, int W, bool Z>
+template <int RPT, int W, bool Z, bool TOL>
 static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_base, int nsub, SmallSubs SS,
                                                                       ResidentCtl RC, Sell L, Diag D,
-                                                                      const double* __restrict__ r_in,
                                                                       const int32_t* __restrict__ own_slot,
                                                                       double* __restrict__ x, Scal S, Ctl C,
                                                                       int32_t m, double inner_tol, int32_t chunk_max,
-                                                                      int32_t ntable) {
+                                                                      int32_t glo_max, int32_t ghi_max, int32_t ntable) {
   constexpr int NT = kNT_RESID;
   extern __shared__ double smem[];
-  __shared__ double red[2][NT / 32];
-  __shared__ double bc[2];
-  double* sp = smem;                  // p of the chunk
-  double* sr = sp + chunk_max;        // r
+  __shared__ double red[kResidNV][NT / 32];
+  __shared__ double bc[kResidNV];
+  double* sp = smem + glo_max;                  // p of the chunk, ghost zones at [-glo, 0) and [nr, nr + ghi)
+  double* sr = smem + glo_max + chunk_max + ghi_max;  // r
   double* sd = sr + chunk_max;        // d (the correction)
   double* stab = sd + chunk_max;      // Z: dictionary values [256]
   double* sinv = stab + 256;          // Z: __drcp_rn of every dictionary value [256]
@@ -1017,8 +1071,13 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
   double* sdg = stab;                 // plain: diagonal of the chunk
   const int gs = RC.gs;
   const int g = blockIdx.x / gs, c = blockIdx.x - g * gs;
-  unsigned long long* slots = RC.slots + (size_t)6 * gs * g;
+  unsigned long long* slots = RC.slots + (size_t)3 * kResidNV * gs * g;
   unsigned seq = 0;
+  // !TOL (fixed m): one reduction of sigma, (z, q), (q, D^-1 q) per iteration.
+  // TOL (exact mode / eta): the standard two reductions, sigma then the direct
+  // rho' = (r', z'), |r'|^2 -- the expansion above is not used to iterate down
+  // to 1e-14 (its rounding drift is not self-correcting).
+  constexpr int NV = TOL ? 1 : 3;
   if (Z)
     for (int i = threadIdx.x; i < ntable; i += NT) {
       const double v = __ldg(&D.table[i]);
@@ -1030,43 +1089,71 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
     const int r0 = SS.row_off[lp], n = SS.nrows[lp];
     const int chunk = ((n / 32 + gs - 1) / gs) * 32;
     const int a = min(n, c * chunk), nr = min(n, a + chunk) - a;
-    const int2 band = RC.band[lp * gs + c];
+    const int4 band = RC.band[lp * gs + c];
     // chunk row i is row-space row rb + i (rb is a multiple of 32: slice aligned);
     // every array below is re-based to the chunk so indices stay 32-bit
     const int32_t rb = r0 + a;
-    double* const zg = RC.zg + rb;
-    const double* const pb0 = RC.pbuf0 + rb;
+    // published arrays re-based to the chunk (recomputed where used: registers are scarce)
+#define RAS_PUB(arr, par) (((par) ? RC.arr[1] : RC.arr[0]) + rb)  // select, not index: no local-memory copy
+    const uint8_t* const dcode = D.code + rb;
+    const double* const dval = D.v + rb;
     __syncthreads();
     for (int i = threadIdx.x; i < nr; i += NT) {
-      sp[i] = __ldcg(&pb0[i]);
-      sr[i] = __ldcg(&r_in[rb + i]);
+      sp[i] = __ldcg(&RAS_PUB(pub_p, 1)[i]);  // p_1 = z_0
+      sr[i] = __ldcg(&RAS_PUB(pub_r, 0)[i]);  // r_0
       if (Z)
-        sdc[i] = __ldg(&D.code[rb + i]);
+        sdc[i] = __ldg(&dcode[i]);
       else
-        sdg[i] = __ldg(&D.v[rb + i]);
+        sdg[i] = __ldg(&dval[i]);
     }
     double q[RPT];
     double rho = S.rho[lp];
     const double rt2 = S.rt2[lp];
-    double beta = 0.0;
+    double alpha = 0.0, beta = 0.0;
     int its = 0;
     __syncthreads();
     auto diag = [&](int i) -> double { return Z ? stab[sdc[i]] : sdg[i]; };
-    auto dinv_r = [&](int i, double r) -> double {  // z = D^-1 r, bitwise as __drcp_rn(diag) * r
-      return __dmul_rn(Z ? sinv[sdc[i]] : __drcp_rn(sdg[i]), r);
-    };
+    auto dinv = [&](int i) -> double { return Z ? sinv[sdc[i]] : __drcp_rn(sdg[i]); };
     for (;;) {
-      // pass 1 (+ the fused pass 3 of the previous iteration for halo columns):
-      // q = A_p p_it, sigma = p_it . q.  li = chunk-relative column.
-      const double* const pold = ((its & 1) ? RC.pbuf0 : RC.pbuf1) + rb;  // p_{it-1} = pbuf[(it-2) & 1]
-      const bool first = its == 0;
-      const double bt = beta;
-      auto Pb = [&](int li) -> double {  // row of the export band: the column may be another CTA's
-        if ((unsigned)li < (unsigned)nr) return sp[li];
-        if (first) return __ldcg(&pb0[li]);
-        return __fma_rn(bt, __ldcg(&pold[li]), __ldcg(&zg[li]));
+      const int it = its + 1;
+      RAS_TRACE(0)
+      // pass A: q = A_p p_it (halo columns recomputed, see above), then the
+      // partials sigma = (p, q), (z, q), (q, D^-1 q) [, (r, q), (q, q)]
+      {
+        // stage the ghost zones of p_it: [-glo, 0) and [nr, nr + ghi)
+        const int ng = band.z + band.w;
+        for (int t = threadIdx.x; t < ng; t += NT) {
+          const int li = t < band.z ? t - band.z : nr + (t - band.z);
+          double pv;
+          if (it == 1) {
+            pv = __ldcg(&RAS_PUB(pub_p, 1)[li]);
+          } else {
+            // p_{it-1}, q_{it-1}, r_{it-2}: the owner's own expression
+            const double di = Z ? sinv[__ldg(&dcode[li])] : __drcp_rn(__ldg(&dval[li]));
+            const double zc = __dmul_rn(
+                di, __fma_rn(-alpha, __ldcg(&RAS_PUB(pub_q, (it - 1) & 1)[li]), __ldcg(&RAS_PUB(pub_r, it & 1)[li])));
+            pv = __fma_rn(beta, __ldcg(&RAS_PUB(pub_p, (it - 1) & 1)[li]), zc);
+          }
+          sp[li] = pv;
+        }
+        __syncthreads();
+      }
+      double v[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[k] = 0.0;
+      auto accum = [&](int j, int i, double pi, double off) {
+        const double qi = __fma_rn(diag(i), pi, off);
+        q[j] = qi;
+        const double di = dinv(i);
+        const double zi = __dmul_rn(di, sr[i]);
+        const double dq = __dmul_rn(di, qi);
+        v[0] += pi * qi;
+        if (!TOL) {
+          v[NV - 2] += zi * qi;
+          v[NV - 1] += qi * dq;
+        }
+        if (i < band.x || i >= band.y) __stcg(&RAS_PUB(pub_q, it & 1)[i], qi);
       };
-      double v1 = 0.0;
       if (Z) {
         // SELL-Z rows software-pipelined: the codes / offsets / slice bases of
         // row j + PD are in flight while row j is computed (L2 latency hiding)
@@ -1101,14 +1188,14 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
           }
         };
 #pragma unroll
-        for (int j = 0; j < PD; ++j) zload(j, j);
+        for (int j = 0; j < PD; ++j) zload(band_first<RPT>(j), j);
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) {
+        for (int jo = 0; jo < RPT; ++jo) {
+          const int j = band_first<RPT>(jo);
           const int i = j * NT + threadIdx.x;
-          const int bi = j % PD;
+          const int bi = jo % PD;
           if (i < nr) {
             const double pi = sp[i];
-            const bool inner = i >= band.x && i < band.y;
             // a slice with a wide group (base < 0: int32 columns) takes the generic decoder
             bool wide = false;
 #pragma unroll
@@ -1119,71 +1206,100 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
               for (int k = 0; k < W; ++k) {
                 const uint32_t code = (bcw[bi][k / 4] >> (8 * (k % 4))) & 0xffu;
                 const int li = bkb[bi][k] - rb + (int)((bdw[bi][k / 2] >> (16 * (k % 2))) & 0xffffu);
-                off += stab[code] * (inner ? sp[li] : Pb(li));
+                off += stab[code] * sp[li];
               }
             } else {
-              off = resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return Pb(col - rb); });
+              off = resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return sp[col - rb]; });
             }
-            q[j] = diag(i) * pi + off;
-            v1 += pi * q[j];
+            accum(j, i, pi, off);
           }
-          if (j + PD < RPT) zload(j + PD, bi);
+          if (jo + PD < RPT) zload(band_first<RPT>(jo + PD), bi);
         }
       } else {
+#pragma unroll
+        for (int jo = 0; jo < RPT; ++jo) {
+          const int j = band_first<RPT>(jo);
+          const int i = j * NT + threadIdx.x;
+          if (i < nr) {
+            const double pi = sp[i];
+            const double off = resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return sp[col - rb]; });
+            accum(j, i, pi, off);
+          }
+        }
+      }
+      RAS_TRACE(1)
+      group_allsum<NV>(v, red, bc, slots, gs, c, seq);
+      RAS_TRACE(2)
+      const double sigma = v[0];
+      if (sigma == 0.0) break;  // R7
+      alpha = rho / sigma;
+      its = it;
+      bool stop;
+      if (!TOL) {
+        const double rho_new = rho - 2.0 * alpha * v[NV - 2] + alpha * alpha * v[NV - 1];
+        stop = its >= m || !(rho_new > 0.0);  // R7 (rho' <= 0 only by rounding: breakdown)
+        beta = rho_new / rho;
+        rho = rho_new;
+        // pass B (own rows): d += alpha p, r -= alpha q, and unless stopping
+        // p_{it+1} = D^-1 r + beta p; publish r_it, p_{it+1} of the export band
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
           const int i = j * NT + threadIdx.x;
           if (i < nr) {
             const double pi = sp[i];
-            const double off = (i >= band.x && i < band.y)
-                                   ? resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return sp[col - rb]; })
-                                   : resident_row<W, Z>(L, (int64_t)rb + i, stab, [&](int32_t col) { return Pb(col - rb); });
-            q[j] = diag(i) * pi + off;
-            v1 += pi * q[j];
+            sd[i] = it == 1 ? alpha * pi : __fma_rn(alpha, pi, sd[i]);
+            if (!stop) {
+              const double rn = __fma_rn(-alpha, q[j], sr[i]);
+              sr[i] = rn;
+              const double pn = __fma_rn(beta, pi, __dmul_rn(dinv(i), rn));
+              sp[i] = pn;
+              if (i < band.x || i >= band.y) {
+                __stcg(&RAS_PUB(pub_r, it & 1)[i], rn);
+                __stcg(&RAS_PUB(pub_p, (it + 1) & 1)[i], pn);
+              }
+            }
+          }
+        }
+      } else {
+        // pass B1: d += alpha p, r -= alpha q (published), z = D^-1 r; (r, z), (r, r)
+        double v2[2] = {0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const int i = j * NT + threadIdx.x;
+          if (i < nr) {
+            const double pi = sp[i];
+            sd[i] = it == 1 ? alpha * pi : __fma_rn(alpha, pi, sd[i]);
+            const double rn = __fma_rn(-alpha, q[j], sr[i]);
+            sr[i] = rn;
+            const double zi = __dmul_rn(dinv(i), rn);
+            v2[0] += rn * zi;
+            v2[1] += rn * rn;
+            if (i < band.x || i >= band.y) __stcg(&RAS_PUB(pub_r, it & 1)[i], rn);
+          }
+        }
+        group_allsum<2>(v2, red, bc, slots, gs, c, seq);
+        stop = its >= m || v2[0] == 0.0 || sqrt(v2[1]) <= inner_tol * sqrt(rt2);  // R7, R6
+        beta = v2[0] / rho;
+        rho = v2[0];
+        // pass B2: p_{it+1} = D^-1 r + beta p (published)
+        if (!stop) {
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            const int i = j * NT + threadIdx.x;
+            if (i < nr) {
+              const double pn = __fma_rn(beta, sp[i], __dmul_rn(dinv(i), sr[i]));
+              sp[i] = pn;
+              if (i < band.x || i >= band.y) __stcg(&RAS_PUB(pub_p, (it + 1) & 1)[i], pn);
+            }
           }
         }
       }
-      double s1[1] = {v1};
-      group_allsum<1>(s1, red, bc, slots, gs, c, seq);
-      const double sigma = s1[0];
-      if (sigma == 0.0) break;  // R7
-      const double alpha = rho / sigma;
-      ++its;
-      // pass 2: d += alpha p, r -= alpha q, z = D^-1 r (published for the export band); r.z, r.r
-      double v2[2] = {0.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int i = j * NT + threadIdx.x;
-        if (i < nr) {
-          const double pi = sp[i];
-          sd[i] = its == 1 ? alpha * pi : sd[i] + alpha * pi;
-          const double rn = sr[i] - alpha * q[j];
-          sr[i] = rn;
-          const double z = dinv_r(i, rn);
-          if (i < band.x || i >= band.y) __stcg(&zg[i], z);
-          v2[0] += rn * z;
-          v2[1] += rn * rn;
-        }
-      }
-      group_allsum<2>(v2, red, bc, slots, gs, c, seq);
-      if (inner_tol > 0.0 && sqrt(v2[1]) <= inner_tol * sqrt(rt2)) break;  // exact mode / eta
-      beta = v2[0] / rho;
-      rho = v2[0];
-      if (its >= m || rho == 0.0) break;
-      // pass 3 (own rows): p_{its+1} = z + beta p_its -> shared memory, export band -> pbuf[its & 1]
-      double* const pw = ((its & 1) ? RC.pbuf1 : RC.pbuf0) + rb;
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int i = j * NT + threadIdx.x;
-        if (i < nr) {
-          const double pn = __fma_rn(beta, sp[i], dinv_r(i, sr[i]));
-          sp[i] = pn;
-          if (i < band.x || i >= band.y) __stcg(&pw[i], pn);
-        }
-      }
+      RAS_TRACE(3)
+      if (stop) break;
       __syncthreads();
     }
     // a4: restricted prolongation of the chunk's owned rows
+    __syncthreads();
     if (its > 0) {
       for (int i = threadIdx.x; i < nr; i += NT) {
         const int32_t s = __ldg(&own_slot[rb + i]);
@@ -1195,6 +1311,7 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
       S.inner_total[lp] += its;
       S.active[lp] = 0;
     }
+#undef RAS_PUB
   }
 }
 

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -145,20 +147,29 @@ static void compute_model_bytes(ras_ctx* c) {
 // RESIDENT path setup (k_resident_pcg): group count / size, rows per thread,
 // export bands, barrier counters and partial-sum slots.  Leaves c->path alone
 // when no configuration fits (the caller falls back to TILED).
-static const void* resident_kernel(int rpt, bool z, int w) {
-#define RAS_RK(RPT)                                                                             \
-  if (z) return w == 4 ? (const void*)k_resident_pcg<RPT, 4, true> : (const void*)k_resident_pcg<RPT, 8, true>; \
-  return w <= 8 ? (const void*)k_resident_pcg<RPT, 8, false> : (const void*)k_resident_pcg<RPT, 0, false>;
+static const void* resident_kernel(int rpt, bool z, int w, bool tol) {
+#define RAS_RK2(RPT, W, Z) return tol ? (const void*)k_resident_pcg<RPT, W, Z, true> : (const void*)k_resident_pcg<RPT, W, Z, false>;
+#define RAS_RK(RPT)                     \
+  if (z) {                              \
+    if (w == 4) {                       \
+      RAS_RK2(RPT, 4, true)             \
+    } else {                            \
+      RAS_RK2(RPT, 8, true)             \
+    }                                   \
+  } else {                              \
+    RAS_RK2(RPT, 0, false)              \
+  }
   // only the rows-per-thread counts the register budget allows are instantiated
   if (rpt <= 4) {
     RAS_RK(4)
   } else if (rpt <= 8 || kResidMaxRPT == 8) {
     RAS_RK(8)
-  } else if (rpt <= 12) {
-    RAS_RK(kResidMaxRPT >= 12 ? 12 : 8)
+  } else if (rpt <= 10) {
+    RAS_RK(10)
   } else {
     RAS_RK(kResidMaxRPT)
   }
+#undef RAS_RK2
 #undef RAS_RK
 }
 
@@ -184,19 +195,15 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
   const int chunk = chunk_of(nmax, gs);
   if (chunk > cap) return RAS_OK;
   const int need = (chunk + kNT_RESID - 1) / kNT_RESID;
-  const int rpt = need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : 16;
-  const size_t smem = (size_t)24 * chunk + (c->z ? 4096 + (size_t)chunk : (size_t)8 * chunk);
-  const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL);
-  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_RESID, smem));
-  if (per_sm < 1) return RAS_OK;
-  // export bands: chunk rows other CTAs of the group read (Ap columns, subdomain-relative)
-  std::vector<int2> band((size_t)nl * gs);
+  const int rpt = need <= 4 ? 4 : need <= 8 ? 8 : need <= 10 ? 10 : kResidMaxRPT;
+  // export bands (chunk rows other CTAs of the group read) and ghost zones (the
+  // columns outside the chunk its rows read), from the CSR of A_p
+  std::vector<int4> band((size_t)nl * gs);
+  int glo_max = 0, ghi_max = 0;
   for (int lp = 0; lp < nl; ++lp) {
     const auto& S = pl->subs[lp];
     const int n = (int)S.nrows_pad, ch = chunk_of(n, gs);
-    std::vector<int> lo(gs, 0), hi(gs), len(gs);
+    std::vector<int> lo(gs, 0), hi(gs), len(gs), glo(gs, 0), ghi(gs, 0);
     for (int cc = 0; cc < gs; ++cc) {
       const int a = std::min(n, cc * ch);
       len[cc] = std::min(n, a + ch) - a;
@@ -212,14 +219,37 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
           lo[cj] = std::max(lo[cj], lj + 1);
         else
           hi[cj] = std::min(hi[cj], lj);
+        const int li = j - ci * ch;  // column relative to the reading chunk
+        if (li < 0)
+          glo[ci] = std::max(glo[ci], -li);
+        else
+          ghi[ci] = std::max(ghi[ci], li - len[ci] + 1);
       }
     }
-    for (int cc = 0; cc < gs; ++cc) band[(size_t)lp * gs + cc] = make_int2(lo[cc], hi[cc]);
+    for (int cc = 0; cc < gs; ++cc) {
+      band[(size_t)lp * gs + cc] = make_int4(lo[cc], hi[cc], glo[cc], ghi[cc]);
+      glo_max = std::max(glo_max, glo[cc]);
+      ghi_max = std::max(ghi_max, ghi[cc]);
+    }
   }
-  int2* dband;
+  const size_t smem = (size_t)8 * (glo_max + ghi_max) + (size_t)24 * chunk +
+                      (c->z ? 4096 + (size_t)chunk : (size_t)8 * chunk);
+  if (smem + 2048 > (size_t)smem_optin) return RAS_OK;  // ghost zones too wide: TILED
+  const bool tol = c->opt.local_solver == RAS_LS_EXACT_PCG || c->opt.inner_tol > 0.0;
+  const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol);
+  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_RESID, smem));
+  if (per_sm < 1) return RAS_OK;
+  int4* dband;
   TRY(upload(c, &dband, band));
-  TRY(zalloc(c, &c->d_resid_slots, (size_t)k * 6 * gs));
-  c->RC = ResidentCtl{dband, c->d_resid_slots, c->d_p, c->d_p2, c->d_q, k, gs};
+  c->resid_glo = glo_max;
+  c->resid_ghi = ghi_max;
+  TRY(zalloc(c, &c->d_resid_slots, (size_t)k * 3 * kResidNV * gs));
+  double* q2;
+  TRY(zalloc(c, &q2, (size_t)c->rows_pad));
+  // published export-band values (kernels.cuh): pub_p[1] = k_residual's p, pub_r[0] = its r
+  c->RC = ResidentCtl{dband, c->d_resid_slots, {c->d_p2, c->d_p}, {c->d_r, c->d_d}, {c->d_q, q2}, k, gs};
   c->resid_rpt = rpt;
   c->resid_chunk = chunk;
   c->resid_smem = smem;
@@ -743,16 +773,15 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
 // + prolongation (k_resident_pcg), batched (sync) solves only.
 static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m, double inner_tol) {
   // every reduction slot starts empty (kSlotEmpty = all ones)
-  RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff, (size_t)c->RC.ngroups * 6 * c->RC.gs * 8, s));
-  const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL);
+  RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff, (size_t)c->RC.ngroups * 3 * kResidNV * c->RC.gs * 8, s));
+  const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0);
   int lp0 = 0, nsub = c->nl;
-  const double* r_in = c->d_r;
   const int32_t* own = c->d_own_slot;
   double* x = c->d_x;
-  int32_t chunk_max = c->resid_chunk;
+  int32_t chunk_max = c->resid_chunk, glo = c->resid_glo, ghi = c->resid_ghi;
   int32_t ntable = c->z ? (int32_t)c->plan->z_table.size() : 0;
-  void* args[] = {&lp0,  &nsub, &c->SS, &c->RC, &c->L,      &c->D,      &r_in,  &own,
-                  &x,    &c->S, &C,     &m,     &inner_tol, &chunk_max, &ntable};
+  void* args[] = {&lp0, &nsub, &c->SS, &c->RC, &c->L,      &c->D,      &own, &x,  &c->S,
+                  &C,   &m,    &inner_tol,     &chunk_max, &glo,       &ghi, &ntable};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(c->RC.ngroups * c->RC.gs));
   cfg.blockDim = dim3(kNT_RESID);
@@ -766,6 +795,19 @@ static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m,
   const int ti = kt_begin(c, s);
   RAS_CUDA(c, cudaLaunchKernelExC(&cfg, fn, args));
   kt_end(c, s, K_RESID, ti);
+#ifdef RAS_RESID_TRACE
+  if (const char* f = getenv("RAS_TRACE_FILE")) {
+    static std::vector<unsigned long long> h(160 * 64 * 4);
+    RAS_CUDA(c, cudaStreamSynchronize(s));
+    RAS_CUDA(c, cudaMemcpyFromSymbol(h.data(), g_resid_trace, h.size() * 8));
+    if (FILE* fp = fopen(f, "wb")) {
+      fwrite(h.data(), 8, h.size(), fp);
+      RAS_CUDA(c, cudaMemcpyFromSymbol(h.data(), g_red_trace, h.size() * 8));
+      fwrite(h.data(), 8, h.size(), fp);
+      fclose(fp);
+    }
+  }
+#endif
   return RAS_OK;
 }
 

@@ -36,6 +36,60 @@ __global__ void __launch_bounds__(512, 1) kbar(unsigned long long* bar, double* 
     for (int o = 16; o; o >>= 1) v += __shfl_down_sync(~0u, v, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
+    if (V >= 9) {  // 3 values per CTA (as k_resident_pcg): 9 = 3 release stores + acquire polls; 10 = + nanosleep(64)
+                   // 11: 1 fence + relaxed stores, relaxed polls; 12: 1 fence + relaxed stores, acquire polls;
+                   // 13: 1 fence + relaxed stores, relaxed polls + 1 reader fence
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double s = lane < 16 ? red[lane] : 0.0;
+        for (int o = 16; o; o >>= 1) s += __shfl_down_sync(~0u, s, o);
+        unsigned long long* sl = bar + 64;
+        const unsigned ring = seq % 3, nxt = (seq + 1) % 3;
+        if (lane == 0) {
+          for (int j = 0; j < 3; ++j)
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(sl + (nxt * 3 + j) * G + c), "l"(~0ull) : "memory");
+          if (V <= 10) {
+            for (int j = 0; j < 3; ++j)
+              asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(sl + (ring * 3 + j) * G + c),
+                           "l"((unsigned long long)__double_as_longlong(s + j)) : "memory");
+          } else {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (int j = 0; j < 3; ++j)
+              asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(sl + (ring * 3 + j) * G + c),
+                           "l"((unsigned long long)__double_as_longlong(s + j)) : "memory");
+          }
+        }
+        unsigned long long u[3][5];
+        for (int j = 0; j < 3; ++j)
+          for (int t = 0; t < 5; ++t) u[j][t] = lane + 32 * t < G ? ~0ull : 0ull;
+        for (;;) {
+          bool done = true;
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int t = 0; t < 5; ++t)
+              if (u[j][t] == ~0ull)
+                u[j][t] = (V == 11 || V == 13) ? ld_rlx(sl + (ring * 3 + j) * G + lane + 32 * t)
+                                               : ld_acq(sl + (ring * 3 + j) * G + lane + 32 * t);
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int t = 0; t < 5; ++t) done = done && u[j][t] != ~0ull;
+          if (__all_sync(~0u, done)) break;
+          if (V == 10) __nanosleep(64);
+        }
+        if (V == 13) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        double a2 = 0;
+        for (int j = 0; j < 3; ++j)
+          for (int t = 0; t < 5; ++t) a2 += __longlong_as_double(u[j][t]);
+        for (int o = 16; o; o >>= 1) a2 += __shfl_xor_sync(~0u, a2, o);
+        if (lane == 0) red[0] = a2;
+      }
+      __syncthreads();
+      acc = red[0] * 1e-9;
+      ++seq;
+      continue;
+    }
     if (V >= 6) {  // 6: parallel poll + fence.sc; 7: parallel poll + fence.acq_rel; 8: no fence
       if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
@@ -177,7 +231,7 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* bar;
   double *part, *out;
-  cudaMalloc(&bar, (64 + 3 * 1024) * 8);
+  cudaMalloc(&bar, (64 + 9 * 1024) * 8);
   cudaMalloc(&part, 2 * 1024 * 8);
   cudaMalloc(&out, 8);
   const int iters = 2000;
@@ -197,6 +251,19 @@ int main() {
     t7 = run<7>(G, iters, bar, part, out);
     cudaMemset(bar + 64, 0xff, 3 * 1024 * 8);
     t8 = run<8>(G, iters, bar, part, out);
+    cudaMemset(bar + 64, 0xff, 3 * 1024 * 8 * 3);
+    float t9 = run<9>(G, iters, bar, part, out);
+    cudaMemset(bar + 64, 0xff, 3 * 1024 * 8 * 3);
+    float t10 = run<10>(G, iters, bar, part, out);
+    float t11, t12, t13;
+    cudaMemset(bar + 64, 0xff, 3 * 1024 * 8 * 3);
+    t11 = run<11>(G, iters, bar, part, out);
+    cudaMemset(bar + 64, 0xff, 3 * 1024 * 8 * 3);
+    t12 = run<12>(G, iters, bar, part, out);
+    cudaMemset(bar + 64, 0xff, 3 * 1024 * 8 * 3);
+    t13 = run<13>(G, iters, bar, part, out);
+    printf("G=%3d 3-value ring: 3 st.release + acquire polls %.2f | + nanosleep %.2f | fence+relaxed st: relaxed polls %.2f, acquire polls %.2f, relaxed polls + fence %.2f\n",
+           G, t9 * 1e3 / iters, t10 * 1e3 / iters, t11 * 1e3 / iters, t12 * 1e3 / iters, t13 * 1e3 / iters);
     printf("G=%3d parallel-poll ring: fence.sc %.2f | fence.acq_rel %.2f | no fence (unsafe) %.2f\n", G, t6 * 1e3 / iters,
            t7 * 1e3 / iters, t8 * 1e3 / iters);
     printf("G=%3d us/barrier: fence+atom+acq %.2f | red.release+rlx %.2f | cg.sync %.2f | +nanosleep %.2f | 2-level %.2f | sentinel ring %.2f\n", G,
