@@ -1098,6 +1098,9 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
     const uint8_t* const dcode = D.code + rb;
     const double* const dval = D.v + rb;
     __syncthreads();
+    const int ng = band.z + band.w;  // ghost rows: [-glo, 0) and [nr, nr + ghi)
+    auto ghost_row = [&](int t) { return t < band.z ? t - band.z : nr + (t - band.z); };
+    for (int t = threadIdx.x; t < ng; t += NT) sp[ghost_row(t)] = __ldcg(&RAS_PUB(pub_p, 1)[ghost_row(t)]);  // p_1
     for (int i = threadIdx.x; i < nr; i += NT) {
       sp[i] = __ldcg(&RAS_PUB(pub_p, 1)[i]);  // p_1 = z_0
       sr[i] = __ldcg(&RAS_PUB(pub_r, 0)[i]);  // r_0
@@ -1114,30 +1117,50 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
     __syncthreads();
     auto diag = [&](int i) -> double { return Z ? stab[sdc[i]] : sdg[i]; };
     auto dinv = [&](int i) -> double { return Z ? sinv[sdc[i]] : __drcp_rn(sdg[i]); };
+    // Ghost zones of p_{it+1}, staged during pass B of iteration it: the loads of
+    // the first kGR ghost rows per thread are issued before pass B (registers),
+    // the values p_{it+1}(c) = fma(beta, p_it(c), D^-1(c) fma(-alpha, q_it(c), r_{it-1}(c)))
+    // -- the owner's expression -- are stored after it.
+    constexpr int kGR = 3;
+    double gq[kGR], gr[kGR], gpv[kGR];
+    uint32_t gc[kGR];
+    auto ghost_issue = [&](int it) {
+#pragma unroll
+      for (int u = 0; u < kGR; ++u) {
+        const int t = threadIdx.x + u * NT;
+        if (t < ng) {
+          const int li = ghost_row(t);
+          gq[u] = __ldcg(&RAS_PUB(pub_q, it & 1)[li]);
+          gr[u] = __ldcg(&RAS_PUB(pub_r, (it - 1) & 1)[li]);
+          gpv[u] = __ldcg(&RAS_PUB(pub_p, it & 1)[li]);
+          if (Z)
+            gc[u] = __ldg(&dcode[li]);
+          else
+            gpv[u] = gpv[u];
+        }
+      }
+    };
+    auto ghost_value = [&](int it, int li, double q_, double r_, double p_, uint32_t code) {
+      const double di = Z ? sinv[code] : __drcp_rn(__ldg(&dval[li]));
+      return __fma_rn(beta, p_, __dmul_rn(di, __fma_rn(-alpha, q_, r_)));
+    };
+    auto ghost_finish = [&](int it) {
+#pragma unroll
+      for (int u = 0; u < kGR; ++u) {
+        const int t = threadIdx.x + u * NT;
+        if (t < ng) sp[ghost_row(t)] = ghost_value(it, ghost_row(t), gq[u], gr[u], gpv[u], Z ? gc[u] : 0u);
+      }
+      for (int t = threadIdx.x + kGR * NT; t < ng; t += NT) {
+        const int li = ghost_row(t);
+        sp[li] = ghost_value(it, li, __ldcg(&RAS_PUB(pub_q, it & 1)[li]), __ldcg(&RAS_PUB(pub_r, (it - 1) & 1)[li]),
+                             __ldcg(&RAS_PUB(pub_p, it & 1)[li]), Z ? (uint32_t)__ldg(&dcode[li]) : 0u);
+      }
+    };
     for (;;) {
       const int it = its + 1;
       RAS_TRACE(0)
       // pass A: q = A_p p_it (halo columns recomputed, see above), then the
       // partials sigma = (p, q), (z, q), (q, D^-1 q) [, (r, q), (q, q)]
-      {
-        // stage the ghost zones of p_it: [-glo, 0) and [nr, nr + ghi)
-        const int ng = band.z + band.w;
-        for (int t = threadIdx.x; t < ng; t += NT) {
-          const int li = t < band.z ? t - band.z : nr + (t - band.z);
-          double pv;
-          if (it == 1) {
-            pv = __ldcg(&RAS_PUB(pub_p, 1)[li]);
-          } else {
-            // p_{it-1}, q_{it-1}, r_{it-2}: the owner's own expression
-            const double di = Z ? sinv[__ldg(&dcode[li])] : __drcp_rn(__ldg(&dval[li]));
-            const double zc = __dmul_rn(
-                di, __fma_rn(-alpha, __ldcg(&RAS_PUB(pub_q, (it - 1) & 1)[li]), __ldcg(&RAS_PUB(pub_r, it & 1)[li])));
-            pv = __fma_rn(beta, __ldcg(&RAS_PUB(pub_p, (it - 1) & 1)[li]), zc);
-          }
-          sp[li] = pv;
-        }
-        __syncthreads();
-      }
       double v[NV];
 #pragma unroll
       for (int k = 0; k < NV; ++k) v[k] = 0.0;
@@ -1240,6 +1263,7 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
         stop = its >= m || !(rho_new > 0.0);  // R7 (rho' <= 0 only by rounding: breakdown)
         beta = rho_new / rho;
         rho = rho_new;
+        if (!stop) ghost_issue(it);
         // pass B (own rows): d += alpha p, r -= alpha q, and unless stopping
         // p_{it+1} = D^-1 r + beta p; publish r_it, p_{it+1} of the export band
 #pragma unroll
@@ -1260,6 +1284,7 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
             }
           }
         }
+        if (!stop) ghost_finish(it);
       } else {
         // pass B1: d += alpha p, r -= alpha q (published), z = D^-1 r; (r, z), (r, r)
         double v2[2] = {0.0, 0.0};
@@ -1281,6 +1306,7 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
         stop = its >= m || v2[0] == 0.0 || sqrt(v2[1]) <= inner_tol * sqrt(rt2);  // R7, R6
         beta = v2[0] / rho;
         rho = v2[0];
+        if (!stop) ghost_issue(it);
         // pass B2: p_{it+1} = D^-1 r + beta p (published)
         if (!stop) {
 #pragma unroll
@@ -1292,6 +1318,7 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
               if (i < band.x || i >= band.y) __stcg(&RAS_PUB(pub_p, (it + 1) & 1)[i], pn);
             }
           }
+          ghost_finish(it);
         }
       }
       RAS_TRACE(3)
