@@ -396,7 +396,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
-        d2h = n * 8 if world == 1 else (n * 8 + info["n_own"] * 8 * 2)
+        d2h = n * 8  # x_out: the assembled global vector (NCCL allreduce on device, one D2H copy)
         e2e = {"value": P * args.e2e_steps / el, "unit": "updates/s", "h2d_bytes_per_step": n * 8,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "note": "each step = ras_solve(x0=pinned host, max_iters=1, x_out=pinned host): H2D x0, one sweep + "

@@ -1018,51 +1018,20 @@ static ras_status load_x0(ras_ctx* c, const double* x0) {
   return RAS_OK;
 }
 
-// Gather owner values to x_out (len n) on every rank (P242).
+// Gather owner values to x_out (len n) on every rank (P242): every rank
+// scatters its owned values into a zeroed global-order vector on the device and
+// one NCCL sum-allreduce over NVLink assembles it (the owned sets partition the
+// index space, so each entry is one rank's value plus zeros: exact).
 static ras_status gather(ras_ctx* c, double* x_out) {
   const ras_plan* pl = c->plan;
-  if (c->world == 1) {
-    TRY(ensure_xglob(c));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n_own + 255) / 256, 148 * 16));
-    LAUNCH(K_CTRL, k_gather_x<<<g, 256, 0, c->stream>>>(c->n_own, c->d_own_gid, c->d_x, c->d_xglob));
-    RAS_CUDA(c, cudaMemcpyAsync(x_out, c->d_xglob, (size_t)pl->n * 8, cudaMemcpyDeviceToHost, c->stream));
-    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-    return RAS_OK;
-  }
-  std::vector<double> own((size_t)c->n_own);
-  RAS_CUDA(c, cudaMemcpyAsync(own.data(), c->d_x, own.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  TRY(ensure_xglob(c));
+  if (c->world > 1) RAS_CUDA(c, cudaMemsetAsync(c->d_xglob, 0, (size_t)pl->n * 8, c->stream));
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n_own + 255) / 256, 148 * 16));
+  LAUNCH(K_CTRL, k_gather_x<<<g, 256, 0, c->stream>>>(c->n_own, c->d_own_gid, c->d_x, c->d_xglob));
+  if (c->world > 1)
+    RAS_NCCL(c, ncclAllReduce(c->d_xglob, c->d_xglob, (size_t)pl->n, ncclDouble, ncclSum, c->nccl, c->stream));
+  RAS_CUDA(c, cudaMemcpyAsync(x_out, c->d_xglob, (size_t)pl->n * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  // all-gather padded (gid, value) pairs
-  std::vector<int64_t> cnt{c->n_own};
-  int64_t *d_cnt, *d_cnts;
-  TRY(upload(c, &d_cnt, cnt));
-  TRY(zalloc(c, &d_cnts, c->world));
-  RAS_NCCL(c, ncclAllGather(d_cnt, d_cnts, 1, ncclInt64, c->nccl, c->stream));
-  std::vector<int64_t> cnts(c->world);
-  RAS_CUDA(c, cudaMemcpyAsync(cnts.data(), d_cnts, c->world * 8, cudaMemcpyDeviceToHost, c->stream));
-  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  const int64_t mx = *std::max_element(cnts.begin(), cnts.end());
-  std::vector<double> pack((size_t)mx * 2, 0.0);
-  for (int64_t i = 0; i < c->n_own; ++i) {
-    pack[i] = own[i];
-    int64_t g = pl->own_gid[i];
-    std::memcpy(&pack[mx + i], &g, 8);
-  }
-  double *d_pack, *d_all;
-  TRY(upload(c, &d_pack, pack));
-  TRY(zalloc(c, &d_all, (size_t)mx * 2 * c->world));
-  RAS_NCCL(c, ncclAllGather(d_pack, d_all, (size_t)mx * 2, ncclDouble, c->nccl, c->stream));
-  std::vector<double> all((size_t)mx * 2 * c->world);
-  RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  for (int r = 0; r < c->world; ++r) {
-    const double* v = all.data() + (size_t)r * mx * 2;
-    for (int64_t i = 0; i < cnts[r]; ++i) {
-      int64_t g;
-      std::memcpy(&g, &v[mx + i], 8);
-      x_out[g] = v[i];
-    }
-  }
   return RAS_OK;
 }
 

@@ -39,7 +39,9 @@ def _worker(rank, world, nccl_id, cfg, q):
             r1 = min(nx * ny, rows.max() + 1 + (gamma + 1) * nx)
             A = ri.laplace_2d_rows(nx, ny, r0, r1)
             b = b[r0:r1]
-        s = R.Solver(A, b, owner, gamma, R.options(cfg["solver"], cfg["m"], detector=cfg.get("detector", "decentral")),
+        s = R.Solver(A, b, owner, gamma,
+                     R.options(cfg["solver"], cfg["m"], detector=cfg.get("detector", "decentral"),
+                               path=cfg.get("path", "auto")),
                      comm={"rank": rank, "world": world, "device": rank, "nccl_id": nccl_id})
         out = {}
         for k in cfg.get("ks", []):
@@ -85,13 +87,13 @@ def _oracle(cfg, K):
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("world", [2, 4])
-def test_multi_gpu_sync_parity(world):
+@pytest.mark.parametrize("world,path", [(2, "auto"), (4, "auto"), (2, "resident"), (2, "tiled")])
+def test_multi_gpu_sync_parity(world, path):
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     nx, ny = 96, 80
     cfg = dict(nx=nx, ny=ny, P=8, gamma=3, solver="jacobi", m=12, ks=[1, 4],
-               owner=ri.voronoi_partition(nx, ny, 8, seed=5), window=True)
+               owner=ri.voronoi_partition(nx, ny, 8, seed=5), window=True, path=path)
     res = _run(world, cfg)
     A, b, ref = _oracle(cfg, 4)
     for r in range(world):
