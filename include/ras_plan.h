@@ -90,6 +90,14 @@ ras_status ras_plan_send_list(const ras_plan* plan, int32_t dst_rank, int64_t* c
 /* Global ids of the owned slots (len n_own) and halo slots (len n_halo). */
 ras_status ras_plan_storage_gids(const ras_plan* plan, int64_t* own_gids, int64_t* halo_gids);
 
+/* Communication pattern of the partition (PAPER §3.3 "Partitioning", Fig. 2, P257-275):
+ * counts[p * P + q] = number of values subdomain p receives from subdomain q per
+ * exchange, i.e. |{g in (Omega_p \ S_p) u Gamma_p : owner(g) = q}| (R4), for this
+ * rank's local subdomains p; every other entry is set to 0 (sum the arrays of all
+ * ranks for the full matrix).  counts: caller-owned host array of P*P int64.
+ * Valid after ras_plan_build.  Errors: RAS_EINVAL on NULL arguments. */
+ras_status ras_plan_comm_pattern(const ras_plan* plan, int64_t* counts);
+
 void ras_plan_free(ras_plan* plan);
 
 /* The plan a context was built from (borrowed; valid until ras_free). */

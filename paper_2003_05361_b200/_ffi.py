@@ -106,6 +106,7 @@ SIGNATURES = [
     ("ras_plan_maps", I32, [C.c_void_p, I32, P(I32), P(I32), P(I32)]),
     ("ras_plan_send_list", I32, [C.c_void_p, I32, P(I64), P(I64), P(I32), P(I64)]),
     ("ras_plan_storage_gids", I32, [C.c_void_p, P(I64), P(I64)]),
+    ("ras_plan_comm_pattern", I32, [C.c_void_p, P(I64)]),
     ("ras_plan_free", None, [C.c_void_p]),
     ("ras_ctx_plan", I32, [C.c_void_p, P(C.c_void_p)]),
 ]

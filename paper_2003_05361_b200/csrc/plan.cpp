@@ -165,17 +165,24 @@ static void build_phase1(ras_plan* pl, const ras_partition* part) {
     }
   };
   for (auto& S : pl->subs) {
+    std::vector<int32_t> src;  // owner subdomain of every value of need_p = (Omega_p \ S_p) u Gamma_p
     for (size_t i = 0; i < S.omega.size(); ++i)
       if (!S.owned[i]) {
         add(S.omega[i]);
-        S.nbr_subs.push_back(part->owner[S.omega[i]]);
+        src.push_back(part->owner[S.omega[i]]);
       }
     for (int64_t g : S.ghosts) {
       add(g);
-      S.nbr_subs.push_back(part->owner[g]);
+      src.push_back(part->owner[g]);
     }
-    std::sort(S.nbr_subs.begin(), S.nbr_subs.end());
-    S.nbr_subs.erase(std::unique(S.nbr_subs.begin(), S.nbr_subs.end()), S.nbr_subs.end());
+    std::sort(src.begin(), src.end());
+    for (size_t i = 0; i < src.size();) {  // run lengths: neighbour subdomains and receive counts (Fig. 2)
+      size_t j = i;
+      while (j < src.size() && src[j] == src[i]) ++j;
+      S.nbr_subs.push_back(src[i]);
+      S.nbr_cnt.push_back((int64_t)(j - i));
+      i = j;
+    }
   }
   std::vector<uint8_t>().swap(hmark);
   std::sort(halo.begin(), halo.end(), [&](int64_t a, int64_t b) {
@@ -543,6 +550,15 @@ ras_status ras_plan_storage_gids(const ras_plan* pl, int64_t* own_gids, int64_t*
   if (!pl) return RAS_EINVAL;
   if (own_gids) std::copy(pl->own_gid.begin(), pl->own_gid.end(), own_gids);
   if (halo_gids) std::copy(pl->halo_gid.begin(), pl->halo_gid.end(), halo_gids);
+  return RAS_OK;
+}
+
+ras_status ras_plan_comm_pattern(const ras_plan* pl, int64_t* counts) {
+  if (!pl || !counts) return RAS_EINVAL;
+  const size_t P = (size_t)pl->P;
+  std::fill(counts, counts + P * P, (int64_t)0);
+  for (const auto& S : pl->subs)
+    for (size_t k = 0; k < S.nbr_subs.size(); ++k) counts[(size_t)S.p * P + S.nbr_subs[k]] = S.nbr_cnt[k];
   return RAS_OK;
 }
 

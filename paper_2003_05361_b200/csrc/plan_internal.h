@@ -41,6 +41,7 @@ struct SubPlan {
   std::vector<uint8_t> owned;    // per omega row
   std::vector<int64_t> ghosts;   // Gamma_p ascending
   std::vector<int32_t> nbr_subs; // owner subdomains of need_p (ascending, != p)
+  std::vector<int64_t> nbr_cnt;  // values of need_p owned by each nbr_subs entry (receive counts)
   int64_t row_off = 0, nrows = 0, nrows_pad = 0;  // row space
   int64_t own_off = 0, nown = 0;                   // owned slots
   int64_t tile_begin = 0, ntiles = 0;

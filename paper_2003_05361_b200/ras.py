@@ -132,6 +132,13 @@ class Plan:
     def finalize(self):
         _check(F.lib().ras_plan_finalize(self._h))
 
+    def comm_pattern(self) -> np.ndarray:
+        """ras_plan_comm_pattern: P x P receive counts, row = receiver (Fig. 2), this rank's rows."""
+        P = self.info()["num_subdomains"]
+        out = np.empty((P, P), dtype=np.int64)
+        _check(F.lib().ras_plan_comm_pattern(self._h, F.ptr(out, F.I64)))
+        return out
+
     def subdomain(self, local_idx):
         p, no, ng = F.I32(), F.I64(), F.I64()
         _check(F.lib().ras_plan_subdomain(self._h, local_idx, C.byref(p), C.byref(no), None, None, C.byref(ng), None))

@@ -144,3 +144,70 @@ def test_plan_validation_errors():
     B.indices[B.indptr[2]], B.indices[B.indptr[2] + 1] = B.indices[B.indptr[2] + 1], B.indices[B.indptr[2]]
     with pytest.raises(R.RasError, match="strictly increasing"):
         R.Plan(B, None, own, 1)
+
+
+def _diameter(C):
+    """Diameter of the subdomain graph p ~ q iff C[p, q] + C[q, p] > 0 (BFS from every node)."""
+    P = C.shape[0]
+    adj = [np.nonzero((C[p] + C[:, p]) > 0)[0] for p in range(P)]
+    best = 0
+    for s in range(P):
+        dist = np.full(P, -1)
+        dist[s] = 0
+        frontier = [s]
+        while frontier:
+            nxt = []
+            for u in frontier:
+                for v in adj[u]:
+                    if v != u and dist[v] < 0:
+                        dist[v] = dist[u] + 1
+                        nxt.append(v)
+            frontier = nxt
+        best = max(best, dist.max())
+    return best
+
+
+@pytest.mark.parametrize("scheme", ["regular1d", "regular2d", "graph"])
+@pytest.mark.parametrize("gamma", [0, 2])
+def test_comm_pattern_bit_exact(scheme, gamma):
+    # NEXT f4 (PAPER §3.3 "Partitioning", Fig. 2, P257-290): the library's receive
+    # counts equal the oracle's, computed independently from its own overlap sets
+    N, P = 48, 9
+    A = ri.laplace_2d(N)
+    owner = {"regular1d": O.partition_regular1d(N, P), "regular2d": O.partition_regular2d(N, P),
+             "graph": ri.voronoi_partition(N, N, P, seed=3)}[scheme]
+    C = R.Plan(A, None, owner, gamma).comm_pattern()
+    ref = O.comm_pattern(O.setup(A, np.zeros(N * N), owner, gamma), owner, P)
+    assert C.dtype == np.int64 and np.array_equal(C, ref)
+    assert np.all(np.diag(C) == 0)
+    assert np.array_equal(C > 0, (C > 0).T)  # symmetric A: p needs q iff q needs p
+
+
+def test_comm_pattern_multi_rank_rows_sum_to_the_whole():
+    N, P, gamma = 40, 6, 1
+    A = ri.laplace_2d(N)
+    owner = ri.voronoi_partition(N, N, P, seed=7)
+    ref = O.comm_pattern(O.setup(A, np.zeros(N * N), owner, gamma), owner, P)
+    tot = np.zeros((P, P), np.int64)
+    for rank in range(3):
+        part = R.Plan(A, None, owner, gamma, rank=rank, world=3).comm_pattern()
+        mine = [p for p in range(P) if (p * 3) // P == rank]
+        assert not part[[p for p in range(P) if p not in mine]].any()
+        tot += part
+    assert np.array_equal(tot, ref)
+
+
+@pytest.mark.parametrize("P", [4, 9, 16])
+def test_information_propagation_distance(P):
+    # P277-286: regular1d needs P - 1 exchanges between the farthest subdomains;
+    # regular2d (px x py tiles) (px - 1) + (py - 1) with face neighbours only
+    # (gamma = 0) and max(px, py) - 1 once the overlap adds the diagonal tiles (R3)
+    N = 48
+    A = ri.laplace_2d(N)
+    px, py = O.factor_pair(P)
+    d1 = _diameter(R.Plan(A, None, O.partition_regular1d(N, P), 1).comm_pattern())
+    d2_face = _diameter(R.Plan(A, None, O.partition_regular2d(N, P), 0).comm_pattern())
+    d2_diag = _diameter(R.Plan(A, None, O.partition_regular2d(N, P), 1).comm_pattern())
+    assert d1 == P - 1
+    assert d2_face == (px - 1) + (py - 1)
+    assert d2_diag == max(px, py) - 1

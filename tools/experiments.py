@@ -6,8 +6,12 @@ line per configuration, through the C ABI:
   regime    E3/E9 + NEXT f2 (P527-546, P716-735): the paper's latency regime, 4096
             unknowns per subdomain, many subdomains per GPU: sync vs async
   detector  E8 (P678-691): centralized vs decentralized detection (async)
+  partition NEXT f4 / E2 (P257-290, P513-546, Figs. 2-3): regular1d vs regular2d vs
+            graph partitions at 4096 unknowns per subdomain: communication
+            pattern (heat map, volume, neighbours, propagation distance) and
+            sweeps / time-to-solution, sync and async
 
-  python tools/experiments.py overlap|regime|detector [--tol 1e-8] [--out FILE]
+  python tools/experiments.py overlap|regime|detector|partition [--tol 1e-8] [--out FILE]
 """
 from __future__ import annotations
 
@@ -25,12 +29,14 @@ import numpy as np  # noqa: E402
 import ras_inputs as ri  # noqa: E402
 
 
-def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decentral", max_iters=200000, reps=1):
+def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decentral", max_iters=200000, reps=1,
+        owner=None):
     import paper_2003_05361_b200 as R
 
     A = ri.laplace_2d(nx, ny)
     b = ri.rhs(nx * ny, 0)
-    owner = R.partition_regular(nx, ny, 1, px, py, 1)
+    if owner is None:
+        owner = R.partition_regular(nx, ny, 1, px, py, 1)
     s = R.Solver(A, b, owner, gamma, R.options(solver, m, detector=detector))
     out = []
     for _ in range(reps):
@@ -53,9 +59,72 @@ def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decen
     return rec
 
 
+def heatmap(C):
+    """Fig. 2 style text heat map of receive counts (row = receiver): '.' none, 1-9 = decile of the max."""
+    mx = max(int(C.max()), 1)
+    rows = []
+    for p in range(C.shape[0]):
+        rows.append("".join("." if v == 0 else str(min(9, 1 + (9 * int(v)) // (mx + 1))) for v in C[p]))
+    return rows
+
+
+def diameter(C):
+    P = C.shape[0]
+    adj = [np.nonzero((C[p] + C[:, p]) > 0)[0] for p in range(P)]
+    best = 0
+    for s0 in range(P):
+        dist = np.full(P, -1)
+        dist[s0] = 0
+        fr = [s0]
+        while fr:
+            nx = []
+            for u in fr:
+                for v in adj[u]:
+                    if v != u and dist[v] < 0:
+                        dist[v] = dist[u] + 1
+                        nx.append(v)
+            fr = nx
+        best = max(best, int(dist.max()))
+    return best
+
+
+def partition_study(tol, reps, gamma=4, sub=64, Ps=(4, 16, 36, 64, 100)):
+    """f4: three partitioners at `sub`^2 unknowns per subdomain (P x sub^2 unknowns)."""
+    import paper_2003_05361_b200 as R
+
+    recs = []
+    for P in Ps:
+        k = int(round(P ** 0.5))
+        N = k * sub
+        px, py = R_factor(P)
+        owners = {"regular1d": R.partition_regular(N, N, 1, 1, P, 1),
+                  "regular2d": R.partition_regular(N, N, 1, px, py, 1),
+                  "graph": ri.voronoi_partition(N, N, P, seed=1)}
+        A = ri.laplace_2d(N)
+        for name, owner in owners.items():
+            C = R.Plan(A, None, owner, gamma).comm_pattern()
+            stats = {"partition": name, "P": P, "grid": [N, N], "overlap": gamma,
+                     "comm_values_per_sweep": int(C.sum()), "max_neighbours": int(((C > 0).sum(1)).max()),
+                     "max_recv_per_subdomain": int(C.sum(1).max()), "propagation_distance": diameter(C)}
+            if P <= 16:
+                stats["heatmap"] = heatmap(C)
+            for mode in ("sync", "async"):
+                r = run(N, N, 1, P, gamma, mode, tol, reps=1 if mode == "sync" else reps, owner=owner)
+                recs.append({**stats, **{k2: v for k2, v in r.items() if k2 not in ("grid", "tiles", "subdomains")}})
+    return recs
+
+
+def R_factor(P):
+    """(px, py), px * py = P, closest to square with py >= px (R23)."""
+    px = int(P ** 0.5)
+    while P % px:
+        px -= 1
+    return px, P // px
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["overlap", "regime", "detector"])
+    ap.add_argument("which", choices=["overlap", "regime", "detector", "partition"])
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--out", default=None)
     ap.add_argument("--reps", type=int, default=3)
@@ -71,6 +140,8 @@ def main():
         for (px, py) in ((2, 2), (4, 4), (6, 6), (8, 8), (12, 8), (12, 12)):
             for mode in ("sync", "async"):
                 recs.append(run(64 * px, 64 * py, px, py, 16, mode, a.tol, reps=1 if mode == "sync" else a.reps))
+    elif a.which == "partition":
+        recs = partition_study(a.tol, a.reps)
     else:
         for det in ("central", "decentral"):
             recs.append(run(512, 512, 8, 8, 16, "async", a.tol, detector=det, reps=a.reps))
