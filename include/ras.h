@@ -62,8 +62,14 @@ typedef enum {
   RAS_LS_JACOBI_PCG = 0, /* PCG, M = diag(A_p), fixed m iterations (P313-315; R6, R8) */
   RAS_LS_IC0_PCG = 1,    /* PCG, M = L L^T, IC(0) of A_p, level-scheduled trisolves (P317-323; R9) */
   RAS_LS_ILU0_PCG = 2,   /* PCG, M = L U, ILU(0) of A_p (R10) */
-  RAS_LS_EXACT_PCG = 3   /* Jacobi-PCG to ||r|| <= 1e-14 ||r~||, <= 10|Omega_p| iterations:
-                            the GPU stand-in for the paper's direct local solve (P317-318; R6) */
+  RAS_LS_EXACT_PCG = 3,  /* Jacobi-PCG to ||r|| <= 1e-14 ||r~||, <= 10|Omega_p| iterations:
+                            the iterative stand-in for the paper's direct local solve (P317-318; R6) */
+  RAS_LS_CHOLESKY = 4    /* direct local solve (P311-318, NEXT f1): complete Cholesky factor of A_p in
+                            natural Omega_p order (banded, computed on the host once in ras_setup),
+                            two banded triangular solves per local solve, one CTA per subdomain.
+                            Needs every padded |Omega_p| <= 12288 rows and the bands (2 n (b+1) FP64
+                            per subdomain) <= 16 GB in total, else RAS_EINVAL; RAS_ENOTSPD on a
+                            non-positive pivot */
 } ras_local_solver;
 
 typedef enum { RAS_DET_CENTRAL = 0, RAS_DET_DECENTRAL = 1 } ras_detector;
@@ -122,7 +128,13 @@ typedef struct {
   int32_t stage_p;               /* 1: stage p in shared memory in the tiled SpMV */
   ras_pcg_path pcg_path;         /* default RAS_PCG_AUTO */
   int32_t reserved_i[3];
-  double reserved_d[4];
+  /* Optimized RAS (NEXT f3, PAPER P760-763, R30): Robin-type transmission condition in algebraic
+   * form -- the local solve uses A~_p = A_p - robin * diag(sum_{j not in Omega_p} |a_ij|) (rows
+   * coupled outside Omega_p); the residual keeps A.  0 = RAS (Dirichlet truncation, default);
+   * -> 1 approaches Neumann.  Must be in [0, 1) (A~_p stays SPD) and > 0 needs overlap >= 1
+   * (the restricted iteration diverges without overlap), else RAS_EINVAL. */
+  double robin;
+  double reserved_d[3];
 } ras_options;
 
 /* Multi-GPU plumbing.  NULL = single GPU (current device, default stream). */

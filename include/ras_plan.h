@@ -90,6 +90,11 @@ ras_status ras_plan_send_list(const ras_plan* plan, int32_t dst_rank, int64_t* c
 /* Global ids of the owned slots (len n_own) and halo slots (len n_halo). */
 ras_status ras_plan_storage_gids(const ras_plan* plan, int64_t* own_gids, int64_t* halo_gids);
 
+/* ORAS transmission parameter of the local matrices (ras_options.robin, R30); call
+ * before ras_plan_finalize.  Errors: RAS_EINVAL if robin is outside [0, 1) or the plan
+ * is already finalized. */
+ras_status ras_plan_set_robin(ras_plan* plan, double robin);
+
 /* Communication pattern of the partition (PAPER §3.3 "Partitioning", Fig. 2, P257-275):
  * counts[p * P + q] = number of values subdomain p receives from subdomain q per
  * exchange, i.e. |{g in (Omega_p \ S_p) u Gamma_p : owner(g) = q}| (R4), for this

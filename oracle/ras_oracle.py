@@ -171,14 +171,22 @@ class Subdomain:
     b: np.ndarray
     solver: object = None
     extra: dict = field(default_factory=dict)
+    Asolve: sp.csr_matrix = None  # matrix of the local solve (A_p, or ORAS's A~_p); None = A
 
     @property
     def owned_global(self) -> np.ndarray:
         return self.omega[self.owned]
 
 
-def setup(A, b, owner, gamma, P=None):
-    """Alg. 1 `initialization_and_setup` (P233-237, P247-303) minus factorization."""
+def setup(A, b, owner, gamma, P=None, robin=0.0):
+    """Alg. 1 `initialization_and_setup` (P233-237, P247-303) minus factorization.
+
+    robin > 0: Optimized RAS (NEXT f3; PAPER P760-763 names ORAS as future work
+    and gives no formula -- DESIGN.md R30): a Robin-type transmission condition in
+    algebraic form, the local matrix loses `robin` times the couplings it drops,
+    A~_p = A_p - robin * diag(|B_p| 1)   (B_p = couplings to columns outside Omega_p),
+    so robin = 0 is RAS's Dirichlet truncation and robin -> 1 a Neumann condition.
+    Only the local solve uses A~_p; the residual b - A x keeps A."""
     A = as_scipy(A)
     owner = np.asarray(owner, dtype=np.int64)
     if P is None:
@@ -193,7 +201,12 @@ def setup(A, b, owner, gamma, P=None):
         Ap.sort_indices()
         Bp = rows[:, ghosts].tocsr()
         Bp.sort_indices()
-        subs.append(Subdomain(p, omega, owned, ghosts, Ap, Bp, np.asarray(b)[omega].copy()))
+        sub = Subdomain(p, omega, owned, ghosts, Ap, Bp, np.asarray(b)[omega].copy())
+        if robin:
+            dropped = np.asarray(abs(Bp).sum(axis=1)).ravel()
+            sub.Asolve = (Ap - sp.diags(robin * dropped)).tocsr()
+            sub.Asolve.sort_indices()
+        subs.append(sub)
     return subs
 
 
@@ -408,14 +421,15 @@ def make_local_solver(sub: Subdomain, kind: str, inner_iters: int = 20, inner_to
     R8), 'ic0' / 'ilu0' (incomplete-factor PCG, R9/R10).  Returns a callable
     r~ -> d and records the inner iteration count in sub.extra['inner']."""
     sub.extra["inner"] = 0
+    M = sub.A if sub.Asolve is None else sub.Asolve  # ORAS: A~_p (R30)
     if kind == "exact":
-        F = cholesky_factor(sub.A)
+        F = cholesky_factor(M)
 
         def solve(rt):
             return cholesky_solve(F, rt)
     elif kind in ("jacobi", "ic0", "ilu0"):
         if kind == "jacobi":
-            diag = sub.A.diagonal()
+            diag = M.diagonal()
             if (diag <= 0).any():
                 raise NotSPDError(f"non-positive diagonal in subdomain {sub.p}")
             dinv = 1.0 / diag
@@ -423,7 +437,7 @@ def make_local_solver(sub: Subdomain, kind: str, inner_iters: int = 20, inner_to
             def minv(r):
                 return dinv * r
         elif kind == "ic0":
-            L = ic0(sub.A).tocsr()
+            L = ic0(M).tocsr()
             Lt = L.T.tocsr()
             sub.extra["L"] = L
 
@@ -431,7 +445,7 @@ def make_local_solver(sub: Subdomain, kind: str, inner_iters: int = 20, inner_to
                 y = spla.spsolve_triangular(L, r, lower=True)
                 return spla.spsolve_triangular(Lt, y, lower=False)
         else:
-            L, U = ilu0(sub.A)
+            L, U = ilu0(M)
             sub.extra["L"], sub.extra["U"] = L, U
 
             def minv(r):
@@ -439,7 +453,7 @@ def make_local_solver(sub: Subdomain, kind: str, inner_iters: int = 20, inner_to
                 return spla.spsolve_triangular(U, y, lower=False)
 
         def solve(rt):
-            d, it = pcg(sub.A, minv, rt, inner_iters, inner_tol)
+            d, it = pcg(M, minv, rt, inner_iters, inner_tol)
             sub.extra["inner"] += it
             return d
     else:

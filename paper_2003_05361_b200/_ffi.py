@@ -15,7 +15,7 @@ RAS_OK, RAS_EINVAL, RAS_ENOTSPD, RAS_ENOCONV, RAS_EVERIFY, RAS_ECUDA, RAS_ENCCL,
 STATUS_NAMES = ["RAS_OK", "RAS_EINVAL", "RAS_ENOTSPD", "RAS_ENOCONV", "RAS_EVERIFY", "RAS_ECUDA", "RAS_ENCCL",
                 "RAS_ENOMEM", "RAS_ESTATE"]
 RAS_SYNC, RAS_ASYNC = 0, 1
-RAS_LS_JACOBI_PCG, RAS_LS_IC0_PCG, RAS_LS_ILU0_PCG, RAS_LS_EXACT_PCG = range(4)
+RAS_LS_JACOBI_PCG, RAS_LS_IC0_PCG, RAS_LS_ILU0_PCG, RAS_LS_EXACT_PCG, RAS_LS_CHOLESKY = range(5)
 RAS_DET_CENTRAL, RAS_DET_DECENTRAL = 0, 1
 RAS_PCG_AUTO, RAS_PCG_TILED, RAS_PCG_BLOCK, RAS_PCG_RESIDENT = range(4)
 ABI_VERSION = 2  # include/ras.h RAS_ABI_VERSION
@@ -37,7 +37,7 @@ class RasOptions(C.Structure):
     _fields_ = [("local_solver", I32), ("inner_iters", I32), ("inner_tol", F64), ("detector", I32),
                 ("local_crit_owned_only", I32), ("max_resumes", I32), ("use_graphs", I32), ("poll_interval", I32),
                 ("async_timeout_s", F64), ("scripted_flags", I32), ("fuse_p", I32), ("matrix_format", I32), ("stage_p", I32),
-                ("pcg_path", I32), ("reserved_i", I32 * 3), ("reserved_d", F64 * 4)]
+                ("pcg_path", I32), ("reserved_i", I32 * 3), ("robin", F64), ("reserved_d", F64 * 3)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -107,6 +107,7 @@ SIGNATURES = [
     ("ras_plan_send_list", I32, [C.c_void_p, I32, P(I64), P(I64), P(I32), P(I64)]),
     ("ras_plan_storage_gids", I32, [C.c_void_p, P(I64), P(I64)]),
     ("ras_plan_comm_pattern", I32, [C.c_void_p, P(I64)]),
+    ("ras_plan_set_robin", I32, [C.c_void_p, F64]),
     ("ras_plan_free", None, [C.c_void_p]),
     ("ras_ctx_plan", I32, [C.c_void_p, P(C.c_void_p)]),
 ]

@@ -23,7 +23,7 @@ struct DevBuf {
 
 struct AsyncRt;  // async-mode runtime (async.cu)
 
-enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_ZDOT, K_SMALL, K_RESID, K_NKINDS };
+enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_ZDOT, K_SMALL, K_RESID, K_BAND, K_NKINDS };
 
 // A range of tiles: every local subdomain (lp < 0) or one subdomain.
 struct Range {
@@ -54,6 +54,7 @@ struct KTimer {
 struct ModelBytes {  // algorithmic bytes per launch over the whole row space
   double residual, spmv_dot, update_dot, pupdate, prolong, pack, trsv, zdot;
   double local_solve;  // BLOCK / RESIDENT: compulsory HBM bytes of one whole local-solve launch
+  double band;         // direct solve: both bands read once + r~ in + x[S_p] read/written
 };
 
 }  // namespace ras
@@ -106,6 +107,10 @@ struct ras_ctx {
   unsigned long long* d_resid_slots = nullptr;
   double* d_q = nullptr;
   double* d_d = nullptr;
+  // direct local solve (NEXT f1): banded Cholesky factors, k_band_chol
+  bool chol = false;
+  ras::BandDev band{};
+  size_t band_smem = 0;
   // IC(0)/ILU(0) path (a3')
   bool ic = false;
   double* d_z = nullptr;

@@ -10,7 +10,9 @@
 // chunks; the device solve processes chunks in level order (trsv.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "plan_internal.h"
@@ -208,6 +210,78 @@ void build_factors(ras_plan* pl, int kind, TriHost& F, TriHost& B) {
     });
     T->rp.insert(T->rp.begin(), 0);
   }
+}
+
+
+
+// ---------------------------------------------------------------------------
+// NEXT f1: complete (direct) Cholesky factor of every local A_p, banded.
+// PAPER §3.3.1 (P311-318): the local matrix is factored once (CHOLMOD) and every
+// local solve is two triangular solves.  A_p in natural Omega_p order is banded
+// (2D tile: bandwidth ~ tile width + 2 gamma), so its complete factor L has all
+// fill inside the band: L = chol(A_p) row by row (Crout / up-looking),
+//   L(i,j) = (A(i,j) - sum_{k<j} L(i,k) L(j,k)) / L(j,j),  j in [i-b, i)
+//   L(i,i) = sqrt(A(i,i) - sum_{k<i} L(i,k)^2)
+// with sums in ascending k.  Stored twice, row-major with b+1 slots per row so
+// both device solves read rows contiguously: lower band L (slot j - i + b) for
+// the forward solve, upper band U = L^T (slot j - i) for the backward solve.
+// Padding rows of the row space are identity rows.  Throws Fail on a pivot <= 0.
+// ---------------------------------------------------------------------------
+void build_band_cholesky(const ras_plan* pl, BandHost& H) {
+  const size_t nl = pl->subs.size();
+  H.off.assign(nl + 1, 0);
+  H.bw.assign(nl, 0);
+  for (size_t lp = 0; lp < nl; ++lp) {
+    const auto& S = pl->subs[lp];
+    int32_t b = 0;
+    for (int64_t i = 0; i < S.nrows_pad; ++i)
+      for (int64_t e = pl->Ap_ptr[S.row_off + i]; e < pl->Ap_ptr[S.row_off + i + 1]; ++e)
+        b = std::max<int32_t>(b, (int32_t)std::llabs(i - (int64_t)pl->Ap_col[e]));
+    H.bw[lp] = b;
+    H.off[lp + 1] = H.off[lp] + S.nrows_pad * (int64_t)(b + 1);
+  }
+  H.L.assign((size_t)H.off[nl], 0.0);
+  H.U.assign((size_t)H.off[nl], 0.0);
+  std::vector<std::string> err(nl);
+  auto factor = [&](size_t lp) {
+    const auto& S = pl->subs[lp];
+    const int64_t n = S.nrows_pad, b = H.bw[lp], w = b + 1;
+    double* L = H.L.data() + H.off[lp];
+    // band of A (lower part) into L, then factor in place
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t e = pl->Ap_ptr[S.row_off + i]; e < pl->Ap_ptr[S.row_off + i + 1]; ++e) {
+        const int64_t j = pl->Ap_col[e];
+        if (j <= i) L[i * w + (j - i + b)] = pl->Ap_val[e];
+      }
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t j0 = std::max<int64_t>(0, i - b);
+      for (int64_t j = j0; j < i; ++j) {
+        double s = L[i * w + (j - i + b)];
+        for (int64_t k = std::max(j0, j - b); k < j; ++k) s -= L[i * w + (k - i + b)] * L[j * w + (k - j + b)];
+        L[i * w + (j - i + b)] = s / L[j * w + b];
+      }
+      double s = L[i * w + b];
+      for (int64_t k = j0; k < i; ++k) s -= L[i * w + (k - i + b)] * L[i * w + (k - i + b)];
+      if (!(s > 0.0)) {
+        err[lp] = "subdomain " + std::to_string(S.p) + ": Cholesky pivot " + std::to_string(s) + " <= 0 (local row " +
+                  std::to_string(i) + ")";
+        return;
+      }
+      L[i * w + b] = std::sqrt(s);
+    }
+    double* U = H.U.data() + H.off[lp];
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = std::max<int64_t>(0, i - b); j <= i; ++j) U[j * w + (i - j)] = L[i * w + (j - i + b)];
+  };
+  const size_t nt = std::max<size_t>(1, std::min<size_t>(nl, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (size_t lp = t; lp < nl; lp += nt) factor(lp);
+    });
+  for (auto& t : th) t.join();
+  for (size_t lp = 0; lp < nl; ++lp)
+    if (!err[lp].empty()) throw Fail{RAS_ENOTSPD, err[lp]};
 }
 
 }  // namespace ras

@@ -792,6 +792,107 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
 }
 
 // ---------------------------------------------------------------------------
+// NEXT f1: direct local solve (PAPER §3.3.1, P311-318: factor once, two
+// triangular solves per local solve) with the complete banded Cholesky factor
+// computed on the host (factor.cpp).  One CTA per subdomain: y = L^-1 r~ then
+// d = L^-T y, in 32-row blocks -- the band contribution of the rows already
+// solved is a warp-parallel dot product per row (coalesced along the band
+// row), the 32 x 32 diagonal triangle a sequential warp-shuffle solve -- with
+// y / d of the whole subdomain in shared memory, then the restricted
+// prolongation.  Runs after k_residual / k_finish (r~ in the row space, active).
+// ---------------------------------------------------------------------------
+constexpr int kNT_BAND = 256;
+constexpr int kBandMaxRows = 12288;  // y / d of one subdomain in shared memory (96 KB)
+
+struct BandDev {
+  const double* L;     // lower band, row-major, bw + 1 slots per row (slot j - i + bw)
+  const double* U;     // upper band = L^T, row-major (slot j - i)
+  const int64_t* off;  // per local subdomain offset into L / U
+  const int32_t* bw;   // per local subdomain bandwidth
+};
+
+static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, SmallSubs SS, BandDev B,
+                                                                 const double* __restrict__ r_in,
+                                                                 const int32_t* __restrict__ own_slot,
+                                                                 double* __restrict__ x, Scal S, Ctl C) {
+  extern __shared__ double sy[];  // y, overwritten by d from the last block down
+  __shared__ double blk[32][33];
+  __shared__ double sv[32];
+  pdl_start();
+  const int lp = lp_base + blockIdx.x;
+  if (stopped(C, lp) || !S.active[lp]) return;
+  const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+  const int b = B.bw[lp];
+  const int64_t w = b + 1;
+  const double* Lp = B.L + B.off[lp];
+  const double* Up = B.U + B.off[lp];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  constexpr int RW = 32 / (kNT_BAND / 32);  // block rows per warp
+  // forward: L y = r~
+  for (int i0 = 0; i0 < n; i0 += 32) {
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+      const int l = wp * RW + rr, i = i0 + l;
+      double acc = 0.0;
+      for (int j = max(0, i - b) + lane; j < i0; j += 32) acc += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
+      acc = warp_sum(acc);
+      if (lane == 0) sv[l] = __ldg(&r_in[r0 + i]) - acc;
+    }
+    for (int t = threadIdx.x; t < 32 * 32; t += kNT_BAND) {
+      const int l = t >> 5, m = t & 31;
+      blk[l][m] = (m <= l && l - m <= b) ? __ldg(&Lp[(int64_t)(i0 + l) * w + (m - l + b)]) : 0.0;
+    }
+    __syncthreads();
+    if (wp == 0) {
+      double s = sv[lane], yv = 0.0;
+      for (int m = 0; m < 32; ++m) {
+        const double ym = __shfl_sync(0xffffffffu, s, m) / blk[m][m];
+        if (lane == m) yv = ym;
+        if (lane > m) s -= blk[lane][m] * ym;
+      }
+      sy[i0 + lane] = yv;
+    }
+    __syncthreads();
+  }
+  // backward: L^T d = y (rows >= i0 + 32 of sy already hold d)
+  for (int i0 = n - 32; i0 >= 0; i0 -= 32) {
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+      const int l = wp * RW + rr, i = i0 + l;
+      double acc = 0.0;
+      const int j1 = min(n - 1, i + b);
+      for (int j = i0 + 32 + lane; j <= j1; j += 32) acc += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
+      acc = warp_sum(acc);
+      if (lane == 0) sv[l] = sy[i] - acc;
+    }
+    for (int t = threadIdx.x; t < 32 * 32; t += kNT_BAND) {
+      const int l = t >> 5, m = t & 31;
+      blk[l][m] = (m >= l && m - l <= b) ? __ldg(&Up[(int64_t)(i0 + l) * w + (m - l)]) : 0.0;
+    }
+    __syncthreads();
+    if (wp == 0) {
+      double s = sv[lane], dv = 0.0;
+      for (int m = 31; m >= 0; --m) {
+        const double dm = __shfl_sync(0xffffffffu, s, m) / blk[m][m];
+        if (lane == m) dv = dm;
+        if (lane < m) s -= blk[lane][m] * dm;
+      }
+      sy[i0 + lane] = dv;
+    }
+    __syncthreads();
+  }
+  // a4: restricted prolongation
+  for (int i = threadIdx.x; i < n; i += kNT_BAND) {
+    const int32_t sl = __ldg(&own_slot[r0 + i]);
+    if (sl >= 0) x[sl] = x[sl] + sy[i];
+  }
+  if (threadIdx.x == 0) {
+    S.its[lp] = 1;
+    S.active[lp] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Grid-resident regime (subdomains of up to ~1.2M rows, e.g. C2's 1024^2 tiles
 // + overlap): a persistent cooperative grid, one CTA per SM, split into groups
 // of gs CTAs; a group runs the WHOLE Jacobi-PCG local solve of one subdomain

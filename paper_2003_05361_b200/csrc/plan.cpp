@@ -267,6 +267,7 @@ static void build_finalize(ras_plan* pl) {
         const int64_t* rp = W.rowp(g, &len);
         int64_t nl_ = 0;
         bool has_diag = false;
+        double outside = 0.0;  // sum of |a_ij| over the columns outside Omega_p (ascending j)
         for (int64_t k = rp[0]; k < rp[0] + len; ++k) {
           int64_t c = pl->A_col[k];
           if (mark[c] == lp) {
@@ -276,8 +277,12 @@ static void build_finalize(ras_plan* pl) {
             } else {
               ++nl_;
             }
+          } else {
+            outside += std::fabs(pl->A_val[k]);
           }
         }
+        // ORAS (R30): the local matrix's diagonal carries the Robin term; R keeps A
+        if (pl->robin != 0.0) pl->diag[row] = pl->diag[row] - pl->robin * outside;
         if (!has_diag || !(pl->diag[row] > 0.0))
           throw fail(RAS_ENOTSPD, "subdomain " + std::to_string(S.p) + ": non-positive or missing diagonal at row " +
                                       std::to_string(g));
@@ -337,7 +342,7 @@ static void build_finalize(ras_plan* pl) {
           ++kR;
           if (mark[c] == lp) {
             pl->Ap_col.push_back(pos[c]);
-            pl->Ap_val.push_back(v);
+            pl->Ap_val.push_back(c == g ? pl->diag[row] : v);  // diagonal of A~_p (R30)
             if (c != g) {
               const int64_t eL = pl->L_sptr[sl] + kL * kSlice + lane;
               pl->L_col[eL] = (int32_t)(S.row_off + pos[c]);
@@ -550,6 +555,12 @@ ras_status ras_plan_storage_gids(const ras_plan* pl, int64_t* own_gids, int64_t*
   if (!pl) return RAS_EINVAL;
   if (own_gids) std::copy(pl->own_gid.begin(), pl->own_gid.end(), own_gids);
   if (halo_gids) std::copy(pl->halo_gid.begin(), pl->halo_gid.end(), halo_gids);
+  return RAS_OK;
+}
+
+ras_status ras_plan_set_robin(ras_plan* pl, double robin) {
+  if (!pl || pl->finalized || !(robin >= 0.0 && robin < 1.0)) return RAS_EINVAL;
+  pl->robin = robin;
   return RAS_OK;
 }
 

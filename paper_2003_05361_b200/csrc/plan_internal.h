@@ -35,6 +35,13 @@ struct TriHost {
   int64_t max_levels = 0;
 };
 
+// Complete banded Cholesky factors of every local A_p (factor.cpp, NEXT f1).
+struct BandHost {
+  std::vector<double> L, U;    // per subdomain nrows_pad x (bw + 1), row-major (see factor.cpp)
+  std::vector<int64_t> off;    // per subdomain offset into L / U (size nl + 1)
+  std::vector<int32_t> bw;     // per subdomain bandwidth b
+};
+
 struct SubPlan {
   int32_t p = -1;                // global subdomain id
   std::vector<int64_t> omega;    // Omega_p ascending
@@ -111,12 +118,15 @@ struct ras_plan {
   std::vector<int32_t> tile_cmin, tile_clen;  // local-matrix column span per tile (-1 = wider than stage_max)
   int32_t stage_max = 4096;                   // must equal ras::kStageMax (kernels.cuh)
   double b2_global_local = 0.0;  // sum over this rank's owned rows of b^2
+  double robin = 0.0;            // ORAS: A~_p,ii = a_ii - robin * sum_{j not in Omega_p} |a_ij| (R30)
 };
 
 namespace ras {
 // IC(0) (kind = RAS_LS_IC0_PCG) or ILU(0) factors of every local A_p, in level
 // order: F = forward (L), B = backward (L^T or U).  Throws Fail on a pivot <= 0.
 void build_factors(ras_plan* pl, int kind, TriHost& F, TriHost& B);
+// Complete banded Cholesky factors (L and L^T bands) of every local A_p.  Throws Fail.
+void build_band_cholesky(const ras_plan* pl, BandHost& H);
 // Dictionary-coded values + base/offset columns of R, L, diag; false = not compressible.
 bool build_zformat(ras_plan* pl);
 }  // namespace ras

@@ -309,6 +309,46 @@ static ras_status upload_factors(ras_ctx* c) {
   return RAS_OK;
 }
 
+// NEXT f1 setup: complete banded Cholesky factors on the host, uploaded once
+static ras_status upload_band(ras_ctx* c) {
+  const ras_plan* pl = c->plan;
+  for (const auto& S : pl->subs)
+    if (S.nrows_pad > kBandMaxRows)
+      return set_err(c, RAS_EINVAL, "cholesky local solve: subdomain " + std::to_string(S.p) + " has " +
+                                        std::to_string(S.nrows_pad) + " rows (max " + std::to_string(kBandMaxRows) + ")");
+  int64_t total = 0;  // band entries, checked before factoring
+  for (const auto& S : pl->subs) {
+    int64_t b = 0;
+    for (int64_t i = 0; i < S.nrows_pad; ++i)
+      for (int64_t e = pl->Ap_ptr[S.row_off + i]; e < pl->Ap_ptr[S.row_off + i + 1]; ++e)
+        b = std::max<int64_t>(b, std::llabs(i - (int64_t)pl->Ap_col[e]));
+    total += S.nrows_pad * (b + 1);
+  }
+  if ((double)total * 16.0 > 16e9) return set_err(c, RAS_EINVAL, "cholesky local solve: bands exceed 16 GB");
+  BandHost H;
+  try {
+    build_band_cholesky(pl, H);
+  } catch (const Fail& f) {
+    return set_err(c, f.st, f.msg);
+  }
+  double *L, *U;
+  int64_t* off;
+  int32_t* bw;
+  TRY(upload(c, &L, H.L, 1));
+  TRY(upload(c, &U, H.U, 1));
+  TRY(upload(c, &off, H.off));
+  TRY(upload(c, &bw, H.bw));
+  c->band = BandDev{L, U, off, bw};
+  int nmax = 0;
+  for (const auto& S : pl->subs) nmax = std::max<int>(nmax, (int)S.nrows_pad);
+  c->band_smem = (size_t)nmax * sizeof(double);
+  RAS_CUDA(c, cudaFuncSetAttribute((const void*)k_band_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)c->band_smem));
+  c->chol = true;
+  c->mb.band = 16.0 * (double)H.off.back() + (double)pl->rows_local * 12.0 + (double)pl->n_own * 16.0;
+  return RAS_OK;
+}
+
 static ras_status upload_plan(ras_ctx* c) {
   ras_plan* pl = c->plan;
   c->rows_pad = pl->rows_pad;
@@ -498,6 +538,10 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
   } else {
     // nothing to exchange: single rank
   }
+  if (ras_plan_set_robin(c->plan, c->opt.robin) != RAS_OK)
+    return set_err(c, RAS_EINVAL, "robin (ORAS transmission parameter) must be in [0, 1)");
+  if (c->opt.robin > 0.0 && overlap < 1)
+    return set_err(c, RAS_EINVAL, "robin > 0 (ORAS) needs overlap >= 1: without overlap the iteration diverges (R30)");
   s = ras_plan_finalize(c->plan);
   if (s != RAS_OK) return set_err(c, s, tls_error());
   TRY(upload_plan(c));
@@ -513,6 +557,8 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
   }
   if (c->opt.local_solver == RAS_LS_IC0_PCG || c->opt.local_solver == RAS_LS_ILU0_PCG) {
     TRY(upload_factors(c));
+  } else if (c->opt.local_solver == RAS_LS_CHOLESKY) {
+    TRY(upload_band(c));
   } else if (c->opt.local_solver != RAS_LS_JACOBI_PCG && c->opt.local_solver != RAS_LS_EXACT_PCG) {
     return set_err(c, RAS_EINVAL, "unknown local solver");
   }
@@ -814,6 +860,12 @@ static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m,
 ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol, bool exact) {
   const unsigned g = R.ntiles;
   const int64_t tb = R.tile_base;
+  if (c->chol) {  // NEXT f1: direct solve, one CTA per subdomain (+ prolongation)
+    g_launch_smem = c->band_smem;
+    KL(s, K_BAND, R.lp < 0 ? (unsigned)c->nl : 1u, kNT_BAND, k_band_chol, R.lp < 0 ? 0 : R.lp, c->SS, c->band,
+       (const double*)c->d_r, (const int32_t*)c->d_own_slot, c->d_x, c->S, C);
+    return RAS_OK;
+  }
   if (c->small) return enq_small_pcg(c, s, R, C, m, inner_tol);
   if (c->path == RAS_PCG_RESIDENT && R.lp < 0) return enq_resident_pcg(c, s, C, m, inner_tol);
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
@@ -916,7 +968,7 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 
 // a4
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
-  if (c->small) return RAS_OK;  // k_small_pcg prolongs in the same kernel
+  if (c->small || c->chol) return RAS_OK;  // k_small_pcg / k_band_chol prolong in the same kernel
   if (c->path == RAS_PCG_RESIDENT && R.lp < 0) return RAS_OK;  // so does k_resident_pcg
   KL(s, K_PROL, R.ntiles, kNT_STREAM, k_prolong, R.tile_base, tiles_next(c), (const int32_t*)c->d_own_slot, (const double*)c->d_d,
      c->d_x, c->S, C);
@@ -1181,7 +1233,11 @@ static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   c->st.num_subdomains = c->plan->P;
   c->st.world = c->world;
   c->st.local_subdomains = c->nl;
-  c->st.pcg_path = c->ic ? RAS_PCG_TILED : c->small ? RAS_PCG_BLOCK : mode == RAS_SYNC ? c->path : RAS_PCG_TILED;
+  c->st.pcg_path = c->chol ? RAS_PCG_BLOCK
+                  : c->ic  ? RAS_PCG_TILED
+                  : c->small ? RAS_PCG_BLOCK
+                  : mode == RAS_SYNC ? c->path
+                                     : RAS_PCG_TILED;
   c->st.rows_local = c->plan->rows_local;
   c->st.halo_values = c->n_halo;
   c->st.kernel_launches = c->launches;
@@ -1193,7 +1249,7 @@ static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   double frac_iters = 0.0;
   const double rows = (double)std::max<int64_t>(c->plan->rows_local, 1);
   for (int i = 0; i < c->nl; ++i) frac_iters += (double)it[i] * (double)c->plan->subs[i].nrows / rows;
-  c->st.model_bytes = (double)c->st.sweeps * (c->mb.residual + c->mb.prolong + c->mb.pack) +
+  c->st.model_bytes = (double)c->st.sweeps * (c->mb.residual + c->mb.prolong + c->mb.pack + (c->chol ? c->mb.band : 0.0)) +
                       frac_iters * (c->mb.spmv_dot + c->mb.update_dot + c->mb.pupdate +
                                     (c->ic ? 2.0 * c->mb.trsv + c->mb.zdot : 0.0));
 }
@@ -1256,10 +1312,10 @@ ras_status ras_kernel_times(const ras_ctx* c, ras_kernel_time_t* out, int32_t ma
   if (!c || !n_out) return RAS_EINVAL;
   const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", c->ic ? "k_update_dot<ic>" : "k_update_dot",
                                  c->ic ? "k_pupdate_z" : "k_pupdate", "k_prolong", "k_pack", "control",
-                                 "k_trsv", "k_zdot", "k_small_pcg", "k_resident_pcg"};
+                                 "k_trsv", "k_zdot", "k_small_pcg", "k_resident_pcg", "k_band_chol"};
   const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate,
                                   c->mb.prolong,  c->mb.pack,     0.0,              c->mb.trsv,
-                                  c->mb.zdot,     c->mb.local_solve, c->mb.local_solve};
+                                  c->mb.zdot,     c->mb.local_solve, c->mb.local_solve, c->mb.band};
   int n = 0;
   for (int k = 0; k < K_NKINDS && n < max_entries; ++k) {
     if (!out) break;

@@ -55,7 +55,7 @@ def nccl_unique_id() -> bytes:
 
 
 _SOLVERS = {"jacobi": F.RAS_LS_JACOBI_PCG, "ic0": F.RAS_LS_IC0_PCG, "ilu0": F.RAS_LS_ILU0_PCG,
-            "exact": F.RAS_LS_EXACT_PCG}
+            "exact": F.RAS_LS_EXACT_PCG, "cholesky": F.RAS_LS_CHOLESKY}
 _DETECTORS = {"central": F.RAS_DET_CENTRAL, "decentral": F.RAS_DET_DECENTRAL}
 
 
@@ -64,19 +64,21 @@ _PATHS = {"auto": F.RAS_PCG_AUTO, "tiled": F.RAS_PCG_TILED, "block": F.RAS_PCG_B
 
 
 def options(local_solver="jacobi", inner_iters=20, inner_tol=0.0, detector="decentral", fuse_p=False,
-            plain=False, stage=False, tiled=False, path="auto", **kw) -> F.RasOptions:
+            plain=False, stage=False, tiled=False, path="auto", robin=0.0, **kw) -> F.RasOptions:
     """ras_options.  Kernel-variant switches (same recurrences, summation order aside):
     fuse_p: fuse the PCG p update into the next SpMV (tiled path);
     plain: force FP64/int32 SELL instead of the default lane-packed SELL-Z;
     stage: shared-memory staging of p in the tiled SpMV;
     path: local-PCG execution path, "auto" | "tiled" | "block" | "resident" (ras_pcg_path);
-    tiled: shorthand for path="tiled"."""
+    tiled: shorthand for path="tiled";
+    robin: ORAS transmission parameter in [0, 1) (0 = RAS; ras_options.robin, R30)."""
     o = F.RasOptions()
     _check(F.lib().ras_options_default(C.byref(o)))
     o.fuse_p = 1 if fuse_p else 0
     o.matrix_format = 1 if plain else 0
     o.stage_p = 1 if stage else 0
     o.pcg_path = _PATHS["tiled" if tiled else path]
+    o.robin = float(robin)
     o.local_solver = _SOLVERS[local_solver] if isinstance(local_solver, str) else int(local_solver)
     o.inner_iters = int(inner_iters)
     o.inner_tol = float(inner_tol)
