@@ -127,7 +127,10 @@ typedef struct {
   int32_t matrix_format;         /* 0: lane-packed SELL-Z when the matrix allows it; 1: plain SELL-32 */
   int32_t stage_p;               /* 1: stage p in shared memory in the tiled SpMV */
   ras_pcg_path pcg_path;         /* default RAS_PCG_AUTO */
-  int32_t reserved_i[3];
+  int32_t async_persistent;      /* async on one GPU with BLOCK-sized subdomains: 1 (default) = one
+                                    persistent cooperative kernel, every CTA iterating its subdomains
+                                    with no host involvement; 0 = one CUDA stream per subdomain */
+  int32_t reserved_i[2];
   /* Optimized RAS (NEXT f3, PAPER P760-763, R30): Robin-type transmission condition in algebraic
    * form -- the local solve uses A~_p = A_p - robin * diag(sum_{j not in Omega_p} |a_ij|) (rows
    * coupled outside Omega_p); the residual keeps A.  0 = RAS (Dirichlet truncation, default);

@@ -85,6 +85,8 @@ struct AsyncRt {
   uint32_t* d_put_ticket = nullptr;
   uint8_t* d_scripted = nullptr;
   int64_t scripted_n = 0;
+  int32_t* h_kill = nullptr;      // mapped pinned: host watchdog -> persistent kernel
+  int32_t* h_kill_dev = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -212,6 +214,103 @@ static __global__ void k_put(int lp, int64_t e0, int64_t e1, const int32_t* __re
 static __global__ void k_mirror_stops(int nl, const int32_t* lstop, volatile int32_t* h) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nl) h[i] = lstop[i];
+}
+
+// ---------------------------------------------------------------------------
+// Persistent asynchronous RAS on one GPU (BLOCK regime: every |Omega_p| fits a
+// CTA's shared memory; the paper's 4096-unknown subdomains, NEXT f2).  One
+// cooperative launch: CTA g owns subdomains g, g + G, ... and loops over them
+// with no barrier and no host involvement -- each update reads the owner
+// values as they stand in L2 ("latest data", P163-176; ld.global.cg, 8-byte
+// stores are atomic), computes r~_p and its Eq. 2 flag, takes one detection
+// step (the same det_step protocol as the stream-based mode), runs the whole
+// local PCG in shared memory (block_pcg) and stores x[S_p] += d.  A CTA exits
+// when all its subdomains stopped (the detection protocol stops all of them)
+// or the host watchdog raises the kill word.
+// ---------------------------------------------------------------------------
+template <int RPT, int WR, int WL, bool Z>
+static __global__ void __launch_bounds__(kNT_SMALL, 1)
+    k_async_persistent(int nl, SmallSubs SS, Sell Rm, Sell L, Diag D, const double* __restrict__ b,
+                       const int32_t* __restrict__ own_slot, double* x, DetDev det, Scal S, double tol,
+                       int64_t max_iters, int32_t m, double inner_tol, int32_t* lstop, volatile int32_t* h_lstop,
+                       int64_t* updates, int32_t* noconv, const volatile int32_t* kill) {
+  extern __shared__ double smem[];
+  __shared__ double red[3][kNT_SMALL / 32];
+  __shared__ int s_stop;
+  const double* tabR = Rm.table;
+  for (;;) {
+    bool any = false;
+    for (int lp = blockIdx.x; lp < nl; lp += gridDim.x) {
+      if (lstop[lp]) continue;  // written only by this CTA
+      any = true;
+      const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+      double* sp = smem;
+      double* sr = smem + n;
+      double* sd = smem + 2 * n;
+      // a1 + a2: r~ = b~ - [A_p | B_p] x (owner storage read through L2), z = D^-1 r
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
+        const int64_t row = (int64_t)r0 + i;
+        const double ax = resident_row<WR, Z>(Rm, row, tabR, [&](int32_t c) { return __ldcg(&x[c]); });
+        const double ri = __ldg(&b[row]) - ax;
+        const double zi = __drcp_rn(diag_at<Z>(D, row)) * ri;
+        sr[i] = ri;
+        sp[i] = zi;
+        sd[i] = 0.0;
+        v[0] += ri * zi;
+        v[1] += ri * ri;
+        v[2] += __ldg(&own_slot[row]) >= 0 ? ri * ri : 0.0;
+      }
+      block_allsum<3>(v, red);
+      // a6: Eq. 2 flag + one detection step (P331-357)
+      if (threadIdx.x == 0) {
+        S.rt2[lp] = v[1];
+        S.own2[lp] = v[2];
+        const int64_t u = ++updates[lp];
+        const int c = local_flag(det, S, lp, tol);
+        const int32_t* in = det.boards[det.my_rank];
+        (void)ld_acquire_sys(in + det.gid[lp]);
+        int stop = det_step(det, lp, c, in, det.boards);
+        if (!stop && u > max_iters) {
+          noconv[lp] = 1;
+          stop = 1;
+        }
+        if (!stop && *kill) stop = 1;
+        if (stop) {
+          updates[lp] = u - 1;  // this sweep performs no update
+          lstop[lp] = 1;
+          h_lstop[lp] = 1;
+        }
+        s_stop = stop;
+      }
+      __syncthreads();
+      if (s_stop) continue;
+      // a3: the whole local PCG in shared memory; a4: x[S_p] += d
+      const int its = v[0] != 0.0 ? block_pcg<RPT, WL, Z>(L, D, r0, n, sp, sr, sd, v[0], v[1], m, inner_tol, red) : 0;
+      if (its > 0)
+        for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
+          const int32_t sl = __ldg(&own_slot[r0 + i]);
+          if (sl >= 0) __stcg(&x[sl], __ldcg(&x[sl]) + sd[i]);
+        }
+      if (threadIdx.x == 0) S.inner_total[lp] += its;
+      __syncthreads();
+    }
+    if (!any) break;
+  }
+}
+
+static const void* async_persistent_kernel(int rpt, bool z, int wr, int wl) {
+#define RAS_AP(RPT)                                                                                        \
+  if (!z) return (const void*)k_async_persistent<RPT, 0, 0, false>;                                        \
+  if (wr == 4) return wl == 4 ? (const void*)k_async_persistent<RPT, 4, 4, true>                           \
+                              : (const void*)k_async_persistent<RPT, 4, 8, true>;                          \
+  return wl == 4 ? (const void*)k_async_persistent<RPT, 8, 4, true> : (const void*)k_async_persistent<RPT, 8, 8, true>;
+  if (rpt <= 4) {
+    RAS_AP(4)
+  } else {
+    RAS_AP(9)
+  }
+#undef RAS_AP
 }
 
 // ---------------------------------------------------------------------------
@@ -385,6 +484,9 @@ ras_status async_setup(ras_ctx* c) {
   RAS_CUDA(c, cudaHostAlloc((void**)&A->h_lstop, std::max(nl, 1) * 4, cudaHostAllocMapped));
   RAS_CUDA(c, cudaHostGetDevicePointer((void**)&A->h_lstop_dev, A->h_lstop, 0));
   RAS_CUDA(c, cudaHostAlloc((void**)&A->h_active, std::max(nl, 1) * 4, cudaHostAllocDefault));
+  RAS_CUDA(c, cudaHostAlloc((void**)&A->h_kill, 4, cudaHostAllocMapped));
+  RAS_CUDA(c, cudaHostGetDevicePointer((void**)&A->h_kill_dev, A->h_kill, 0));
+  *A->h_kill = 0;
   // put lists: entries of the send lists whose source slot belongs to local p
   std::vector<int64_t> n_own_all(W, 0);
   n_own_all[c->rank] = c->n_own;
@@ -433,6 +535,7 @@ void async_free(ras_ctx* c) {
   for (void* p : A->opened) cudaIpcCloseMemHandle(p);
   if (A->h_lstop) cudaFreeHost(A->h_lstop);
   if (A->h_active) cudaFreeHost(A->h_active);
+  if (A->h_kill) cudaFreeHost(A->h_kill);
   delete A;
   c->async = nullptr;
 }
@@ -529,6 +632,67 @@ static ras_status run_async_loop(ras_ctx* c, double tol, int64_t max_iters, int 
   return st;
 }
 
+// persistent single-GPU async mode (BLOCK regime): one cooperative launch, the
+// host only watches the wall clock
+static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol,
+                                       bool* timeout) {
+  AsyncRt* A = c->async;
+  const int nl = c->nl;
+  const void* fn = async_persistent_kernel((c->small_nmax + kNT_SMALL - 1) / kNT_SMALL, c->z, c->zwR, c->zwL);
+  const size_t smem = (size_t)3 * c->small_nmax * sizeof(double);
+  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0, sms = 0;
+  RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_SMALL, smem));
+  RAS_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  if (per_sm < 1) return set_err(c, RAS_ESTATE, "persistent async kernel does not fit an SM");
+  int G = std::min(nl, per_sm * sms);
+  *A->h_kill = 0;
+  Ctl C{nullptr, 0};
+  (void)C;
+  int nl_ = nl;
+  Sell Rm = c->R, L = c->L;
+  Diag D = c->D;
+  const double* b = c->d_b;
+  const int32_t* own = c->d_own_slot;
+  double* x = c->d_x;
+  DetDev det = A->det;
+  Scal S = c->S;
+  int64_t mi = max_iters;
+  int32_t mm = m;
+  int32_t* lstop = A->d_lstop;
+  volatile int32_t* hl = A->h_lstop_dev;
+  int64_t* up = A->d_updates;
+  int32_t* nc = A->d_noconv;
+  const volatile int32_t* kill = A->h_kill_dev;
+  SmallSubs SS = c->SS;
+  void* args[] = {&nl_, &SS, &Rm, &L, &D, &b, &own, &x, &det, &S, &tol, &mi, &mm, &inner_tol, &lstop, &hl, &up, &nc, &kill};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3(kNT_SMALL);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RAS_CUDA(c, cudaLaunchKernelExC(&cfg, fn, args));
+  c->launches += 1;
+  const double t0 = now_s();
+  *timeout = false;
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(c->stream);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) return cuda_err(c, e, "persistent async kernel");
+    if (!*timeout && now_s() - t0 > c->opt.async_timeout_s) {
+      *timeout = true;
+      *(volatile int32_t*)A->h_kill = 1;  // every CTA stops at its next update
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  return RAS_OK;
+}
+
 // scripted lock-step mode (single rank): deterministic detector schedule
 static ras_status run_scripted(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol) {
   AsyncRt* A = c->async;
@@ -588,6 +752,8 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
     TRY(reset_detection(c));
     if (c->opt.scripted_flags) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
+    } else if (c->world == 1 && c->small && c->opt.async_persistent != 0) {
+      st = run_async_persistent(c, tol, max_iters, m, inner_tol, &timeout);
     } else {
       st = run_async_loop(c, tol, max_iters, m, inner_tol, exact, &timeout);
     }

@@ -711,32 +711,15 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[kNT_S
   __syncthreads();
 }
 
-// Runs after k_residual<JAC>/k_finish<F_RES_JAC> (r, p = z, rho, rt2, active set).
+// The whole Jacobi-PCG solve of one subdomain by one CTA (kNT_SMALL threads):
+// rows [r0, r0 + n) of the row space, p (= z_0), r (= r~) and d in shared
+// memory (sp, sr, sd), q in registers; returns the iterations performed.
+// Same recurrences as the tiled path; only summation order differs.
 template <int RPT, int W, bool Z>
-static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, SmallSubs SS, Sell L, Diag D,
-                                                                   const double* __restrict__ r_in,
-                                                                   const double* __restrict__ p_in,
-                                                                   const int32_t* __restrict__ own_slot,
-                                                                   double* __restrict__ x, Scal S, Ctl C, int32_t m,
-                                                                   double inner_tol) {
-  extern __shared__ double smem[];
-  __shared__ double red[2][kNT_SMALL / 32];
-  pdl_start();
-  const int lp = lp_base + blockIdx.x;
-  if (stopped(C, lp) || !S.active[lp]) return;  // uniform per CTA
-  const int r0 = SS.row_off[lp], n = SS.nrows[lp];
-  double* sp = smem;           // p
-  double* sr = smem + n;       // r
-  double* sd = smem + 2 * n;   // d (correction)
-  for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
-    sp[i] = __ldg(&p_in[r0 + i]);
-    sr[i] = __ldg(&r_in[r0 + i]);
-    sd[i] = 0.0;
-  }
-  double rho = S.rho[lp];
-  const double rt2 = S.rt2[lp];
+__device__ __forceinline__ int block_pcg(const Sell& L, const Diag& D, int r0, int n, double* sp, double* sr,
+                                         double* sd, double rho, double rt2, int m, double inner_tol,
+                                         double (*red)[kNT_SMALL / 32]) {
   int its = 0;
-  __syncthreads();
   for (;;) {
     // pass 1: q = A_p p, sigma = p.q
     double q[RPT];
@@ -778,6 +761,33 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
       sp[i] = __drcp_rn(diag_at<Z>(D, (int64_t)r0 + i)) * sr[i] + beta * sp[i];
     __syncthreads();
   }
+  return its;
+}
+
+// Runs after k_residual<JAC>/k_finish<F_RES_JAC> (r, p = z, rho, rt2, active set).
+template <int RPT, int W, bool Z>
+static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, SmallSubs SS, Sell L, Diag D,
+                                                                   const double* __restrict__ r_in,
+                                                                   const double* __restrict__ p_in,
+                                                                   const int32_t* __restrict__ own_slot,
+                                                                   double* __restrict__ x, Scal S, Ctl C, int32_t m,
+                                                                   double inner_tol) {
+  extern __shared__ double smem[];
+  __shared__ double red[2][kNT_SMALL / 32];
+  pdl_start();
+  const int lp = lp_base + blockIdx.x;
+  if (stopped(C, lp) || !S.active[lp]) return;  // uniform per CTA
+  const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+  double* sp = smem;           // p
+  double* sr = smem + n;       // r
+  double* sd = smem + 2 * n;   // d (correction)
+  for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
+    sp[i] = __ldg(&p_in[r0 + i]);
+    sr[i] = __ldg(&r_in[r0 + i]);
+    sd[i] = 0.0;
+  }
+  __syncthreads();
+  const int its = block_pcg<RPT, W, Z>(L, D, r0, n, sp, sr, sd, S.rho[lp], S.rt2[lp], m, inner_tol, red);
   // a4: restricted prolongation of the owned rows
   if (its > 0)
     for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
@@ -795,18 +805,22 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
 // NEXT f1: direct local solve (PAPER §3.3.1, P311-318: factor once, two
 // triangular solves per local solve) with the complete banded Cholesky factor
 // computed on the host (factor.cpp).  One CTA per subdomain: y = L^-1 r~ then
-// d = L^-T y, in 32-row blocks -- the band contribution of the rows already
-// solved is a warp-parallel dot product per row (coalesced along the band
-// row), the 32 x 32 diagonal triangle a sequential warp-shuffle solve -- with
-// y / d of the whole subdomain in shared memory, then the restricted
-// prolongation.  Runs after k_residual / k_finish (r~ in the row space, active).
+// d = L^-T y in 32-row blocks, software-pipelined: while warp 0 finishes block
+// k (the 32 x 32 coupling to block k-1 and the diagonal triangle, both already
+// staged in shared memory, then a warp-shuffle forward substitution with the
+// host's reciprocal pivots), warps 1..7 compute block k+1's far band sums
+// (rows already solved before block k, coalesced along the band rows) and stage
+// its coupling / triangle blocks.  One CTA barrier per block.  y / d of the whole
+// subdomain live in shared memory; then the restricted prolongation.
+// Runs after k_residual / k_finish (r~ in the row space, active set).
 // ---------------------------------------------------------------------------
-constexpr int kNT_BAND = 256;
+constexpr int kNT_BAND = 512;
 constexpr int kBandMaxRows = 12288;  // y / d of one subdomain in shared memory (96 KB)
 
 struct BandDev {
   const double* L;     // lower band, row-major, bw + 1 slots per row (slot j - i + bw)
   const double* U;     // upper band = L^T, row-major (slot j - i)
+  const double* dinv;  // row space: 1 / L(i, i)
   const int64_t* off;  // per local subdomain offset into L / U
   const int32_t* bw;   // per local subdomain bandwidth
 };
@@ -815,69 +829,120 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
                                                                  const double* __restrict__ r_in,
                                                                  const int32_t* __restrict__ own_slot,
                                                                  double* __restrict__ x, Scal S, Ctl C) {
-  extern __shared__ double sy[];  // y, overwritten by d from the last block down
-  __shared__ double blk[32][33];
-  __shared__ double sv[32];
+  extern __shared__ double sy[];        // y, overwritten by d from the last block down
+  __shared__ double blkN[2][32][33];    // coupling of a block's rows to the neighbouring block
+  __shared__ double blkT[2][32][33];    // the block's diagonal triangle
+  __shared__ double sfar[2][32];        // rhs minus the far band sums
+  __shared__ double sdi[2][32];         // reciprocal pivots of the block
   pdl_start();
   const int lp = lp_base + blockIdx.x;
   if (stopped(C, lp) || !S.active[lp]) return;
-  const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+  const int r0 = SS.row_off[lp], n = SS.nrows[lp], nb = n / 32;
   const int b = B.bw[lp];
   const int64_t w = b + 1;
   const double* Lp = B.L + B.off[lp];
   const double* Up = B.U + B.off[lp];
+  const double* dip = B.dinv + r0;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  constexpr int RW = 32 / (kNT_BAND / 32);  // block rows per warp
-  // forward: L y = r~
-  for (int i0 = 0; i0 < n; i0 += 32) {
-#pragma unroll
-    for (int rr = 0; rr < RW; ++rr) {
-      const int l = wp * RW + rr, i = i0 + l;
+  // ---- forward: L y = r~ ----
+  // stage block kb (rows i0..i0+31): far sums over columns < i0 - 32, the
+  // coupling to block kb-1 and the triangle (helper warps / all warps)
+  // t0 / nt: this thread's rank among the staging threads and their count
+  auto stage_f = [&](int kb, int buf, int t0, int nt) {
+    const int i0 = kb * 32;
+    // coupling to block kb-1 and the triangle: 2 x 32 x 32 independent loads
+    for (int t = t0; t < 2048; t += nt) {
+      const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
+      if (t < 1024) {
+        const int jn = i0 - 32 + m;
+        blkN[buf][l][m] = (kb > 0 && i - jn <= b) ? __ldg(&Lp[(int64_t)i * w + (jn - i + b)]) : 0.0;
+      } else {
+        const int jt = i0 + m;
+        blkT[buf][l][m] = (jt < i && i - jt <= b) ? __ldg(&Lp[(int64_t)i * w + (jt - i + b)]) : 0.0;
+      }
+    }
+    // far band sums (columns before block kb-1), one warp per row
+    for (int l = t0 >> 5; l < 32; l += nt >> 5) {
+      const int i = i0 + l;
       double acc = 0.0;
-      for (int j = max(0, i - b) + lane; j < i0; j += 32) acc += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
+#pragma unroll 4
+      for (int j = max(0, i - b) + lane; j < i0 - 32; j += 32) acc += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
       acc = warp_sum(acc);
-      if (lane == 0) sv[l] = __ldg(&r_in[r0 + i]) - acc;
+      if (lane == 0) {
+        sfar[buf][l] = __ldg(&r_in[r0 + i]) - acc;
+        sdi[buf][l] = __ldg(&dip[i]);
+      }
     }
-    for (int t = threadIdx.x; t < 32 * 32; t += kNT_BAND) {
-      const int l = t >> 5, m = t & 31;
-      blk[l][m] = (m <= l && l - m <= b) ? __ldg(&Lp[(int64_t)(i0 + l) * w + (m - l + b)]) : 0.0;
-    }
-    __syncthreads();
+  };
+  stage_f(0, 0, threadIdx.x, kNT_BAND);
+  __syncthreads();
+  for (int kb = 0; kb < nb; ++kb) {
+    const int cur = kb & 1;
     if (wp == 0) {
-      double s = sv[lane], yv = 0.0;
+      const int i0 = kb * 32;
+      double s = sfar[cur][lane];
+      if (kb > 0) {
+#pragma unroll 8
+        for (int m = 0; m < 32; ++m) s -= blkN[cur][lane][m] * sy[i0 - 32 + m];
+      }
+      double yv = 0.0;
       for (int m = 0; m < 32; ++m) {
-        const double ym = __shfl_sync(0xffffffffu, s, m) / blk[m][m];
+        const double ym = __shfl_sync(0xffffffffu, s, m) * sdi[cur][m];
         if (lane == m) yv = ym;
-        if (lane > m) s -= blk[lane][m] * ym;
+        if (lane > m) s -= blkT[cur][lane][m] * ym;
       }
       sy[i0 + lane] = yv;
+    } else if (kb + 1 < nb) {
+      stage_f(kb + 1, cur ^ 1, threadIdx.x - 32, kNT_BAND - 32);
     }
     __syncthreads();
   }
-  // backward: L^T d = y (rows >= i0 + 32 of sy already hold d)
-  for (int i0 = n - 32; i0 >= 0; i0 -= 32) {
-#pragma unroll
-    for (int rr = 0; rr < RW; ++rr) {
-      const int l = wp * RW + rr, i = i0 + l;
+  // ---- backward: L^T d = y (block kb's rows of sy hold y until it is solved) ----
+  auto stage_b = [&](int kb, int buf, int t0, int nt) {
+    const int i0 = kb * 32;
+    for (int t = t0; t < 2048; t += nt) {
+      const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
+      if (t < 1024) {
+        const int jn = i0 + 32 + m;  // coupling column in block kb+1
+        blkN[buf][l][m] = (kb + 1 < nb && jn - i <= b) ? __ldg(&Up[(int64_t)i * w + (jn - i)]) : 0.0;
+      } else {
+        const int jt = i0 + m;
+        blkT[buf][l][m] = (jt > i && jt - i <= b) ? __ldg(&Up[(int64_t)i * w + (jt - i)]) : 0.0;
+      }
+    }
+    for (int l = t0 >> 5; l < 32; l += nt >> 5) {
+      const int i = i0 + l;
       double acc = 0.0;
       const int j1 = min(n - 1, i + b);
-      for (int j = i0 + 32 + lane; j <= j1; j += 32) acc += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
+#pragma unroll 4
+      for (int j = i0 + 64 + lane; j <= j1; j += 32) acc += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
       acc = warp_sum(acc);
-      if (lane == 0) sv[l] = sy[i] - acc;
+      if (lane == 0) {
+        sfar[buf][l] = sy[i] - acc;
+        sdi[buf][l] = __ldg(&dip[i]);
+      }
     }
-    for (int t = threadIdx.x; t < 32 * 32; t += kNT_BAND) {
-      const int l = t >> 5, m = t & 31;
-      blk[l][m] = (m >= l && m - l <= b) ? __ldg(&Up[(int64_t)(i0 + l) * w + (m - l)]) : 0.0;
-    }
-    __syncthreads();
+  };
+  stage_b(nb - 1, (nb - 1) & 1, threadIdx.x, kNT_BAND);
+  __syncthreads();
+  for (int kb = nb - 1; kb >= 0; --kb) {
+    const int cur = kb & 1;
     if (wp == 0) {
-      double s = sv[lane], dv = 0.0;
+      const int i0 = kb * 32;
+      double s = sfar[cur][lane];
+      if (kb + 1 < nb) {
+#pragma unroll 8
+        for (int m = 0; m < 32; ++m) s -= blkN[cur][lane][m] * sy[i0 + 32 + m];
+      }
+      double dv = 0.0;
       for (int m = 31; m >= 0; --m) {
-        const double dm = __shfl_sync(0xffffffffu, s, m) / blk[m][m];
+        const double dm = __shfl_sync(0xffffffffu, s, m) * sdi[cur][m];
         if (lane == m) dv = dm;
-        if (lane < m) s -= blk[lane][m] * dm;
+        if (lane < m) s -= blkT[cur][lane][m] * dm;
       }
       sy[i0 + lane] = dv;
+    } else if (kb > 0) {
+      stage_b(kb - 1, cur ^ 1, threadIdx.x - 32, kNT_BAND - 32);
     }
     __syncthreads();
   }

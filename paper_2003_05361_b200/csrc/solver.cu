@@ -331,14 +331,21 @@ static ras_status upload_band(ras_ctx* c) {
   } catch (const Fail& f) {
     return set_err(c, f.st, f.msg);
   }
-  double *L, *U;
+  double *L, *U, *dinv;
   int64_t* off;
   int32_t* bw;
+  std::vector<double> di((size_t)c->rows_pad, 1.0);  // reciprocal pivots, row space
+  for (size_t lp = 0; lp < pl->subs.size(); ++lp) {
+    const auto& S = pl->subs[lp];
+    const int64_t wdt = H.bw[lp] + 1;
+    for (int64_t i = 0; i < S.nrows_pad; ++i) di[S.row_off + i] = 1.0 / H.L[H.off[lp] + i * wdt + H.bw[lp]];
+  }
   TRY(upload(c, &L, H.L, 1));
   TRY(upload(c, &U, H.U, 1));
+  TRY(upload(c, &dinv, di, 1));
   TRY(upload(c, &off, H.off));
   TRY(upload(c, &bw, H.bw));
-  c->band = BandDev{L, U, off, bw};
+  c->band = BandDev{L, U, dinv, off, bw};
   int nmax = 0;
   for (const auto& S : pl->subs) nmax = std::max<int>(nmax, (int)S.nrows_pad);
   c->band_smem = (size_t)nmax * sizeof(double);
@@ -1141,6 +1148,7 @@ ras_status ras_options_default(ras_options* o) {
   o->use_graphs = 1;
   o->poll_interval = 4;
   o->async_timeout_s = 1800.0;
+  o->async_persistent = 1;
   return RAS_OK;
 }
 

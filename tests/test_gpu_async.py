@@ -100,3 +100,22 @@ def test_async_single_subdomain_is_exact():
     xs = np.linalg.solve(A.to_scipy().toarray(), b)
     assert np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(xs)
     s.close()
+
+
+@pytest.mark.parametrize("persistent", [0, 1])
+@pytest.mark.parametrize("detector", ["central", "decentral"])
+def test_async_single_gpu_modes_converge(persistent, detector):
+    # BLOCK-sized subdomains on one GPU: the persistent cooperative kernel
+    # (default) and the stream-per-subdomain driver both reach tol and verify
+    N = 96
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 3)
+    owner = ri.voronoi_partition(N, N, 9, seed=6)
+    s = R.Solver(A, b, owner, 3, R.options("jacobi", 20, detector=detector, async_persistent=persistent))
+    st, x = s.solve(1e-8, 50000, "async")
+    stt = s.stats()
+    assert st == 0 and O.verify_global(A, x, b, 1e-8)[0], stt
+    assert stt["updates_min"] > 0 and stt["kernel_launches"] >= 1
+    if persistent:
+        assert stt["kernel_launches"] <= 10 * (stt["resumes"] + 1) + 20  # one persistent launch per attempt
+    s.close()

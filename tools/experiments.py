@@ -11,7 +11,11 @@ line per configuration, through the C ABI:
             pattern (heat map, volume, neighbours, propagation distance) and
             sweeps / time-to-solution, sync and async
 
-  python tools/experiments.py overlap|regime|detector|partition [--tol 1e-8] [--out FILE]
+  direct    NEXT f1 (P311-318): direct (banded Cholesky) vs Jacobi-PCG local solves in the
+            4096-unknowns-per-subdomain regime: sweeps, time-to-solution, sync and async
+  oras      NEXT f3 (P760-763, R30): sweeps / time-to-solution vs the Robin parameter
+
+  python tools/experiments.py overlap|regime|detector|partition|direct|oras [--tol 1e-8] [--out FILE]
 """
 from __future__ import annotations
 
@@ -30,14 +34,14 @@ import ras_inputs as ri  # noqa: E402
 
 
 def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decentral", max_iters=200000, reps=1,
-        owner=None):
+        owner=None, robin=0.0):
     import paper_2003_05361_b200 as R
 
     A = ri.laplace_2d(nx, ny)
     b = ri.rhs(nx * ny, 0)
     if owner is None:
         owner = R.partition_regular(nx, ny, 1, px, py, 1)
-    s = R.Solver(A, b, owner, gamma, R.options(solver, m, detector=detector))
+    s = R.Solver(A, b, owner, gamma, R.options(solver, m, detector=detector, robin=robin))
     out = []
     for _ in range(reps):
         t0 = time.perf_counter()
@@ -51,7 +55,7 @@ def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decen
                     "launches": d["kernel_launches"]})
     s.close()
     rec = {"grid": [nx, ny], "subdomains": px * py, "tiles": [px, py], "unknowns_per_subdomain": nx * ny // (px * py),
-           "overlap": gamma, "mode": mode, "tol": tol, "local_solver": f"{solver}-PCG m={m}", "detector": detector,
+           "overlap": gamma, "mode": mode, "tol": tol, "local_solver": solver if solver == "cholesky" else f"{solver}-PCG m={m}", "detector": detector,
            "runs": out}
     if reps > 1:
         t = [r["tts_s"] for r in out]
@@ -99,7 +103,7 @@ def partition_study(tol, reps, gamma=4, sub=64, Ps=(4, 16, 36, 64, 100)):
         px, py = R_factor(P)
         owners = {"regular1d": R.partition_regular(N, N, 1, 1, P, 1),
                   "regular2d": R.partition_regular(N, N, 1, px, py, 1),
-                  "graph": ri.voronoi_partition(N, N, P, seed=1)}
+                  "graph": voronoi_valid(N, P)}
         A = ri.laplace_2d(N)
         for name, owner in owners.items():
             C = R.Plan(A, None, owner, gamma).comm_pattern()
@@ -114,6 +118,16 @@ def partition_study(tol, reps, gamma=4, sub=64, Ps=(4, 16, 36, 64, 100)):
     return recs
 
 
+def voronoi_valid(N, P):
+    """First seed >= 1 whose Voronoi cells are all non-empty and 4-connected."""
+    for seed in range(1, 100):
+        try:
+            return ri.voronoi_partition(N, N, P, seed=seed)
+        except ValueError:
+            continue
+    raise RuntimeError("no valid Voronoi partition")
+
+
 def R_factor(P):
     """(px, py), px * py = P, closest to square with py >= px (R23)."""
     px = int(P ** 0.5)
@@ -124,7 +138,7 @@ def R_factor(P):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["overlap", "regime", "detector", "partition"])
+    ap.add_argument("which", choices=["overlap", "regime", "detector", "partition", "direct", "oras"])
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--out", default=None)
     ap.add_argument("--reps", type=int, default=3)
@@ -142,6 +156,16 @@ def main():
                 recs.append(run(64 * px, 64 * py, px, py, 16, mode, a.tol, reps=1 if mode == "sync" else a.reps))
     elif a.which == "partition":
         recs = partition_study(a.tol, a.reps)
+    elif a.which == "direct":
+        for (px, py) in ((4, 4), (8, 8), (12, 12)):
+            for solver in ("cholesky", "jacobi"):
+                for mode in ("sync", "async"):
+                    recs.append(run(64 * px, 64 * py, px, py, 4, mode, a.tol, solver=solver,
+                                    reps=1 if mode == "sync" else a.reps))
+    elif a.which == "oras":
+        for solver, m in (("cholesky", 1), ("jacobi", 20)):
+            for w in (0.0, 0.3, 0.5, 0.7, 0.8, 0.9):
+                recs.append({"robin": w, **run(256, 256, 4, 4, 2, "sync", a.tol, m=m, solver=solver, robin=w)})
     else:
         for det in ("central", "decentral"):
             recs.append(run(512, 512, 8, 8, 16, "async", a.tol, detector=det, reps=a.reps))
