@@ -87,6 +87,19 @@ struct AsyncRt {
   int64_t scripted_n = 0;
   int32_t* h_kill = nullptr;      // mapped pinned: host watchdog -> persistent kernel
   int32_t* h_kill_dev = nullptr;
+  int64_t* d_put_off = nullptr;       // device copies of put_off / put_peer_off (persistent kernel)
+  int32_t* d_put_peer_off = nullptr;
+};
+
+// NVLink put lists for the persistent kernel (device view of AsyncRt's lists)
+struct PutDev {
+  const int64_t* off;       // [nl + 1]
+  const int32_t* slot;      // owned slot of each entry
+  const int32_t* rank;      // destination rank
+  const int64_t* ridx;      // index in the destination's storage
+  double* const* peer_x;    // [world] storage base per rank (IPC-mapped)
+  const int32_t* peer_off;  // [nl + 1] into peers
+  const int32_t* peers;     // destination ranks per local subdomain
 };
 
 // ---------------------------------------------------------------------------
@@ -217,21 +230,23 @@ static __global__ void k_mirror_stops(int nl, const int32_t* lstop, volatile int
 }
 
 // ---------------------------------------------------------------------------
-// Persistent asynchronous RAS on one GPU (BLOCK regime: every |Omega_p| fits a
-// CTA's shared memory; the paper's 4096-unknown subdomains, NEXT f2).  One
-// cooperative launch: CTA g owns subdomains g, g + G, ... and loops over them
-// with no barrier and no host involvement -- each update reads the owner
-// values as they stand in L2 ("latest data", P163-176; ld.global.cg, 8-byte
-// stores are atomic), computes r~_p and its Eq. 2 flag, takes one detection
-// step (the same det_step protocol as the stream-based mode), runs the whole
-// local PCG in shared memory (block_pcg) and stores x[S_p] += d.  A CTA exits
-// when all its subdomains stopped (the detection protocol stops all of them)
-// or the host watchdog raises the kill word.
+// Persistent asynchronous RAS (BLOCK regime: every |Omega_p| fits a CTA's
+// shared memory; the paper's 4096-unknown subdomains, NEXT f2).  One
+// cooperative launch per GPU: CTA g owns subdomains g, g + G, ... and loops
+// over them with no barrier and no host involvement -- each update reads the
+// owner / halo values as they stand in L2 ("latest data", P163-176;
+// ld.global.cg, 8-byte stores are atomic; peers' NVLink stores land in this
+// GPU's memory), computes r~_p and its Eq. 2 flag, takes one detection step
+// (the same det_step protocol as the stream-based mode, boards shared across
+// GPUs), runs the whole local PCG in shared memory (block_pcg), stores
+// x[S_p] += d and puts the values other GPUs need into their halo storage.  A
+// CTA exits when all its subdomains stopped (the detection protocol stops all
+// of them) or the host watchdog raises the kill word.
 // ---------------------------------------------------------------------------
 template <int RPT, int WR, int WL, bool Z>
 static __global__ void __launch_bounds__(kNT_SMALL, 1)
     k_async_persistent(int nl, SmallSubs SS, Sell Rm, Sell L, Diag D, const double* __restrict__ b,
-                       const int32_t* __restrict__ own_slot, double* x, DetDev det, Scal S, double tol,
+                       const int32_t* __restrict__ own_slot, double* x, DetDev det, PutDev PD, Scal S, double tol,
                        int64_t max_iters, int32_t m, double inner_tol, int32_t* lstop, volatile int32_t* h_lstop,
                        int64_t* updates, int32_t* noconv, const volatile int32_t* kill) {
   extern __shared__ double smem[];
@@ -292,6 +307,21 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
           const int32_t sl = __ldg(&own_slot[r0 + i]);
           if (sl >= 0) __stcg(&x[sl], __ldcg(&x[sl]) + sd[i]);
         }
+      // a5 (multi-GPU): owner values other GPUs need, stored straight into their
+      // halo storage over NVLink; then a system-scope fence and a version bump in
+      // each destination's board (MPI_Put + flush analogue, P394-396)
+      const int64_t e0 = PD.off[lp], e1 = PD.off[lp + 1];
+      if (its > 0 && e1 > e0) {
+        __syncthreads();  // this CTA's x[S_p] stores before the reads below
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += kNT_SMALL)
+          PD.peer_x[PD.rank[e]][PD.ridx[e]] = __ldcg(&x[PD.slot[e]]);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence_system();
+          for (int k = PD.peer_off[lp]; k < PD.peer_off[lp + 1]; ++k)
+            atomicAdd_system(det.boards[PD.peers[k]] + 3 * det.P + det.gid[lp], 1);
+        }
+      }
       if (threadIdx.x == 0) S.inner_total[lp] += its;
       __syncthreads();
     }
@@ -523,6 +553,8 @@ ras_status async_setup(ras_ctx* c) {
   TRY(upload(c, &A->d_put_rank, pr, 1));
   TRY(upload(c, &A->d_put_ridx, pi, 1));
   TRY(upload(c, &A->d_put_peers, peers, 1));
+  TRY(upload(c, &A->d_put_off, A->put_off, 1));
+  TRY(upload(c, &A->d_put_peer_off, A->put_peer_off, 1));
   A->streams.resize(nl);
   for (auto& s : A->streams) RAS_CUDA(c, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   return RAS_OK;
@@ -632,8 +664,8 @@ static ras_status run_async_loop(ras_ctx* c, double tol, int64_t max_iters, int 
   return st;
 }
 
-// persistent single-GPU async mode (BLOCK regime): one cooperative launch, the
-// host only watches the wall clock
+// persistent async mode (BLOCK regime, any number of GPUs): one cooperative
+// launch per GPU, the host only watches the wall clock
 static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol,
                                        bool* timeout) {
   AsyncRt* A = c->async;
@@ -656,6 +688,7 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   const int32_t* own = c->d_own_slot;
   double* x = c->d_x;
   DetDev det = A->det;
+  PutDev PD{A->d_put_off, A->d_put_slot, A->d_put_rank, A->d_put_ridx, A->d_peer_x, A->d_put_peer_off, A->d_put_peers};
   Scal S = c->S;
   int64_t mi = max_iters;
   int32_t mm = m;
@@ -665,7 +698,7 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   int32_t* nc = A->d_noconv;
   const volatile int32_t* kill = A->h_kill_dev;
   SmallSubs SS = c->SS;
-  void* args[] = {&nl_, &SS, &Rm, &L, &D, &b, &own, &x, &det, &S, &tol, &mi, &mm, &inner_tol, &lstop, &hl, &up, &nc, &kill};
+  void* args[] = {&nl_, &SS, &Rm, &L, &D, &b, &own, &x, &det, &PD, &S, &tol, &mi, &mm, &inner_tol, &lstop, &hl, &up, &nc, &kill};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)G);
   cfg.blockDim = dim3(kNT_SMALL);
@@ -752,7 +785,7 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
     TRY(reset_detection(c));
     if (c->opt.scripted_flags) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
-    } else if (c->world == 1 && c->small && c->opt.async_persistent != 0) {
+    } else if (c->small && c->opt.async_persistent != 0) {
       st = run_async_persistent(c, tol, max_iters, m, inner_tol, &timeout);
     } else {
       st = run_async_loop(c, tol, max_iters, m, inner_tol, exact, &timeout);
