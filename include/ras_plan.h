@@ -95,6 +95,14 @@ ras_status ras_plan_storage_gids(const ras_plan* plan, int64_t* own_gids, int64_
  * is already finalized. */
 ras_status ras_plan_set_robin(ras_plan* plan, double robin);
 
+/* Complete banded Cholesky factor of local subdomain `local_idx`'s A_p (the direct local
+ * solve, RAS_LS_CHOLESKY, NEXT f1; PAPER P311-318), as the library computes it in
+ * ras_setup: on return *n = padded |Omega_p| rows, *bw = bandwidth b and, if L_out is not
+ * NULL, L_out[i * (b + 1) + (j - i + b)] = L(i, j) for j in [i - b, i] (row-major lower band;
+ * entries outside the matrix are 0).  Call with L_out = NULL to get the sizes.  Valid after
+ * ras_plan_finalize.  Errors: RAS_EINVAL (bad index / not finalized), RAS_ENOTSPD. */
+ras_status ras_plan_band_cholesky(const ras_plan* plan, int32_t local_idx, int64_t* n, int32_t* bw, double* L_out);
+
 /* Communication pattern of the partition (PAPER §3.3 "Partitioning", Fig. 2, P257-275):
  * counts[p * P + q] = number of values subdomain p receives from subdomain q per
  * exchange, i.e. |{g in (Omega_p \ S_p) u Gamma_p : owner(g) = q}| (R4), for this

@@ -108,6 +108,7 @@ SIGNATURES = [
     ("ras_plan_storage_gids", I32, [C.c_void_p, P(I64), P(I64)]),
     ("ras_plan_comm_pattern", I32, [C.c_void_p, P(I64)]),
     ("ras_plan_set_robin", I32, [C.c_void_p, F64]),
+    ("ras_plan_band_cholesky", I32, [C.c_void_p, I32, P(I64), P(I32), P(F64)]),
     ("ras_plan_free", None, [C.c_void_p]),
     ("ras_ctx_plan", I32, [C.c_void_p, P(C.c_void_p)]),
 ]

@@ -558,6 +558,23 @@ ras_status ras_plan_storage_gids(const ras_plan* pl, int64_t* own_gids, int64_t*
   return RAS_OK;
 }
 
+ras_status ras_plan_band_cholesky(const ras_plan* pl, int32_t lp, int64_t* n, int32_t* bw, double* L_out) {
+  if (!pl || !n || !bw || !pl->finalized || lp < 0 || lp >= (int32_t)pl->subs.size()) return RAS_EINVAL;
+  try {
+    ras_plan one = *pl;  // factor just this subdomain (copy of the plan's arrays; debug ABI)
+    one.subs.assign(1, pl->subs[lp]);
+    ras::BandHost H;
+    ras::build_band_cholesky(&one, H);
+    *n = pl->subs[lp].nrows_pad;
+    *bw = H.bw[0];
+    if (L_out) std::copy(H.L.begin(), H.L.end(), L_out);
+    return RAS_OK;
+  } catch (const Fail& f) {
+    ras::set_tls_error(f.msg);
+    return f.st;
+  }
+}
+
 ras_status ras_plan_set_robin(ras_plan* pl, double robin) {
   if (!pl || pl->finalized || !(robin >= 0.0 && robin < 1.0)) return RAS_EINVAL;
   pl->robin = robin;

@@ -134,6 +134,17 @@ class Plan:
     def finalize(self):
         _check(F.lib().ras_plan_finalize(self._h))
 
+    def band_cholesky(self, local_idx):
+        """ras_plan_band_cholesky: (L band (n, b+1), b) of local subdomain local_idx (after finalize)."""
+        n, bw = F.I64(), F.I32()
+        _check(F.lib().ras_plan_band_cholesky(self._h, int(local_idx), C.byref(n), C.byref(bw), None))
+        out = np.empty((n.value, bw.value + 1), dtype=np.float64)
+        _check(F.lib().ras_plan_band_cholesky(self._h, int(local_idx), C.byref(n), C.byref(bw), F.ptr(out, F.F64)))
+        return out, bw.value
+
+    def set_robin(self, robin):
+        _check(F.lib().ras_plan_set_robin(self._h, float(robin)))
+
     def comm_pattern(self) -> np.ndarray:
         """ras_plan_comm_pattern: P x P receive counts, row = receiver (Fig. 2), this rank's rows."""
         P = self.info()["num_subdomains"]

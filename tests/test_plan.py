@@ -211,3 +211,33 @@ def test_information_propagation_distance(P):
     assert d1 == P - 1
     assert d2_face == (px - 1) + (py - 1)
     assert d2_diag == max(px, py) - 1
+
+
+@pytest.mark.parametrize("robin", [0.0, 0.6])
+def test_band_cholesky_host_factor(robin):
+    # NEXT f1 host part: the library's complete banded Cholesky factor of every
+    # local A_p (ORAS-modified for robin > 0) reproduces A_p (L L^T) and equals
+    # LAPACK's factor of the oracle's matrix (up to summation order)
+    N, gamma = 30, 2
+    A = ri.laplace_2d(N)
+    owner = ri.voronoi_partition(N, N, 4, seed=2)
+    pl = R.Plan(A, None, owner, gamma)
+    pl.set_robin(robin)
+    pl.finalize()
+    subs = O.setup(A, np.zeros(N * N), owner, gamma, robin=robin)
+    for lp in range(4):
+        Lb, b = pl.band_cholesky(lp)
+        n = Lb.shape[0]
+        L = np.zeros((n, n))
+        for i in range(n):
+            for j in range(max(0, i - b), i + 1):
+                L[i, j] = Lb[i, j - i + b]
+        M = (subs[lp].Asolve if robin else subs[lp].A).toarray()
+        m = M.shape[0]
+        Mp = np.eye(n)
+        Mp[:m, :m] = M  # padding rows are identity rows
+        assert np.linalg.norm(L @ L.T - Mp) <= 1e-14 * np.linalg.norm(Mp)
+        ref = np.linalg.cholesky(M)
+        assert np.linalg.norm(L[:m, :m] - ref) <= 1e-13 * np.linalg.norm(ref)
+        bw_ref = max(abs(i - j) for i, j in zip(*np.nonzero(M)))
+        assert b == bw_ref
