@@ -104,6 +104,7 @@ struct ras_ctx {
   size_t resid_smem = 0;    // dynamic shared memory per CTA (p, r of the largest chunk)
   int resid_chunk = 0;      // rows per CTA of the largest subdomain
   int resid_glo = 0, resid_ghi = 0;  // widest ghost zones below / above a chunk (rows)
+  bool resid_pat = false;   // row-pattern dictionary SpMV (no matrix stream)
   unsigned long long* d_resid_slots = nullptr;
   double* d_q = nullptr;
   double* d_d = nullptr;

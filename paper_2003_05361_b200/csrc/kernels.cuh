@@ -1004,9 +1004,12 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
 #define RAS_PD_RESID 1
 #endif
 constexpr int kNT_RESID = RAS_NT_RESID;
-constexpr int kResidMaxRPT = kNT_RESID >= 1024 ? 8 : kNT_RESID >= 768 ? 12 : 16;  // rows per thread: q in registers (2 * RPT registers)
+// rows per thread (q in registers, 2 * RPT registers): the largest count the
+// register budget of kNT_RESID threads per SM holds without spills
+constexpr int kResidMaxRPT = kNT_RESID >= 1024 ? 8 : kNT_RESID >= 832 ? 9 : kNT_RESID >= 768 ? 10 : 16;
 constexpr unsigned long long kSlotEmpty = 0xffffffffffffffffull;  // NaN pattern never stored (see group_allsum)
 constexpr int kMaxGroupCTAs = 160;  // >= SMs of a B200 (148): CTAs of one group
+constexpr int kMaxPat = 128;       // PAT: patterns per chunk table
 constexpr int kResidNV = 4;         // slot sector per CTA: up to 4 values per reduction (3 used)
 
 #ifdef RAS_RESID_TRACE
@@ -1032,6 +1035,15 @@ struct ResidentCtl {
                               // by other CTAs (export band); the chunk's rows reference columns in
                               // [-glo, nr + ghi) (ghost zones, staged in shared memory every iteration)
   unsigned long long* slots;  // per group [3 ring][gs][kResidNV] partial sums, kSlotEmpty before launch
+  // row-pattern dictionary (PAT): per chunk (local subdomain, CTA) a table of the
+  // distinct rows of A_p -- diagonal + (column delta, value) of each off-diagonal
+  // entry, padded to the SELL-Z width W -- and a uint8 pattern id per row
+  const int32_t* pat_off;     // per (lp, CTA): first pattern of the chunk's table
+  const int32_t* pat_cnt;     // per (lp, CTA): patterns in the table (<= kMaxPat)
+  const double* pat_val;      // [pattern][W] off-diagonal values (0 = padding)
+  const int32_t* pat_dlt;     // [pattern][W] column - row (0 = padding)
+  const double* pat_diag;     // [pattern] diagonal
+  const uint8_t* pid;         // row space: pattern id of every row
   double* pub_p[2];           // [1] = k_residual's p (p_1)
   double* pub_r[2];           // [0] = k_residual's r (r_0)
   double* pub_q[2];
@@ -1217,7 +1229,7 @@ __device__ __forceinline__ constexpr int band_first(int jo) {
 // plain: FP64); q lives in registers.  Rows of the export band are the only
 // ones with off-chunk columns (A_p is symmetric), so every other row gathers p
 // from shared memory without range checks.
-template <int RPT, int W, bool Z, bool TOL>
+template <int RPT, int W, bool Z, bool TOL, bool PAT>
 static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_base, int nsub, SmallSubs SS,
                                                                       ResidentCtl RC, Sell L, Diag D,
                                                                       const int32_t* __restrict__ own_slot,
@@ -1233,8 +1245,15 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
   double* sd = sr + chunk_max;        // d (the correction)
   double* stab = sd + chunk_max;      // Z: dictionary values [256]
   double* sinv = stab + 256;          // Z: __drcp_rn of every dictionary value [256]
-  uint8_t* sdc = reinterpret_cast<uint8_t*>(sinv + 256);  // Z: diagonal codes of the chunk
+  uint8_t* sdc = reinterpret_cast<uint8_t*>(sinv + 256);  // Z: diagonal codes (PAT: pattern ids) of the chunk
   double* sdg = stab;                 // plain: diagonal of the chunk
+  // PAT: the chunk's pattern table after the ids (8-byte aligned)
+  constexpr int WP = W > 0 ? W : 1;
+  double* spv = reinterpret_cast<double*>(sdc + ((chunk_max + 7) & ~7));  // [kMaxPat][W] values
+  double* spdg = spv + kMaxPat * WP;                                       // [kMaxPat] diagonal
+  double* spdi = spdg + kMaxPat;                                           // [kMaxPat] __drcp_rn(diagonal)
+  int32_t* spdl = reinterpret_cast<int32_t*>(spdi + kMaxPat);              // [kMaxPat][W] deltas
+  static_assert(!PAT || Z, "the row-pattern path needs SELL-Z (ghost pivots come from its dictionary)");
   const int gs = RC.gs;
   const int g = blockIdx.x / gs, c = blockIdx.x - g * gs;
   unsigned long long* slots = RC.slots + (size_t)3 * kResidNV * gs * g;
@@ -1270,10 +1289,24 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
     for (int i = threadIdx.x; i < nr; i += NT) {
       sp[i] = __ldcg(&RAS_PUB(pub_p, 1)[i]);  // p_1 = z_0
       sr[i] = __ldcg(&RAS_PUB(pub_r, 0)[i]);  // r_0
-      if (Z)
+      if (PAT)
+        sdc[i] = __ldg(&RC.pid[rb + i]);
+      else if (Z)
         sdc[i] = __ldg(&dcode[i]);
       else
         sdg[i] = __ldg(&dval[i]);
+    }
+    if (PAT) {
+      const int p0 = RC.pat_off[lp * gs + c], np = RC.pat_cnt[lp * gs + c];
+      for (int t = threadIdx.x; t < np * WP; t += NT) {
+        spv[t] = __ldg(&RC.pat_val[(size_t)p0 * WP + t]);
+        spdl[t] = __ldg(&RC.pat_dlt[(size_t)p0 * WP + t]);
+      }
+      for (int t = threadIdx.x; t < np; t += NT) {
+        const double dg = __ldg(&RC.pat_diag[p0 + t]);
+        spdg[t] = dg;
+        spdi[t] = __drcp_rn(dg);  // bitwise the dictionary's reciprocal the ghost readers use
+      }
     }
     double q[RPT];
     double rho = S.rho[lp];
@@ -1281,8 +1314,8 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
     double alpha = 0.0, beta = 0.0;
     int its = 0;
     __syncthreads();
-    auto diag = [&](int i) -> double { return Z ? stab[sdc[i]] : sdg[i]; };
-    auto dinv = [&](int i) -> double { return Z ? sinv[sdc[i]] : __drcp_rn(sdg[i]); };
+    auto diag = [&](int i) -> double { return PAT ? spdg[sdc[i]] : Z ? stab[sdc[i]] : sdg[i]; };
+    auto dinv = [&](int i) -> double { return PAT ? spdi[sdc[i]] : Z ? sinv[sdc[i]] : __drcp_rn(sdg[i]); };
     // Ghost zones of p_{it+1}, staged during pass B of iteration it: the loads of
     // the first kGR ghost rows per thread are issued before pass B (registers),
     // the values p_{it+1}(c) = fma(beta, p_it(c), D^-1(c) fma(-alpha, q_it(c), r_{it-1}(c)))
@@ -1343,7 +1376,23 @@ static __global__ void __launch_bounds__(kNT_RESID, 1) k_resident_pcg(int lp_bas
         }
         if (i < band.x || i >= band.y) __stcg(&RAS_PUB(pub_q, it & 1)[i], qi);
       };
-      if (Z) {
+      if (PAT) {
+        // row patterns: the row's off-diagonal (delta, value) pairs from the
+        // chunk's table in shared memory (mostly one pattern per warp: broadcast)
+#pragma unroll
+        for (int jo = 0; jo < RPT; ++jo) {
+          const int j = band_first<RPT>(jo);
+          const int i = j * NT + threadIdx.x;
+          if (i < nr) {
+            const double pi = sp[i];
+            const int pt = sdc[i];
+            double off = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) off += spv[pt * WP + k] * sp[i + spdl[pt * WP + k]];
+            accum(j, i, pi, off);
+          }
+        }
+      } else if (Z) {
         // SELL-Z rows software-pipelined: the codes / offsets / slice bases of
         // row j + PD are in flight while row j is computed (L2 latency hiding)
         constexpr int PD = RPT < RAS_PD_RESID ? RPT : RAS_PD_RESID;

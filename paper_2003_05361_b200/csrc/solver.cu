@@ -147,28 +147,34 @@ static void compute_model_bytes(ras_ctx* c) {
 // RESIDENT path setup (k_resident_pcg): group count / size, rows per thread,
 // export bands, barrier counters and partial-sum slots.  Leaves c->path alone
 // when no configuration fits (the caller falls back to TILED).
-static const void* resident_kernel(int rpt, bool z, int w, bool tol) {
-#define RAS_RK2(RPT, W, Z) return tol ? (const void*)k_resident_pcg<RPT, W, Z, true> : (const void*)k_resident_pcg<RPT, W, Z, false>;
+static const void* resident_kernel(int rpt, bool z, int w, bool tol, bool pat) {
+#define RAS_RK3(RPT, W, Z, PAT) \
+  return tol ? (const void*)k_resident_pcg<RPT, W, Z, true, PAT> : (const void*)k_resident_pcg<RPT, W, Z, false, PAT>;
+#define RAS_RK2(RPT, W)     \
+  if (pat) {                \
+    RAS_RK3(RPT, W, true, true) \
+  } else {                  \
+    RAS_RK3(RPT, W, true, false) \
+  }
 #define RAS_RK(RPT)                     \
   if (z) {                              \
     if (w == 4) {                       \
-      RAS_RK2(RPT, 4, true)             \
+      RAS_RK2(RPT, 4)                   \
     } else {                            \
-      RAS_RK2(RPT, 8, true)             \
+      RAS_RK2(RPT, 8)                   \
     }                                   \
   } else {                              \
-    RAS_RK2(RPT, 0, false)              \
+    RAS_RK3(RPT, 0, false, false)       \
   }
-  // only the rows-per-thread counts the register budget allows are instantiated
+  // instantiated rows-per-thread counts: 4, 8 and kResidMaxRPT (the register budget's limit)
   if (rpt <= 4) {
     RAS_RK(4)
-  } else if (rpt <= 8 || kResidMaxRPT == 8) {
+  } else if (rpt <= 8) {
     RAS_RK(8)
-  } else if (rpt <= 10) {
-    RAS_RK(10)
   } else {
     RAS_RK(kResidMaxRPT)
   }
+#undef RAS_RK3
 #undef RAS_RK2
 #undef RAS_RK
 }
@@ -195,7 +201,7 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
   const int chunk = chunk_of(nmax, gs);
   if (chunk > cap) return RAS_OK;
   const int need = (chunk + kNT_RESID - 1) / kNT_RESID;
-  const int rpt = need <= 4 ? 4 : need <= 8 ? 8 : need <= 10 ? 10 : kResidMaxRPT;
+  const int rpt = need <= 4 ? 4 : need <= 8 ? 8 : kResidMaxRPT;
   // export bands (chunk rows other CTAs of the group read) and ghost zones (the
   // columns outside the chunk its rows read), from the CSR of A_p
   std::vector<int4> band((size_t)nl * gs);
@@ -232,11 +238,75 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
       ghi_max = std::max(ghi_max, ghi[cc]);
     }
   }
+  // row-pattern dictionary per chunk (PAT): SELL-Z matrices whose every chunk has
+  // <= kMaxPat distinct rows (diagonal + (delta, value) list); then no matrix
+  // stream from L2 in the SpMV
+  std::vector<int32_t> pat_off((size_t)nl * gs, 0), pat_cnt((size_t)nl * gs, 0), pat_dlt;
+  std::vector<double> pat_val, pat_diag;
+  std::vector<uint8_t> pid;
+#ifdef RAS_NO_PAT  // timing experiment: force the SELL-Z stream
+  bool pat = false;
+#else
+  bool pat = c->z;
+#endif
+  if (pat) {
+    const int W = c->zwL;
+    pid.assign((size_t)c->rows_pad, 0);
+    std::vector<uint64_t> key;
+    for (int lp = 0; lp < nl && pat; ++lp) {
+      const auto& S = pl->subs[lp];
+      const int n = (int)S.nrows_pad, ch = chunk_of(n, gs);
+      for (int cc = 0; cc < gs && pat; ++cc) {
+        const int a = std::min(n, cc * ch), e = std::min(n, a + ch);
+        std::vector<std::vector<uint64_t>> keys;  // this chunk's distinct patterns
+        pat_off[(size_t)lp * gs + cc] = (int32_t)pat_diag.size();
+        for (int i = a; i < e; ++i) {
+          const int64_t row = S.row_off + i;
+          key.assign(1 + 2 * W, 0);
+          double dg = pl->diag[row];
+          std::memcpy(&key[0], &dg, 8);
+          int k = 0;
+          for (int64_t q = pl->Ap_ptr[row]; q < pl->Ap_ptr[row + 1]; ++q) {
+            const int j = pl->Ap_col[q];
+            if (j == i) continue;
+            if (k == W) {
+              pat = false;
+              break;
+            }
+            const double v = pl->Ap_val[q];
+            key[1 + k] = (uint64_t)(uint32_t)(j - i);
+            std::memcpy(&key[1 + W + k], &v, 8);
+            ++k;
+          }
+          if (!pat) break;
+          size_t id = 0;
+          while (id < keys.size() && keys[id] != key) ++id;
+          if (id == keys.size()) {
+            if (keys.size() == (size_t)kMaxPat) {
+              pat = false;
+              break;
+            }
+            keys.push_back(key);
+            pat_diag.push_back(dg);
+            for (int t = 0; t < W; ++t) {
+              pat_dlt.push_back((int32_t)(uint32_t)key[1 + t]);
+              double v;
+              std::memcpy(&v, &key[1 + W + t], 8);
+              pat_val.push_back(v);
+            }
+          }
+          pid[(size_t)row] = (uint8_t)id;
+        }
+        pat_cnt[(size_t)lp * gs + cc] = (int32_t)keys.size();
+      }
+    }
+  }
+  const size_t pat_smem = pat ? (size_t)kMaxPat * (8 * (size_t)c->zwL + 8 + 8 + 4 * (size_t)c->zwL) + 8 : 0;
   const size_t smem = (size_t)8 * (glo_max + ghi_max) + (size_t)24 * chunk +
-                      (c->z ? 4096 + (size_t)chunk : (size_t)8 * chunk);
+                      (c->z ? 4096 + (size_t)((chunk + 7) & ~7) : (size_t)8 * chunk) + pat_smem;
   if (smem + 2048 > (size_t)smem_optin) return RAS_OK;  // ghost zones too wide: TILED
   const bool tol = c->opt.local_solver == RAS_LS_EXACT_PCG || c->opt.inner_tol > 0.0;
-  const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol);
+  const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol, pat);
   RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_RESID, smem));
@@ -249,7 +319,20 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
   double* q2;
   TRY(zalloc(c, &q2, (size_t)c->rows_pad));
   // published export-band values (kernels.cuh): pub_p[1] = k_residual's p, pub_r[0] = its r
-  c->RC = ResidentCtl{dband, c->d_resid_slots, {c->d_p2, c->d_p}, {c->d_r, c->d_d}, {c->d_q, q2}, k, gs};
+  int32_t *dpo = nullptr, *dpc = nullptr, *dpd = nullptr;
+  double *dpv = nullptr, *dpg = nullptr;
+  uint8_t* dpid = nullptr;
+  if (pat) {
+    TRY(upload(c, &dpo, pat_off));
+    TRY(upload(c, &dpc, pat_cnt));
+    TRY(upload(c, &dpd, pat_dlt, 1));
+    TRY(upload(c, &dpv, pat_val, 1));
+    TRY(upload(c, &dpg, pat_diag, 1));
+    TRY(upload(c, &dpid, pid, 1));
+  }
+  c->resid_pat = pat;
+  c->RC = ResidentCtl{dband, c->d_resid_slots, dpo, dpc, dpv, dpd, dpg, dpid,
+                      {c->d_p2, c->d_p}, {c->d_r, c->d_d}, {c->d_q, q2}, k, gs};
   c->resid_rpt = rpt;
   c->resid_chunk = chunk;
   c->resid_smem = smem;
@@ -827,7 +910,7 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
 static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m, double inner_tol) {
   // every reduction slot starts empty (kSlotEmpty = all ones)
   RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff, (size_t)c->RC.ngroups * 3 * kResidNV * c->RC.gs * 8, s));
-  const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0);
+  const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0, c->resid_pat);
   int lp0 = 0, nsub = c->nl;
   const int32_t* own = c->d_own_slot;
   double* x = c->d_x;
