@@ -79,7 +79,7 @@ typedef enum { RAS_DET_CENTRAL = 0, RAS_DET_DECENTRAL = 1 } ras_detector;
  * products differs.  IC(0)/ILU(0) always use TILED.
  *   TILED    one streaming launch per PCG pass over every subdomain's rows
  *   BLOCK    one CTA per subdomain runs the whole local solve in shared memory
- *            (|Omega_p| <= 9216 rows; the paper's 4096-unknown regime)
+ *            (|Omega_p| <= 14336 padded rows; the paper's 4096-unknown regime)
  *   RESIDENT a cooperative grid, one CTA per SM, runs each subdomain's whole
  *            local solve with p, r in shared memory and q, d in registers
  *            (|Omega_p| <= 24 * 512 rows per CTA of its group); sync mode only,

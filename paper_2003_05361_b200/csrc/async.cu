@@ -248,7 +248,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
     k_async_persistent(int nl, SmallSubs SS, Sell Rm, Sell L, Diag D, const double* __restrict__ b,
                        const int32_t* __restrict__ own_slot, double* x, DetDev det, PutDev PD, Scal S, double tol,
                        int64_t max_iters, int32_t m, double inner_tol, int32_t* lstop, volatile int32_t* h_lstop,
-                       int64_t* updates, int32_t* noconv, const volatile int32_t* kill) {
+                       int64_t* updates, int32_t* noconv, const volatile int32_t* kill, double* dglob) {
   extern __shared__ double smem[];
   __shared__ double red[3][kNT_SMALL / 32];
   __shared__ int s_stop;
@@ -261,7 +261,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       const int r0 = SS.row_off[lp], n = SS.nrows[lp];
       double* sp = smem;
       double* sr = smem + n;
-      double* sd = smem + 2 * n;
+      double* sd = dglob ? dglob + r0 : smem + 2 * n;  // d: row-private, shared memory or L2
       // a1 + a2: r~ = b~ - [A_p | B_p] x (owner storage read through L2), z = D^-1 r
       double v[3] = {0.0, 0.0, 0.0};
       for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
@@ -337,8 +337,10 @@ static const void* async_persistent_kernel(int rpt, bool z, int wr, int wl) {
   return wl == 4 ? (const void*)k_async_persistent<RPT, 8, 4, true> : (const void*)k_async_persistent<RPT, 8, 8, true>;
   if (rpt <= 4) {
     RAS_AP(4)
-  } else {
+  } else if (rpt <= 9) {
     RAS_AP(9)
+  } else {
+    RAS_AP(14)
   }
 #undef RAS_AP
 }
@@ -671,7 +673,9 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   AsyncRt* A = c->async;
   const int nl = c->nl;
   const void* fn = async_persistent_kernel((c->small_nmax + kNT_SMALL - 1) / kNT_SMALL, c->z, c->zwR, c->zwL);
-  const size_t smem = (size_t)3 * c->small_nmax * sizeof(double);
+  const bool dl2 = c->small_nmax > kSmallSmemDRows;  // d in L2 (row space d_d) for the larger subdomains
+  const size_t smem = (size_t)(dl2 ? 2 : 3) * c->small_nmax * sizeof(double);
+  double* dglob = dl2 ? c->d_d : nullptr;
   RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, sms = 0;
   RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_SMALL, smem));
@@ -698,7 +702,8 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   int32_t* nc = A->d_noconv;
   const volatile int32_t* kill = A->h_kill_dev;
   SmallSubs SS = c->SS;
-  void* args[] = {&nl_, &SS, &Rm, &L, &D, &b, &own, &x, &det, &PD, &S, &tol, &mi, &mm, &inner_tol, &lstop, &hl, &up, &nc, &kill};
+  void* args[] = {&nl_, &SS, &Rm, &L, &D, &b, &own, &x, &det, &PD, &S, &tol, &mi, &mm, &inner_tol, &lstop, &hl, &up, &nc, &kill,
+                  &dglob};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)G);
   cfg.blockDim = dim3(kNT_SMALL);

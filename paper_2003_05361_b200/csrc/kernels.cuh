@@ -685,7 +685,8 @@ static __global__ void __launch_bounds__(kNT_STREAM, RAS_MB_STREAM) k_pupdate_z(
 // recurrences as the tiled path; only summation order differs.
 // ---------------------------------------------------------------------------
 constexpr int kNT_SMALL = 1024;
-constexpr int kSmallMaxRows = 9216;  // 24 B of shared memory per row (p, r, d) <= 216 KB
+constexpr int kSmallMaxRows = 14336;      // p, r in shared memory (16 B / row <= 224 KB)
+constexpr int kSmallSmemDRows = 9216;     // up to here d lives in shared memory too (24 B / row), beyond in L2
 
 struct SmallSubs {
   const int32_t* row_off;  // per local subdomain: first row-space row
@@ -771,7 +772,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
                                                                    const double* __restrict__ p_in,
                                                                    const int32_t* __restrict__ own_slot,
                                                                    double* __restrict__ x, Scal S, Ctl C, int32_t m,
-                                                                   double inner_tol) {
+                                                                   double inner_tol, double* dglob) {
   extern __shared__ double smem[];
   __shared__ double red[2][kNT_SMALL / 32];
   pdl_start();
@@ -780,7 +781,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
   const int r0 = SS.row_off[lp], n = SS.nrows[lp];
   double* sp = smem;           // p
   double* sr = smem + n;       // r
-  double* sd = smem + 2 * n;   // d (correction)
+  double* sd = dglob ? dglob + r0 : smem + 2 * n;  // d (correction): row-private, shared memory or L2
   for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
     sp[i] = __ldg(&p_in[r0 + i]);
     sr[i] = __ldg(&r_in[r0 + i]);

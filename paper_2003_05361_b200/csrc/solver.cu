@@ -542,7 +542,7 @@ static ras_status upload_plan(ras_ctx* c) {
       return set_err(c, RAS_EINVAL, "pcg_path BLOCK/RESIDENT need Jacobi or exact PCG without fuse_p/stage_p");
     c->small = eligible && nmax <= kSmallMaxRows && (req == RAS_PCG_AUTO || req == RAS_PCG_BLOCK);
     if (req == RAS_PCG_BLOCK && !c->small)
-      return set_err(c, RAS_EINVAL, "pcg_path BLOCK needs every |Omega_p| <= 9216 rows (padded)");
+      return set_err(c, RAS_EINVAL, "pcg_path BLOCK needs every |Omega_p| <= 14336 rows (padded)");
     c->small_nmax = nmax;
     c->path = c->small ? RAS_PCG_BLOCK : RAS_PCG_TILED;
     int32_t *dro, *dnr;
@@ -874,13 +874,15 @@ static void small_attr(size_t smem) {
 static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol) {
   const unsigned nsub = R.lp < 0 ? (unsigned)c->nl : 1u;
   const int lp0 = R.lp < 0 ? 0 : R.lp;
-  const size_t smem = (size_t)3 * c->small_nmax * sizeof(double);
+  const bool dl2 = c->small_nmax > kSmallSmemDRows;  // d in L2 (row space d_d) for the larger subdomains
+  const size_t smem = (size_t)(dl2 ? 2 : 3) * c->small_nmax * sizeof(double);
+  double* dglob = dl2 ? c->d_d : nullptr;
   const int rpt = (c->small_nmax + kNT_SMALL - 1) / kNT_SMALL;
 #define RAS_SMALL(RPT, W, Z)                                                                                     \
   small_attr<RPT, W, Z>(smem);                                                                                   \
   g_launch_smem = smem;                                                                                          \
   KL(s, K_SMALL, nsub, kNT_SMALL, (k_small_pcg<RPT, W, Z>), lp0, c->SS, c->L, c->D, (const double*)c->d_r,      \
-     (const double*)c->d_p, (const int32_t*)c->d_own_slot, c->d_x, c->S, C, m, inner_tol)
+     (const double*)c->d_p, (const int32_t*)c->d_own_slot, c->d_x, c->S, C, m, inner_tol, dglob)
 #define RAS_SMALL_R(W, Z)              \
   if (rpt <= 2) {                      \
     RAS_SMALL(2, W, Z);                \
@@ -888,8 +890,10 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
     RAS_SMALL(4, W, Z);                \
   } else if (rpt <= 6) {               \
     RAS_SMALL(6, W, Z);                \
-  } else {                             \
+  } else if (rpt <= 9) {               \
     RAS_SMALL(9, W, Z);                \
+  } else {                             \
+    RAS_SMALL(14, W, Z);               \
   }
 #define RAS_SMALL_Z(W) RAS_SMALL_R(W, true)
 #define RAS_SMALL_0(W) RAS_SMALL_R(W, false)

@@ -195,3 +195,21 @@ def test_non_compressible_matrix_takes_plain_path():
     st, x = s.solve(1e-300, 3, "sync")
     assert rel(x, ref.iterates[3]) <= 1e-10
     s.close()
+
+
+def test_block_path_with_d_in_l2():
+    # subdomains of 9216..14336 padded rows: the one-CTA kernel keeps p, r in
+    # shared memory and the correction d in L2
+    nx, ny = 150, 150
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 4)
+    owner = R.partition_regular(nx, ny, 1, 1, 2, 1)  # 150 x 75 + overlap 3 = 11700 rows
+    ref = oracle_iterates(A, b, owner, 3, "jacobi", 15, 3)
+    s = R.Solver(A, b, owner, 3, R.options("jacobi", 15, path="block"))
+    for k in (1, 3):
+        st, x = s.solve(1e-300, k, "sync")
+        assert s.stats()["pcg_path"] == R._ffi.RAS_PCG_BLOCK
+        assert rel(x, ref.iterates[k]) <= 1e-10, (k, rel(x, ref.iterates[k]))
+    st, x = s.solve(1e-8, 50000, "async")
+    assert st == 0 and O.verify_global(A, x, b, 1e-8)[0]
+    s.close()
