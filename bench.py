@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--fuse-p", action="store_true", help="fuse the PCG p update into the next SpMV")
     ap.add_argument("--path", default="auto", choices=["auto", "tiled", "block", "resident"],
                     help="local-PCG execution path (ras_pcg_path)")
+    ap.add_argument("--robin", type=float, default=0.0, help="ORAS transmission parameter (0 = RAS, the C2 config)")
     return ap.parse_args()
 
 
@@ -294,7 +295,7 @@ def main():
         nccl_id = obj[0]
     t_setup0 = time.perf_counter()
     prob = build_rank_problem(N, rank, args.scale)
-    opts = R.options("jacobi", M_INNER, plain=args.plain, fuse_p=args.fuse_p, path=args.path)
+    opts = R.options("jacobi", M_INNER, plain=args.plain, fuse_p=args.fuse_p, path=args.path, robin=args.robin)
     solver = R.Solver(prob["A"], prob["b"], prob["owner"], GAMMA, opts,
                       comm={"rank": rank, "world": world, "device": local, "nccl_id": nccl_id,
                             "stream": stream.cuda_stream})
@@ -434,6 +435,7 @@ def main():
             "sweeps_done": sweeps,
             "inner_iters_total": stats["inner_iters_total"],
             "pcg_path": ["auto", "tiled", "block", "resident"][stats["pcg_path"]],
+            "robin": args.robin,
             "roofline": roof,
             "pcg_path_gbs": pcg_bytes / (pcg_ms / 1e3) / 1e9 if pcg_ms else None,
             "kernels": kern,
