@@ -119,3 +119,18 @@ def test_async_single_gpu_modes_converge(persistent, detector):
     if persistent:
         assert stt["kernel_launches"] <= 10 * (stt["resumes"] + 1) + 20  # one persistent launch per attempt
     s.close()
+
+
+def test_async_persistent_more_subdomains_than_ctas():
+    # 13 x 13 = 169 subdomains > the 148 co-resident CTAs: every CTA loops over
+    # two subdomains of its own; the solve still detects, verifies and matches
+    N = 13 * 12
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 8)
+    owner = R.partition_regular(N, N, 1, 13, 13, 1)
+    s = R.Solver(A, b, owner, 2, R.options("jacobi", 10, detector="decentral"))
+    st, x = s.solve(1e-8, 200000, "async")
+    stt = s.stats()
+    assert st == 0 and O.verify_global(A, x, b, 1e-8)[0], stt
+    assert stt["updates_min"] > 0 and stt["kernel_launches"] < 50
+    s.close()
