@@ -1104,9 +1104,7 @@ __device__ __forceinline__ void group_allsum(double (&v)[NV], double (*red)[kNT_
       for (int j = 0; j < NV; ++j) st_relaxed_gpu_u64(&nxt[c * 4 + j], kSlotEmpty);
       // release: one fence orders the CTA's earlier stores (export band, ordered
       // before this thread by the CTA barrier) before the value stores
-#ifndef RAS_EXP_NOWFENCE  // timing experiment only (unsafe ordering)
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#endif
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         unsigned long long u = (unsigned long long)__double_as_longlong(s[j]);
