@@ -36,6 +36,37 @@ __global__ void __launch_bounds__(512, 1) kbar(unsigned long long* bar, double* 
     for (int o = 16; o; o >>= 1) v += __shfl_down_sync(~0u, v, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
+    if (V == 14) {  // 3 values per CTA, sum via 8 distributed arrival counters + one read of all slots
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double s = lane < 16 ? red[lane] : 0.0;
+        for (int o = 16; o; o >>= 1) s += __shfl_down_sync(~0u, s, o);
+        unsigned long long* ctr = bar;          // 8 counters, one 64-byte line
+        double* sl = part;                      // [2][G][4]
+        const int par = seq & 1;
+        if (lane == 0) {
+          for (int j = 0; j < 3; ++j) __stcg(&sl[(par * G + c) * 4 + j], s + j);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          atomicAdd(&ctr[c & 7], 1ull);
+        }
+        // counter k receives ceil/floor(G / 8) arrivals per reduction
+        const unsigned long long need = lane < 8 ? (unsigned long long)((G - lane + 7) / 8) * (seq + 1) : 0ull;
+        for (;;) {
+          const unsigned long long v = lane < 8 ? ld_rlx(&ctr[lane]) : 0ull;
+          if (__all_sync(~0u, v >= need)) break;
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        double a2 = 0;
+        for (int k = lane; k < G; k += 32)
+          for (int j = 0; j < 3; ++j) a2 += __ldcg(&sl[(par * G + k) * 4 + j]);
+        for (int o = 16; o; o >>= 1) a2 += __shfl_xor_sync(~0u, a2, o);
+        if (lane == 0) red[0] = a2;
+      }
+      __syncthreads();
+      acc = red[0] * 1e-9;
+      ++seq;
+      continue;
+    }
     if (V >= 9) {  // 3 values per CTA (as k_resident_pcg): 9 = 3 release stores + acquire polls; 10 = + nanosleep(64)
                    // 11: 1 fence + relaxed stores, relaxed polls; 12: 1 fence + relaxed stores, acquire polls;
                    // 13: 1 fence + relaxed stores, relaxed polls + 1 reader fence
@@ -232,7 +263,7 @@ int main() {
   unsigned long long* bar;
   double *part, *out;
   cudaMalloc(&bar, (64 + 9 * 1024) * 8);
-  cudaMalloc(&part, 2 * 1024 * 8);
+  cudaMalloc(&part, 2 * 1024 * 4 * 8);
   cudaMalloc(&out, 8);
   const int iters = 2000;
   for (int G : {sms, sms / 2, 74, 37, 16}) {
@@ -262,6 +293,9 @@ int main() {
     t12 = run<12>(G, iters, bar, part, out);
     cudaMemset(bar + 64, 0xff, 3 * 1024 * 8 * 3);
     t13 = run<13>(G, iters, bar, part, out);
+    cudaMemset(bar, 0, 64 * 8);
+    float t14 = run<14>(G, iters, bar, part, out);
+    printf("G=%3d 3-value distributed counters (8) + one slot read: %.2f\n", G, t14 * 1e3 / iters);
     printf("G=%3d 3-value ring: 3 st.release + acquire polls %.2f | + nanosleep %.2f | fence+relaxed st: relaxed polls %.2f, acquire polls %.2f, relaxed polls + fence %.2f\n",
            G, t9 * 1e3 / iters, t10 * 1e3 / iters, t11 * 1e3 / iters, t12 * 1e3 / iters, t13 * 1e3 / iters);
     printf("G=%3d parallel-poll ring: fence.sc %.2f | fence.acq_rel %.2f | no fence (unsafe) %.2f\n", G, t6 * 1e3 / iters,
