@@ -807,9 +807,9 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
 // triangular solves per local solve) with the complete banded Cholesky factor
 // computed on the host (factor.cpp).  One CTA per subdomain: y = L^-1 r~ then
 // d = L^-T y in 32-row blocks, software-pipelined: while warp 0 finishes block
-// k (the 32 x 32 coupling to block k-1 and the diagonal triangle, both already
-// staged in shared memory, then a warp-shuffle forward substitution with the
-// host's reciprocal pivots), warps 1..7 compute block k+1's far band sums
+// k (the 32 x 32 coupling to block k-1 and the inverse of the diagonal block,
+// both already staged in shared memory: two 32-term dot products per lane,
+// no sequential substitution), the other warps compute block k+1's far band sums
 // (rows already solved before block k, coalesced along the band rows) and stage
 // its coupling / triangle blocks.  One CTA barrier per block.  y / d of the whole
 // subdomain live in shared memory; then the restricted prolongation.
@@ -817,11 +817,16 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1) k_small_pcg(int lp_base, 
 // ---------------------------------------------------------------------------
 constexpr int kNT_BAND = 512;
 constexpr int kBandMaxRows = 12288;  // y / d of one subdomain in shared memory (96 KB)
+#ifndef RAS_BAND_PF
+#define RAS_BAND_PF 4
+#endif
+constexpr int kBandPF = RAS_BAND_PF;  // L2 prefetch distance (blocks) of the band rows
 
 struct BandDev {
   const double* L;     // lower band, row-major, bw + 1 slots per row (slot j - i + bw)
   const double* U;     // upper band = L^T, row-major (slot j - i)
-  const double* dinv;  // row space: 1 / L(i, i)
+  const double* binv;  // inverses of the 32 x 32 diagonal blocks of L, [block][32][32] row-major (lower)
+  const int64_t* boff; // per local subdomain offset into binv
   const int64_t* off;  // per local subdomain offset into L / U
   const int32_t* bw;   // per local subdomain bandwidth
 };
@@ -832,9 +837,9 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
                                                                  double* __restrict__ x, Scal S, Ctl C) {
   extern __shared__ double sy[];        // y, overwritten by d from the last block down
   __shared__ double blkN[2][32][33];    // coupling of a block's rows to the neighbouring block
-  __shared__ double blkT[2][32][33];    // the block's diagonal triangle
+  __shared__ double blkT[2][32][33];    // inverse of the block's diagonal triangle (L_kk^-1 or L_kk^-T)
+  __shared__ double sv2[32];            // block right-hand side before the triangle (warp 0)
   __shared__ double sfar[2][32];        // rhs minus the far band sums
-  __shared__ double sdi[2][32];         // reciprocal pivots of the block
   pdl_start();
   const int lp = lp_base + blockIdx.x;
   if (stopped(C, lp) || !S.active[lp]) return;
@@ -843,14 +848,23 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
   const int64_t w = b + 1;
   const double* Lp = B.L + B.off[lp];
   const double* Up = B.U + B.off[lp];
-  const double* dip = B.dinv + r0;
+  const double* bip = B.binv + B.boff[lp];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   // ---- forward: L y = r~ ----
   // stage block kb (rows i0..i0+31): far sums over columns < i0 - 32, the
   // coupling to block kb-1 and the triangle (helper warps / all warps)
   // t0 / nt: this thread's rank among the staging threads and their count
+  // L2 prefetch of the band rows of block kb (one 128-byte line per thread)
+  auto prefetch_rows = [&](const double* band, int kb, int t0, int nt) {
+    if (kb < 0 || kb >= nb) return;
+    const char* base = reinterpret_cast<const char*>(band + (int64_t)kb * 32 * w);
+    const int64_t bytes = (int64_t)32 * w * 8;
+    for (int64_t o = (int64_t)t0 * 128; o < bytes; o += (int64_t)nt * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
+  };
   auto stage_f = [&](int kb, int buf, int t0, int nt) {
     const int i0 = kb * 32;
+    prefetch_rows(Lp, kb + kBandPF, t0, nt);  // a later staging reads these from L2
     // coupling to block kb-1 and the triangle: 2 x 32 x 32 independent loads
     for (int t = t0; t < 2048; t += nt) {
       const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
@@ -858,8 +872,7 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
         const int jn = i0 - 32 + m;
         blkN[buf][l][m] = (kb > 0 && i - jn <= b) ? __ldg(&Lp[(int64_t)i * w + (jn - i + b)]) : 0.0;
       } else {
-        const int jt = i0 + m;
-        blkT[buf][l][m] = (jt < i && i - jt <= b) ? __ldg(&Lp[(int64_t)i * w + (jt - i + b)]) : 0.0;
+        blkT[buf][l][m] = __ldg(&bip[(int64_t)kb * 1024 + l * 32 + m]);  // (L_kk^-1)[l][m]
       }
     }
     // far band sums (columns before block kb-1), one warp per row
@@ -869,30 +882,30 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
 #pragma unroll 4
       for (int j = max(0, i - b) + lane; j < i0 - 32; j += 32) acc += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
       acc = warp_sum(acc);
-      if (lane == 0) {
-        sfar[buf][l] = __ldg(&r_in[r0 + i]) - acc;
-        sdi[buf][l] = __ldg(&dip[i]);
-      }
+      if (lane == 0) sfar[buf][l] = __ldg(&r_in[r0 + i]) - acc;
     }
   };
+  for (int k = 1; k < kBandPF; ++k) prefetch_rows(Lp, k, threadIdx.x, kNT_BAND);
   stage_f(0, 0, threadIdx.x, kNT_BAND);
   __syncthreads();
   for (int kb = 0; kb < nb; ++kb) {
     const int cur = kb & 1;
     if (wp == 0) {
       const int i0 = kb * 32;
-      double s = sfar[cur][lane];
+      // s = rhs - coupling to block kb-1 (four independent partial sums), then
+      // y = L_kk^-1 s: a 32-term dot product per lane instead of a 32-step substitution
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
       if (kb > 0) {
-#pragma unroll 8
-        for (int m = 0; m < 32; ++m) s -= blkN[cur][lane][m] * sy[i0 - 32 + m];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) a4[m & 3] += blkN[cur][lane][m] * sy[i0 - 32 + m];
       }
-      double yv = 0.0;
-      for (int m = 0; m < 32; ++m) {
-        const double ym = __shfl_sync(0xffffffffu, s, m) * sdi[cur][m];
-        if (lane == m) yv = ym;
-        if (lane > m) s -= blkT[cur][lane][m] * ym;
-      }
-      sy[i0 + lane] = yv;
+      sv2[lane] = sfar[cur][lane] - ((a4[0] + a4[1]) + (a4[2] + a4[3]));
+      __syncwarp();
+      double y4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < 32; ++m) y4[m & 3] += blkT[cur][lane][m] * sv2[m];
+      sy[i0 + lane] = (y4[0] + y4[1]) + (y4[2] + y4[3]);
+      __syncwarp();
     } else if (kb + 1 < nb) {
       stage_f(kb + 1, cur ^ 1, threadIdx.x - 32, kNT_BAND - 32);
     }
@@ -901,14 +914,14 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
   // ---- backward: L^T d = y (block kb's rows of sy hold y until it is solved) ----
   auto stage_b = [&](int kb, int buf, int t0, int nt) {
     const int i0 = kb * 32;
+    prefetch_rows(Up, kb - kBandPF, t0, nt);
     for (int t = t0; t < 2048; t += nt) {
       const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
       if (t < 1024) {
         const int jn = i0 + 32 + m;  // coupling column in block kb+1
         blkN[buf][l][m] = (kb + 1 < nb && jn - i <= b) ? __ldg(&Up[(int64_t)i * w + (jn - i)]) : 0.0;
       } else {
-        const int jt = i0 + m;
-        blkT[buf][l][m] = (jt > i && jt - i <= b) ? __ldg(&Up[(int64_t)i * w + (jt - i)]) : 0.0;
+        blkT[buf][l][m] = __ldg(&bip[(int64_t)kb * 1024 + m * 32 + l]);  // (L_kk^-T)[l][m] = (L_kk^-1)[m][l]
       }
     }
     for (int l = t0 >> 5; l < 32; l += nt >> 5) {
@@ -918,30 +931,28 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
 #pragma unroll 4
       for (int j = i0 + 64 + lane; j <= j1; j += 32) acc += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
       acc = warp_sum(acc);
-      if (lane == 0) {
-        sfar[buf][l] = sy[i] - acc;
-        sdi[buf][l] = __ldg(&dip[i]);
-      }
+      if (lane == 0) sfar[buf][l] = sy[i] - acc;
     }
   };
+  for (int k = 1; k < kBandPF; ++k) prefetch_rows(Up, nb - 1 - k, threadIdx.x, kNT_BAND);
   stage_b(nb - 1, (nb - 1) & 1, threadIdx.x, kNT_BAND);
   __syncthreads();
   for (int kb = nb - 1; kb >= 0; --kb) {
     const int cur = kb & 1;
     if (wp == 0) {
       const int i0 = kb * 32;
-      double s = sfar[cur][lane];
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
       if (kb + 1 < nb) {
-#pragma unroll 8
-        for (int m = 0; m < 32; ++m) s -= blkN[cur][lane][m] * sy[i0 + 32 + m];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) a4[m & 3] += blkN[cur][lane][m] * sy[i0 + 32 + m];
       }
-      double dv = 0.0;
-      for (int m = 31; m >= 0; --m) {
-        const double dm = __shfl_sync(0xffffffffu, s, m) * sdi[cur][m];
-        if (lane == m) dv = dm;
-        if (lane < m) s -= blkT[cur][lane][m] * dm;
-      }
-      sy[i0 + lane] = dv;
+      sv2[lane] = sfar[cur][lane] - ((a4[0] + a4[1]) + (a4[2] + a4[3]));
+      __syncwarp();
+      double d4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < 32; ++m) d4[m & 3] += blkT[cur][lane][m] * sv2[m];
+      sy[i0 + lane] = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+      __syncwarp();
     } else if (kb > 0) {
       stage_b(kb - 1, cur ^ 1, threadIdx.x - 32, kNT_BAND - 32);
     }

@@ -414,21 +414,44 @@ static ras_status upload_band(ras_ctx* c) {
   } catch (const Fail& f) {
     return set_err(c, f.st, f.msg);
   }
-  double *L, *U, *dinv;
-  int64_t* off;
+  double *L, *U, *binv;
+  int64_t *off, *boff;
   int32_t* bw;
-  std::vector<double> di((size_t)c->rows_pad, 1.0);  // reciprocal pivots, row space
+  // inverses of the 32 x 32 diagonal blocks of every L (forward substitution on
+  // the host, FP64): the device applies them as dense products
+  std::vector<int64_t> bo(pl->subs.size() + 1, 0);
+  for (size_t lp = 0; lp < pl->subs.size(); ++lp) bo[lp + 1] = bo[lp] + pl->subs[lp].nrows_pad * 32;
+  std::vector<double> bi((size_t)bo.back(), 0.0);
   for (size_t lp = 0; lp < pl->subs.size(); ++lp) {
-    const auto& S = pl->subs[lp];
-    const int64_t wdt = H.bw[lp] + 1;
-    for (int64_t i = 0; i < S.nrows_pad; ++i) di[S.row_off + i] = 1.0 / H.L[H.off[lp] + i * wdt + H.bw[lp]];
+    const int64_t n = pl->subs[lp].nrows_pad, b = H.bw[lp], wdt = b + 1;
+    const double* Lb = H.L.data() + H.off[lp];
+    for (int64_t k = 0; k < n / 32; ++k) {
+      double T[32][32] = {}, X[32][32] = {};
+      for (int l = 0; l < 32; ++l)
+        for (int m = 0; m <= l; ++m) {
+          const int64_t i = 32 * k + l, j = 32 * k + m;
+          if (i - j <= b) T[l][m] = Lb[i * wdt + (j - i + b)];
+        }
+      for (int m = 0; m < 32; ++m) {  // column m of T^-1
+        X[m][m] = 1.0 / T[m][m];
+        for (int l = m + 1; l < 32; ++l) {
+          double acc = 0.0;
+          for (int t = m; t < l; ++t) acc += T[l][t] * X[t][m];
+          X[l][m] = -acc / T[l][l];
+        }
+      }
+      double* dst = bi.data() + bo[lp] + k * 1024;
+      for (int l = 0; l < 32; ++l)
+        for (int m = 0; m < 32; ++m) dst[l * 32 + m] = X[l][m];
+    }
   }
   TRY(upload(c, &L, H.L, 1));
   TRY(upload(c, &U, H.U, 1));
-  TRY(upload(c, &dinv, di, 1));
+  TRY(upload(c, &binv, bi, 1));
+  TRY(upload(c, &boff, bo));
   TRY(upload(c, &off, H.off));
   TRY(upload(c, &bw, H.bw));
-  c->band = BandDev{L, U, dinv, off, bw};
+  c->band = BandDev{L, U, binv, boff, off, bw};
   int nmax = 0;
   for (const auto& S : pl->subs) nmax = std::max<int>(nmax, (int)S.nrows_pad);
   c->band_smem = (size_t)nmax * sizeof(double);
