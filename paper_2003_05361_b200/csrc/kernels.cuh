@@ -821,6 +821,8 @@ constexpr int kBandMaxRows = 12288;  // y / d of one subdomain in shared memory 
 #define RAS_BAND_PF 4
 #endif
 constexpr int kBandPF = RAS_BAND_PF;  // L2 prefetch distance (blocks) of the band rows
+constexpr int kStageU = (2048 + (kNT_BAND - 32) - 1) / (kNT_BAND - 32);  // staged block entries per helper thread
+constexpr int kStageR = (32 + (kNT_BAND / 32 - 1) - 1) / (kNT_BAND / 32 - 1);  // far-sum rows per helper warp
 
 struct BandDev {
   const double* L;     // lower band, row-major, bw + 1 slots per row (slot j - i + bw)
@@ -865,24 +867,69 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
   auto stage_f = [&](int kb, int buf, int t0, int nt) {
     const int i0 = kb * 32;
     prefetch_rows(Lp, kb + kBandPF, t0, nt);  // a later staging reads these from L2
-    // coupling to block kb-1 and the triangle: 2 x 32 x 32 independent loads
-    for (int t = t0; t < 2048; t += nt) {
+    // coupling to block kb-1 and the triangle: 2 x 32 x 32 independent loads,
+    // all issued before any is stored (kStageU per thread)
+    double ld[kStageU];
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int t = t0 + u * nt;
+      ld[u] = 0.0;
+      if (t < 2048) {
+        const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
+        if (t < 1024) {
+          const int jn = i0 - 32 + m;
+          if (kb > 0 && i - jn <= b) ld[u] = __ldg(&Lp[(int64_t)i * w + (jn - i + b)]);
+        } else {
+          ld[u] = __ldg(&bip[(int64_t)kb * 1024 + l * 32 + m]);  // (L_kk^-1)[l][m]
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int t = t0 + u * nt;
+      if (t < 2048) {
+        const int l = (t >> 5) & 31, m = t & 31;
+        if (t < 1024)
+          blkN[buf][l][m] = ld[u];
+        else
+          blkT[buf][l][m] = ld[u];
+      }
+    }
+    for (int t = t0 + kStageU * nt; t < 2048; t += nt) {  // only when fewer threads stage
       const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
       if (t < 1024) {
         const int jn = i0 - 32 + m;
         blkN[buf][l][m] = (kb > 0 && i - jn <= b) ? __ldg(&Lp[(int64_t)i * w + (jn - i + b)]) : 0.0;
       } else {
-        blkT[buf][l][m] = __ldg(&bip[(int64_t)kb * 1024 + l * 32 + m]);  // (L_kk^-1)[l][m]
+        blkT[buf][l][m] = __ldg(&bip[(int64_t)kb * 1024 + l * 32 + m]);
       }
     }
-    // far band sums (columns before block kb-1), one warp per row
-    for (int l = t0 >> 5; l < 32; l += nt >> 5) {
-      const int i = i0 + l;
-      double acc = 0.0;
+    // far band sums (columns before block kb-1), one warp per row, the loads of
+    // all the warp's rows in flight together
+    const int w0 = t0 >> 5, nw = nt >> 5;
+    double acc[kStageR];
+#pragma unroll
+    for (int u = 0; u < kStageR; ++u) {
+      acc[u] = 0.0;
+      const int l = w0 + u * nw;
+      if (l < 32) {
+        const int i = i0 + l;
 #pragma unroll 4
-      for (int j = max(0, i - b) + lane; j < i0 - 32; j += 32) acc += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
-      acc = warp_sum(acc);
-      if (lane == 0) sfar[buf][l] = __ldg(&r_in[r0 + i]) - acc;
+        for (int j = max(0, i - b) + lane; j < i0 - 32; j += 32) acc[u] += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kStageR; ++u) {
+      const int l = w0 + u * nw;
+      const double a = warp_sum(acc[u]);
+      if (l < 32 && lane == 0) sfar[buf][l] = __ldg(&r_in[r0 + i0 + l]) - a;
+    }
+    for (int l = w0 + kStageR * nw; l < 32; l += nw) {  // only when fewer warps stage
+      const int i = i0 + l;
+      double a = 0.0;
+      for (int j = max(0, i - b) + lane; j < i0 - 32; j += 32) a += __ldg(&Lp[(int64_t)i * w + (j - i + b)]) * sy[j];
+      a = warp_sum(a);
+      if (lane == 0) sfar[buf][l] = __ldg(&r_in[r0 + i]) - a;
     }
   };
   for (int k = 1; k < kBandPF; ++k) prefetch_rows(Lp, k, threadIdx.x, kNT_BAND);
@@ -915,23 +962,67 @@ static __global__ void __launch_bounds__(kNT_BAND) k_band_chol(int lp_base, Smal
   auto stage_b = [&](int kb, int buf, int t0, int nt) {
     const int i0 = kb * 32;
     prefetch_rows(Up, kb - kBandPF, t0, nt);
-    for (int t = t0; t < 2048; t += nt) {
-      const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
-      if (t < 1024) {
-        const int jn = i0 + 32 + m;  // coupling column in block kb+1
-        blkN[buf][l][m] = (kb + 1 < nb && jn - i <= b) ? __ldg(&Up[(int64_t)i * w + (jn - i)]) : 0.0;
-      } else {
-        blkT[buf][l][m] = __ldg(&bip[(int64_t)kb * 1024 + m * 32 + l]);  // (L_kk^-T)[l][m] = (L_kk^-1)[m][l]
+    double ld[kStageU];
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int t = t0 + u * nt;
+      ld[u] = 0.0;
+      if (t < 2048) {
+        const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
+        if (t < 1024) {
+          const int jn = i0 + 32 + m;  // coupling column in block kb+1
+          if (kb + 1 < nb && jn - i <= b) ld[u] = __ldg(&Up[(int64_t)i * w + (jn - i)]);
+        } else {
+          ld[u] = __ldg(&bip[(int64_t)kb * 1024 + m * 32 + l]);  // (L_kk^-T)[l][m] = (L_kk^-1)[m][l]
+        }
       }
     }
-    for (int l = t0 >> 5; l < 32; l += nt >> 5) {
-      const int i = i0 + l;
-      double acc = 0.0;
-      const int j1 = min(n - 1, i + b);
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int t = t0 + u * nt;
+      if (t < 2048) {
+        const int l = (t >> 5) & 31, m = t & 31;
+        if (t < 1024)
+          blkN[buf][l][m] = ld[u];
+        else
+          blkT[buf][l][m] = ld[u];
+      }
+    }
+    for (int t = t0 + kStageU * nt; t < 2048; t += nt) {
+      const int l = (t >> 5) & 31, m = t & 31, i = i0 + l;
+      if (t < 1024) {
+        const int jn = i0 + 32 + m;
+        blkN[buf][l][m] = (kb + 1 < nb && jn - i <= b) ? __ldg(&Up[(int64_t)i * w + (jn - i)]) : 0.0;
+      } else {
+        blkT[buf][l][m] = __ldg(&bip[(int64_t)kb * 1024 + m * 32 + l]);
+      }
+    }
+    const int w0 = t0 >> 5, nw = nt >> 5;
+    double acc[kStageR];
+#pragma unroll
+    for (int u = 0; u < kStageR; ++u) {
+      acc[u] = 0.0;
+      const int l = w0 + u * nw;
+      if (l < 32) {
+        const int i = i0 + l;
+        const int j1 = min(n - 1, i + b);
 #pragma unroll 4
-      for (int j = i0 + 64 + lane; j <= j1; j += 32) acc += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
-      acc = warp_sum(acc);
-      if (lane == 0) sfar[buf][l] = sy[i] - acc;
+        for (int j = i0 + 64 + lane; j <= j1; j += 32) acc[u] += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kStageR; ++u) {
+      const int l = w0 + u * nw;
+      const double a = warp_sum(acc[u]);
+      if (l < 32 && lane == 0) sfar[buf][l] = sy[i0 + l] - a;
+    }
+    for (int l = w0 + kStageR * nw; l < 32; l += nw) {
+      const int i = i0 + l;
+      double a = 0.0;
+      const int j1 = min(n - 1, i + b);
+      for (int j = i0 + 64 + lane; j <= j1; j += 32) a += __ldg(&Up[(int64_t)i * w + (j - i)]) * sy[j];
+      a = warp_sum(a);
+      if (lane == 0) sfar[buf][l] = sy[i] - a;
     }
   };
   for (int k = 1; k < kBandPF; ++k) prefetch_rows(Up, nb - 1 - k, threadIdx.x, kNT_BAND);
