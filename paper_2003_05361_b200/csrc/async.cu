@@ -256,7 +256,12 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
   for (;;) {
     bool any = false;
     for (int lp = blockIdx.x; lp < nl; lp += gridDim.x) {
-      if (lstop[lp]) continue;  // written only by this CTA
+      // lstop[lp] is written by this CTA's thread 0; read it once and broadcast so
+      // the whole CTA takes the same branch (another thread's L1 may hold the old word)
+      __syncthreads();
+      if (threadIdx.x == 0) s_stop = ((volatile int32_t*)lstop)[lp];
+      __syncthreads();
+      if (s_stop) continue;
       any = true;
       const int r0 = SS.row_off[lp], n = SS.nrows[lp];
       double* sp = smem;
@@ -790,7 +795,7 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
     TRY(reset_detection(c));
     if (c->opt.scripted_flags) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
-    } else if (c->small && c->opt.async_persistent != 0) {
+    } else if (c->small && (c->opt.async_persistent == 1 || (c->opt.async_persistent == 2 && inner_tol > 0.0))) {
       st = run_async_persistent(c, tol, max_iters, m, inner_tol, &timeout);
     } else {
       st = run_async_loop(c, tol, max_iters, m, inner_tol, exact, &timeout);

@@ -1258,7 +1258,7 @@ ras_status ras_options_default(ras_options* o) {
   o->use_graphs = 1;
   o->poll_interval = 4;
   o->async_timeout_s = 1800.0;
-  o->async_persistent = 1;
+  o->async_persistent = 2;
   return RAS_OK;
 }
 

@@ -33,6 +33,9 @@ import numpy as np  # noqa: E402
 import ras_inputs as ri  # noqa: E402
 
 
+ASYNC_PERSISTENT = 2  # ras_options.async_persistent (--persistent)
+
+
 def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decentral", max_iters=200000, reps=1,
         owner=None, robin=0.0):
     import paper_2003_05361_b200 as R
@@ -41,7 +44,8 @@ def run(nx, ny, px, py, gamma, mode, tol, m=20, solver="jacobi", detector="decen
     b = ri.rhs(nx * ny, 0)
     if owner is None:
         owner = R.partition_regular(nx, ny, 1, px, py, 1)
-    s = R.Solver(A, b, owner, gamma, R.options(solver, m, detector=detector, robin=robin))
+    s = R.Solver(A, b, owner, gamma, R.options(solver, m, detector=detector, robin=robin,
+                                               async_persistent=ASYNC_PERSISTENT))
     out = []
     for _ in range(reps):
         t0 = time.perf_counter()
@@ -142,7 +146,10 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--out", default=None)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--persistent", type=int, default=2, help="ras_options.async_persistent (0, 1, 2)")
     a = ap.parse_args()
+    global ASYNC_PERSISTENT
+    ASYNC_PERSISTENT = a.persistent
     recs = []
     if a.which == "overlap":
         # 1024^2, 4x4 subdomains of 256^2 (E4 shape: few subdomains, growing overlap)

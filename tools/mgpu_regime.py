@@ -49,7 +49,7 @@ def main():
     b = ri.rhs(nx * ny, 0)
     owner = R.partition_regular(nx, ny, 1, px, py, 1)
     out = []
-    for persistent in (1, 0):
+    for persistent in (1, 0):  # 1: force the persistent kernel for the fixed-m solves (opt-in, R33)
         s = R.Solver(A, b, owner, a.gamma, R.options("jacobi", 20, async_persistent=persistent),
                      comm={"rank": rank, "world": world, "device": local, "nccl_id": nccl_id()})
         for mode in ("sync", "async"):
