@@ -130,8 +130,10 @@ typedef struct {
   int32_t async_persistent;      /* async on one or more GPUs with BLOCK-sized subdomains: one persistent
                                     cooperative kernel per GPU, every CTA iterating its subdomains with no
                                     host involvement.  2 (default) = only for tolerance-based local solves
-                                    (exact / inner_tol > 0; R33); 1 = also for fixed-m PCG (measured to
-                                    diverge on thin strips with wide overlap); 0 = CUDA streams */
+                                    (exact / inner_tol > 0; R33); 1 = also for fixed-m PCG (asynchronous
+                                    convergence then needs rho(|T|) < 1, which inexact PCG local solves do
+                                    not guarantee: measured to diverge on thin strips with wide overlap);
+                                    0 = CUDA streams */
   int32_t reserved_i[2];
   /* Optimized RAS (NEXT f3, PAPER P760-763, R30): Robin-type transmission condition in algebraic
    * form -- the local solve uses A~_p = A_p - robin * diag(sum_{j not in Omega_p} |a_ij|) (rows
