@@ -71,7 +71,9 @@ def options(local_solver="jacobi", inner_iters=20, inner_tol=0.0, detector="dece
     stage: shared-memory staging of p in the tiled SpMV;
     path: local-PCG execution path, "auto" | "tiled" | "block" | "resident" (ras_pcg_path);
     tiled: shorthand for path="tiled";
-    robin: ORAS transmission parameter in [0, 1) (0 = RAS; ras_options.robin, R30)."""
+    robin: ORAS transmission parameter in [0, 1) (0 = RAS; ras_options.robin, R30).
+    Other ras_options fields pass through **kw, e.g. async_persistent=0|1|2 (async driver,
+    R33), detector, max_resumes, poll_interval, async_timeout_s."""
     o = F.RasOptions()
     _check(F.lib().ras_options_default(C.byref(o)))
     o.fuse_p = 1 if fuse_p else 0
