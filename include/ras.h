@@ -118,7 +118,8 @@ typedef struct {
   ras_detector detector;         /* async termination detection (default DECENTRAL, P481-484) */
   int32_t local_crit_owned_only; /* Eq. 2 over owned rows only (R12); default 0 = paper's Eq. 2 */
   int32_t max_resumes;           /* async: resumes after failed verification (R20), default 3 */
-  int32_t use_graphs;            /* capture the sync sweep in a CUDA graph (default 1) */
+  int32_t use_graphs;            /* async stream driver, fixed-m local solves: replay each subdomain's
+                                    update as a captured CUDA graph (default 1) */
   int32_t poll_interval;         /* sweeps between host polls of the device stop flag (default 4) */
   double async_timeout_s;        /* async wall-clock watchdog, default 1800 s */
   int32_t scripted_flags;        /* test hook: Eq. 2 flags come from ras_set_scripted_flags */

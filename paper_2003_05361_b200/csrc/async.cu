@@ -89,6 +89,14 @@ struct AsyncRt {
   int32_t* h_kill_dev = nullptr;
   int64_t* d_put_off = nullptr;       // device copies of put_off / put_peer_off (persistent kernel)
   int32_t* d_put_peer_off = nullptr;
+  // stream driver: one CUDA graph per local subdomain holding a whole update
+  // (residual, detection step, m PCG iterations, prolongation, puts), captured
+  // once per (tol, max_iters, m, inner_tol) -- one launch per update instead of ~100
+  std::vector<cudaGraphExec_t> graph;
+  std::vector<int64_t> graph_launches;  // kernels in each graph (statistics)
+  double g_tol = -1.0, g_itol = -1.0;
+  int64_t g_maxit = -1;
+  int g_m = -1;
 };
 
 // NVLink put lists for the persistent kernel (device view of AsyncRt's lists)
@@ -575,6 +583,8 @@ void async_free(ras_ctx* c) {
   if (A->h_lstop) cudaFreeHost(A->h_lstop);
   if (A->h_active) cudaFreeHost(A->h_active);
   if (A->h_kill) cudaFreeHost(A->h_kill);
+  for (auto g : A->graph)
+    if (g) cudaGraphExecDestroy(g);
   delete A;
   c->async = nullptr;
 }
@@ -631,6 +641,34 @@ static ras_status run_async_loop(ras_ctx* c, double tol, int64_t max_iters, int 
   for (auto& v : ev)
     for (auto& e : v) RAS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   std::vector<int64_t> enq(nl, 0);
+  // capture each subdomain's update as a CUDA graph (fixed-m solves: the kernel
+  // sequence is static; the exact mode polls the host and is enqueued directly)
+  const bool use_graph = !exact && c->opt.use_graphs != 0;
+  if (use_graph && (A->graph.size() != (size_t)nl || A->g_tol != tol || A->g_maxit != max_iters || A->g_m != m ||
+                    A->g_itol != inner_tol)) {
+    for (auto g : A->graph)
+      if (g) cudaGraphExecDestroy(g);
+    A->graph.assign(nl, nullptr);
+    A->graph_launches.assign(nl, 0);
+    for (int lp = 0; lp < nl; ++lp) {
+      cudaStream_t s = A->streams[lp];
+      const int64_t l0 = c->launches;
+      RAS_CUDA(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const ras_status cs = enqueue_sub_sweep(c, lp, s, tol, max_iters, m, inner_tol, exact);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (cs != RAS_OK) return cs;
+      RAS_CUDA(c, ce);
+      RAS_CUDA(c, cudaGraphInstantiate(&A->graph[lp], g, 0));
+      cudaGraphDestroy(g);
+      A->graph_launches[lp] = c->launches - l0;
+      c->launches = l0;
+    }
+    A->g_tol = tol;
+    A->g_maxit = max_iters;
+    A->g_m = m;
+    A->g_itol = inner_tol;
+  }
   const double t0 = now_s();
   *timeout = false;
   ras_status st = RAS_OK;
@@ -643,7 +681,16 @@ static ras_status run_async_loop(ras_ctx* c, double tol, int64_t max_iters, int 
         continue;
       }
       if (enq[lp] >= Q && cudaEventQuery(ev[lp][enq[lp] % Q]) == cudaErrorNotReady) continue;
-      st = enqueue_sub_sweep(c, lp, A->streams[lp], tol, max_iters, m, inner_tol, exact);
+      if (use_graph) {
+        const cudaError_t e = cudaGraphLaunch(A->graph[lp], A->streams[lp]);
+        if (e != cudaSuccess) {
+          st = cuda_err(c, e, "cudaGraphLaunch (async update)");
+          break;
+        }
+        c->launches += A->graph_launches[lp];
+      } else {
+        st = enqueue_sub_sweep(c, lp, A->streams[lp], tol, max_iters, m, inner_tol, exact);
+      }
       if (st != RAS_OK) break;
       RAS_CUDA(c, cudaEventRecord(ev[lp][enq[lp] % Q], A->streams[lp]));
       ++enq[lp];
