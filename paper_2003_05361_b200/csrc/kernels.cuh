@@ -571,6 +571,10 @@ static __global__ void __launch_bounds__(kFinThreads) k_finish(int lp_base, Tile
 // a3' (IC(0)/ILU(0)-PCG): M = L U, z = U^-1 L^-1 r by two level-scheduled
 // triangular solves (P320-323, level-set strategy).
 // ---------------------------------------------------------------------------
+#ifndef RAS_TRSV_SLEEP
+#define RAS_TRSV_SLEEP 64  // ns between polls of a level counter
+#endif
+
 struct TriDev {
   const int32_t* rows;    // level-ordered row-space rows
   const int32_t* rp;      // entry offsets per level-ordered position
@@ -614,7 +618,11 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
     const bool skip = stopped(C, lp) || !active[lp];
     if (!skip && lev > 0 && threadIdx.x == 0) {
       const int32_t need = T.lev_nchunks[T.sub_lev_off[lp] + lev - 1];
-      while (ld_acquire_gpu(done + lev - 1) < need) __nanosleep(64);
+      while (ld_acquire_gpu(done + lev - 1) < need) {
+#if RAS_TRSV_SLEEP > 0
+        __nanosleep(RAS_TRSV_SLEEP);
+#endif
+      }
     }
     __syncthreads();
     const int k = ch.x + threadIdx.x;
