@@ -735,8 +735,6 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   if (per_sm < 1) return set_err(c, RAS_ESTATE, "persistent async kernel does not fit an SM");
   int G = std::min(nl, per_sm * sms);
   *A->h_kill = 0;
-  Ctl C{nullptr, 0};
-  (void)C;
   int nl_ = nl;
   Sell Rm = c->R, L = c->L;
   Diag D = c->D;
@@ -794,7 +792,6 @@ static ras_status run_scripted(ras_ctx* c, double tol, int64_t max_iters, int m,
     A->scripted_n = c->scripted_sweeps;
   }
   RAS_CUDA(c, cudaMemsetAsync(A->d_stop_sweep, 0xff, nl * 8, c->stream));
-  const unsigned g = (unsigned)c->ntiles;
   Ctl C{A->d_lstop, 1};
   int32_t** bufs[2] = {A->d_boards, A->d_boards2};
   int32_t* raw[2] = {A->board, A->board2};

@@ -79,9 +79,8 @@ static ras_status exchange_requests(ras_ctx* c) {
   RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   // all[q*W + r] = how many values rank q needs from rank r
-  int64_t tot_out = 0, tot_in = 0;
+  int64_t tot_in = 0;
   for (int q = 0; q < W; ++q) tot_in += all[(size_t)q * W + me];
-  tot_out = pl->n_halo;
   int64_t *d_req = nullptr, *d_inc = nullptr;
   TRY(upload(c, &d_req, pl->halo_gid, 1));
   TRY(zalloc(c, &d_inc, std::max<int64_t>(tot_in, 1)));
