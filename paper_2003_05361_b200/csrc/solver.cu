@@ -98,7 +98,6 @@ static ras_status exchange_requests(ras_ctx* c) {
   std::vector<int64_t> inc(std::max<int64_t>(tot_in, 1));
   RAS_CUDA(c, cudaMemcpyAsync(inc.data(), d_inc, inc.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  (void)tot_out;
   for (int q = 0; q < W; ++q) {
     if (q == me) continue;
     // where my segment lands in q's halo: sum of what q needs from ranks < me
