@@ -781,6 +781,50 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   return RAS_OK;
 }
 
+// Asynchronous RAS on one GPU with RESIDENT-sized subdomains (each local solve
+// needs the whole GPU): the subdomain updates -- residual, Eq. 2 flag +
+// detection step, the on-chip local solve with prolongation -- are issued one
+// after another on one stream, each reading the latest data (R34: a legal
+// asynchronous schedule, multiplicative-Schwarz ordered).  The host keeps <= Q
+// rounds in flight and stops issuing when every subdomain stopped.
+static ras_status run_async_sequential(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact,
+                                       bool* timeout) {
+  AsyncRt* A = c->async;
+  const int nl = c->nl;
+  const int Q = 4;
+  std::vector<cudaEvent_t> ev(Q);
+  for (auto& e : ev) RAS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  c->resid_seq = true;
+  const double t0 = now_s();
+  *timeout = false;
+  ras_status st = RAS_OK;
+  for (int64_t k = 0;; ++k) {
+    if (k >= Q && cudaEventSynchronize(ev[k % Q]) != cudaSuccess) {
+      st = cuda_err(c, cudaGetLastError(), "async round");
+      break;
+    }
+    int nstopped = 0;
+    for (int lp = 0; lp < nl; ++lp) nstopped += ((volatile int32_t*)A->h_lstop)[lp] != 0;
+    if (nstopped == nl) break;
+    if (now_s() - t0 > c->opt.async_timeout_s) {
+      *timeout = true;
+      break;
+    }
+    for (int lp = 0; lp < nl && st == RAS_OK; ++lp)
+      if (!((volatile int32_t*)A->h_lstop)[lp]) st = enqueue_sub_sweep(c, lp, c->stream, tol, max_iters, m, inner_tol, exact);
+    if (st != RAS_OK) break;
+    RAS_CUDA(c, cudaEventRecord(ev[k % Q], c->stream));
+  }
+  c->resid_seq = false;
+  if (*timeout) {
+    std::vector<int32_t> ones(nl, 1);
+    cudaMemcpy(A->d_lstop, ones.data(), nl * 4, cudaMemcpyHostToDevice);
+  }
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return st;
+}
+
 // scripted lock-step mode (single rank): deterministic detector schedule
 static ras_status run_scripted(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol) {
   AsyncRt* A = c->async;
@@ -839,6 +883,8 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
     TRY(reset_detection(c));
     if (c->opt.scripted_flags) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
+    } else if (c->world == 1 && c->path == RAS_PCG_RESIDENT && !c->small) {
+      st = run_async_sequential(c, tol, max_iters, m, inner_tol, exact, &timeout);
     } else if (c->small && (c->opt.async_persistent == 1 || (c->opt.async_persistent == 2 && inner_tol > 0.0))) {
       st = run_async_persistent(c, tol, max_iters, m, inner_tol, &timeout);
     } else {

@@ -105,6 +105,7 @@ struct ras_ctx {
   int resid_chunk = 0;      // rows per CTA of the largest subdomain
   int resid_glo = 0, resid_ghi = 0;  // widest ghost zones below / above a chunk (rows)
   bool resid_pat = false;   // row-pattern dictionary SpMV (no matrix stream)
+  bool resid_seq = false;   // async sequential schedule: per-subdomain calls use k_resident_pcg
   unsigned long long* d_resid_slots = nullptr;
   double* d_q = nullptr;
   double* d_d = nullptr;

@@ -932,11 +932,12 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
 
 // RESIDENT path: one cooperative launch runs every local subdomain's whole PCG
 // + prolongation (k_resident_pcg), batched (sync) solves only.
-static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m, double inner_tol) {
+static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m, double inner_tol, int lp_first,
+                                   int nsub_) {
   // every reduction slot starts empty (kSlotEmpty = all ones)
   RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff, (size_t)c->RC.ngroups * 3 * kResidNV * c->RC.gs * 8, s));
   const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0, c->resid_pat);
-  int lp0 = 0, nsub = c->nl;
+  int lp0 = lp_first, nsub = nsub_;
   const int32_t* own = c->d_own_slot;
   double* x = c->d_x;
   int32_t chunk_max = c->resid_chunk, glo = c->resid_glo, ghi = c->resid_ghi;
@@ -982,7 +983,8 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
     return RAS_OK;
   }
   if (c->small) return enq_small_pcg(c, s, R, C, m, inner_tol);
-  if (c->path == RAS_PCG_RESIDENT && R.lp < 0) return enq_resident_pcg(c, s, C, m, inner_tol);
+  if (c->path == RAS_PCG_RESIDENT && (R.lp < 0 || c->resid_seq))
+    return enq_resident_pcg(c, s, C, m, inner_tol, R.lp < 0 ? 0 : R.lp, R.lp < 0 ? c->nl : 1);
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
     TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
     KL(s, K_ZDOT, g, kNT_STREAM, k_zdot<true>, tb, tiles_next(c), (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);
@@ -1084,7 +1086,7 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
 // a4
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
   if (c->small || c->chol) return RAS_OK;  // k_small_pcg / k_band_chol prolong in the same kernel
-  if (c->path == RAS_PCG_RESIDENT && R.lp < 0) return RAS_OK;  // so does k_resident_pcg
+  if (c->path == RAS_PCG_RESIDENT && (R.lp < 0 || c->resid_seq)) return RAS_OK;  // so does k_resident_pcg
   KL(s, K_PROL, R.ntiles, kNT_STREAM, k_prolong, R.tile_base, tiles_next(c), (const int32_t*)c->d_own_slot, (const double*)c->d_d,
      c->d_x, c->S, C);
   return RAS_OK;

@@ -213,3 +213,21 @@ def test_block_path_with_d_in_l2():
     st, x = s.solve(1e-8, 50000, "async")
     assert st == 0 and O.verify_global(A, x, b, 1e-8)[0]
     s.close()
+
+
+def test_async_sequential_schedule_on_resident_subdomains():
+    # R34: RESIDENT-sized subdomains in async mode on one GPU run one after
+    # another on one stream (a legal asynchronous, multiplicative-ordered
+    # schedule): converges, verifies, and needs fewer updates than sync sweeps
+    nx, ny = 262, 250
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 2)
+    owner = R.partition_regular(nx, ny, 1, 2, 2, 1)
+    s = R.Solver(A, b, owner, 4, R.options("jacobi", 12))
+    st, x = s.solve(1e-8, 100000, "sync")
+    sync_sweeps = s.stats()["sweeps"]
+    st, x = s.solve(1e-8, 100000, "async")
+    stt = s.stats()
+    assert st == 0 and O.verify_global(A, x, b, 1e-8)[0], stt
+    assert stt["updates_max"] < sync_sweeps, (stt["updates_max"], sync_sweeps)
+    s.close()
