@@ -781,8 +781,8 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   return RAS_OK;
 }
 
-// Asynchronous RAS on one GPU with RESIDENT-sized subdomains (each local solve
-// needs the whole GPU): the subdomain updates -- residual, Eq. 2 flag +
+// Asynchronous RAS with RESIDENT-sized subdomains (each local solve needs the
+// whole GPU; any number of GPUs, puts to peers included): a rank's subdomain updates -- residual, Eq. 2 flag +
 // detection step, the on-chip local solve with prolongation -- are issued one
 // after another on one stream, each reading the latest data (R34: a legal
 // asynchronous schedule, multiplicative-Schwarz ordered).  The host keeps <= Q
@@ -883,7 +883,7 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
     TRY(reset_detection(c));
     if (c->opt.scripted_flags) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
-    } else if (c->world == 1 && c->path == RAS_PCG_RESIDENT && !c->small) {
+    } else if (c->path == RAS_PCG_RESIDENT && !c->small) {
       st = run_async_sequential(c, tol, max_iters, m, inner_tol, exact, &timeout);
     } else if (c->small && (c->opt.async_persistent == 1 || (c->opt.async_persistent == 2 && inner_tol > 0.0))) {
       st = run_async_persistent(c, tol, max_iters, m, inner_tol, &timeout);

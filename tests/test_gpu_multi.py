@@ -138,3 +138,20 @@ def test_multi_gpu_sync_converges():
         st, x, stats = res[r][("conv", "sync")]
         assert st == 0 and stats["sweeps"] == ref.sweeps
         assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-10
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
+def test_multi_gpu_async_resident_sequential():
+    # R34 on 2 GPUs: RESIDENT-sized subdomains, per-rank sequential updates with
+    # NVLink puts to the peer; converges and verifies
+    nx, ny = 262, 250
+    cfg = dict(nx=nx, ny=ny, P=4, gamma=4, solver="jacobi", m=12, converge="async",
+               owner=O.partition_regular(nx, ny, 1, 2, 2, 1))
+    res = _run(2, cfg)
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 0)
+    for r in range(2):
+        st, x, stats = res[r][("conv", "async")]
+        assert st == 0, stats
+        assert O.verify_global(A, x, b, 1e-8)[0]
+        assert stats["pcg_path"] == 3 or stats["pcg_path"] in (1, 2)
