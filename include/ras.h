@@ -242,8 +242,14 @@ ras_status ras_set_scripted_flags(ras_ctx* ctx, const uint8_t* flags, int64_t ns
 ras_status ras_detector_stops(const ras_ctx* ctx, int64_t* stop_out);
 
 /* Per-kernel CUDA-event timing on the library stream (for the roofline report).
- * When enabled, every kernel launch of ras_solve* is bracketed by events; the
- * totals of the last solve are returned per kernel kind. */
+ * When enabled, every kernel launch of ras_solve* on the library stream is
+ * bracketed by events (sync mode; the async drivers' per-subdomain streams and
+ * graphs are not timed); the totals of the last solve are returned per kernel
+ * kind: k_residual, k_spmv_dot, k_update_dot, k_pupdate, k_prolong, k_pack,
+ * control (scalar / check kernels), k_trsv, k_zdot, k_small_pcg (BLOCK),
+ * k_resident_pcg (RESIDENT), k_band_chol (direct solve).  bytes_per_launch is
+ * the DESIGN.md §5 model; for the whole-solve kernels (BLOCK / RESIDENT) it is the
+ * compulsory HBM bytes of one launch.  out may be NULL to query the count. */
 typedef struct {
   char name[32];
   int64_t launches;
