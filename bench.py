@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--path", default="auto", choices=["auto", "tiled", "block", "resident"],
                     help="local-PCG execution path (ras_pcg_path)")
     ap.add_argument("--robin", type=float, default=0.0, help="ORAS transmission parameter (0 = RAS, the C2 config)")
+    ap.add_argument("--overlap", type=int, default=GAMMA, help="overlap gamma (8 = the C2 config; C3 sweeps 1/2/4/8)")
     return ap.parse_args()
 
 
@@ -271,7 +272,9 @@ def config_dict(N, nx, ny, P, mode, ws_bytes=None):
 # our arm
 # ----------------------------------------------------------------------------
 def main():
+    global GAMMA
     args = parse()
+    GAMMA = args.overlap
     if args.impl == "reference":
         return run_reference(args)
     import torch
