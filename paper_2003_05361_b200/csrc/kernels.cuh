@@ -34,11 +34,21 @@ constexpr int kTileRows = 256 * RAS_RPT;    // rows per CTA tile (plan tile_rows
 // budget) of each streaming kernel; rows per thread = kTileRows / threads.
 // Tuned on B200 (round 1 sweep): the gather kernels want more,
 // lighter threads (2 rows each), the pure streams 4 rows per thread.
+// k_residual on the row-pattern (SELL-Z) matrix: 256 threads x 8 CTAs/SM (4 rows
+// per thread, full occupancy) measured 268 us vs 281 us for 512 x 4 on C2
+// (profiles/r01_exp_residual_cta.txt); the SELL-32 instantiations keep 512 x 4
+// (they spill 2-3x more at 32 registers and were not re-measured).
 #ifndef RAS_NT_RES
 #define RAS_NT_RES 512
 #endif
 #ifndef RAS_MB_RES
 #define RAS_MB_RES 4
+#endif
+#ifndef RAS_NT_RES_Z
+#define RAS_NT_RES_Z 256
+#endif
+#ifndef RAS_MB_RES_Z
+#define RAS_MB_RES_Z 8
 #endif
 #ifndef RAS_NT_SPMV
 #define RAS_NT_SPMV 512
@@ -58,7 +68,7 @@ constexpr int kTileRows = 256 * RAS_RPT;    // rows per CTA tile (plan tile_rows
 #ifndef RAS_MB_STREAM
 #define RAS_MB_STREAM 6
 #endif
-constexpr int kNT_RES = RAS_NT_RES, kNT_SPMV = RAS_NT_SPMV, kNT_UPD = RAS_NT_UPD, kNT_STREAM = RAS_NT_STREAM;
+constexpr int kNT_RES = RAS_NT_RES, kNT_RES_Z = RAS_NT_RES_Z, kNT_SPMV = RAS_NT_SPMV, kNT_UPD = RAS_NT_UPD, kNT_STREAM = RAS_NT_STREAM;
 constexpr int kNP = 4;                      // partial slots per warp
 constexpr int kMaxW = 8;                    // unrolled SELL width (wider slices take the loop path)
 constexpr int kStageMax = 4096;             // max p span staged in shared memory by k_spmv_dot (32 KB)
@@ -244,12 +254,12 @@ __device__ __forceinline__ double sell_dot(const Sell& M, int64_t row, const dou
 //   JAC: z = D^-1 r, p = z.  Partials: r.z, ||r~||^2, owned ||r~||^2.
 // ---------------------------------------------------------------------------
 template <bool JAC, int W, bool Z>
-static __global__ void __launch_bounds__(kNT_RES, RAS_MB_RES) k_residual(int64_t tile_base, Tiles T, Sell R,
+static __global__ void __launch_bounds__(Z ? kNT_RES_Z : kNT_RES, Z ? RAS_MB_RES_Z : RAS_MB_RES) k_residual(int64_t tile_base, Tiles T, Sell R,
                                                               const double* __restrict__ b, Diag D,
                                                               const int32_t* __restrict__ own_slot,
                                                               const double* __restrict__ x, double* __restrict__ r,
                                                               double* __restrict__ p, Scal S, Ctl C) {
-  constexpr int NT = kNT_RES, RPT = kTileRows / NT;
+  constexpr int NT = Z ? kNT_RES_Z : kNT_RES, RPT = kTileRows / NT;
   pdl_start();
   const int64_t t = tile_base + (T.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
   const int4 ti = T.tile[t];

@@ -814,7 +814,7 @@ static Tiles tiles_next(ras_ctx* c) {
 
 ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
 #define RAS_RES(JAC, W, Z)                                                                                  \
-  KL(s, K_RES, R.ntiles, kNT_RES, (k_residual<JAC, W, Z>), R.tile_base, tiles_next(c), c->R, (const double*)c->d_b, \
+  KL(s, K_RES, R.ntiles, (Z) ? kNT_RES_Z : kNT_RES, (k_residual<JAC, W, Z>), R.tile_base, tiles_next(c), c->R, (const double*)c->d_b, \
      c->D, (const int32_t*)c->d_own_slot, (const double*)c->d_x, c->d_r, c->d_p, c->S, C)
 #define RAS_RES_J0(W) RAS_RES(true, W, false)
 #define RAS_RES_I0(W) RAS_RES(false, W, false)
