@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RAS_ABI_VERSION 2
+#define RAS_ABI_VERSION 3
 
 typedef struct ras_ctx ras_ctx; /* opaque; one per rank (process) */
 
@@ -81,9 +81,10 @@ typedef enum { RAS_DET_CENTRAL = 0, RAS_DET_DECENTRAL = 1 } ras_detector;
  *   BLOCK    one CTA per subdomain runs the whole local solve in shared memory
  *            (|Omega_p| <= 14336 padded rows; the paper's 4096-unknown regime)
  *   RESIDENT a cooperative grid, one CTA per SM, runs each subdomain's whole
- *            local solve with p, r in shared memory and q, d in registers
- *            (|Omega_p| <= 24 * 512 rows per CTA of its group); sync mode only,
- *            async solves fall back to TILED
+ *            local solve with p, r, d in shared memory and q in registers
+ *            (a chunk of <= kResidMaxRPT * 768 rows per CTA of its group).  Sync
+ *            solves run every local subdomain in one launch; async solves issue
+ *            one launch per subdomain update, one after another (R34)
  *   AUTO     BLOCK if it applies, else RESIDENT if it applies, else TILED */
 typedef enum { RAS_PCG_AUTO = 0, RAS_PCG_TILED = 1, RAS_PCG_BLOCK = 2, RAS_PCG_RESIDENT = 3 } ras_pcg_path;
 
@@ -135,7 +136,10 @@ typedef struct {
                                     convergence then needs rho(|T|) < 1, which inexact PCG local solves do
                                     not guarantee: measured to diverge on thin strips with wide overlap);
                                     0 = CUDA streams */
-  int32_t reserved_i[2];
+  int32_t force_first_stop;      /* test hook (async): in the first detection round every Eq. 2 flag reads
+                                    as set, so detection terminates after a few updates and the
+                                    post-termination verification fails -> the R20 resume path runs */
+  int32_t reserved_i[1];
   /* Optimized RAS (NEXT f3, PAPER P760-763, R30): Robin-type transmission condition in algebraic
    * form -- the local solve uses A~_p = A_p - robin * diag(sum_{j not in Omega_p} |a_ij|) (rows
    * coupled outside Omega_p); the residual keeps A.  0 = RAS (Dirichlet truncation, default);
@@ -145,17 +149,32 @@ typedef struct {
   double reserved_d[3];
 } ras_options;
 
+/* Transport of a multi-rank context (ras_comm.transport). */
+typedef enum {
+  RAS_TRANSPORT_NCCL = 0,     /* one process per GPU: NCCL collectives + CUDA IPC peer windows over NVLink */
+  RAS_TRANSPORT_LOOPBACK = 1  /* test transport: `world` virtual ranks driven by host threads of ONE process
+                                 on ONE device.  Collectives are host rendezvous of the group's threads
+                                 (device buffers staged through the host or copied device-to-device); peer
+                                 windows are the peers' plain device pointers, so the async kernels' puts,
+                                 version counters and detector boards run unchanged.  Every rank's thread
+                                 must call ras_setup / ras_solve / ras_set_rhs concurrently (they are
+                                 collective); a rank that never arrives makes the others fail with
+                                 RAS_ESTATE after 600 s instead of hanging. */
+} ras_transport;
+
 /* Multi-GPU plumbing.  NULL = single GPU (current device, default stream). */
 typedef struct {
   int32_t rank, world;          /* this process's rank and the number of ranks (GPUs) */
   int32_t device;               /* CUDA device ordinal this rank drives */
   const void* nccl_unique_id;   /* 128 bytes from ras_nccl_unique_id() on rank 0, broadcast by
-                                   the caller (torch.distributed); NULL when world == 1 */
+                                   the caller (torch.distributed); NULL when world == 1.  LOOPBACK:
+                                   any 128 bytes naming the group, identical on its ranks */
   void* cuda_stream;            /* cudaStream_t for sync-mode work; NULL = a library stream */
   /* optional device allocator hooks (e.g. torch's caching allocator); NULL = cudaMalloc */
   void* (*dev_alloc)(size_t bytes, void* user);
   void (*dev_free)(void* ptr, void* user);
   void* alloc_user;
+  int32_t transport;            /* ras_transport (0 = NCCL) */
 } ras_comm;
 
 typedef struct {
@@ -167,15 +186,23 @@ typedef struct {
   int64_t updates_min, updates_median, updates_max; /* per-subdomain local solves (Fig. 7c, P727-735) */
   int64_t inner_iters_total;   /* total local PCG iterations over all subdomains on this rank */
   double final_rel_residual;   /* true ||b - A x|| / ||b|| of the returned iterate */
-  double t_residual, t_local_solve, t_prolong, t_exchange, t_convcheck; /* per-phase seconds (Figs. 3a-7a) */
+  /* per-phase device seconds of the last solve (Figs. 3a-7a: restrict + residual, local solve, prolongation,
+   * exchange, convergence check).  Sync: CUDA events around each batched phase on the library stream
+   * (every local subdomain advances together, so this is also each subdomain's time); their sum is the
+   * device part of time_to_solution_s.  Async: %globaltimer at the phase boundaries of every update,
+   * summed over a subdomain's updates and averaged over the local subdomains.  Where the local solve
+   * kernel also prolongs (BLOCK, RESIDENT, direct) t_prolong is 0 and the prolongation is in t_local_solve. */
+  double t_residual, t_local_solve, t_prolong, t_exchange, t_convcheck;
   double model_bytes;          /* algorithmic HBM bytes moved by this rank's kernels */
   int32_t num_subdomains, world;
   int32_t local_subdomains;
-  int32_t pcg_path;            /* ras_pcg_path the Jacobi/exact local solves of a sync solve ran on */
+  int32_t pcg_path;            /* ras_pcg_path the local solves of the last solve ran on (sync or async) */
   int64_t rows_local;          /* sum |Omega_p| on this rank */
   int64_t halo_values;         /* halo slots on this rank (values received per exchange) */
   int64_t kernel_launches;     /* kernels launched by the last ras_solve on this rank */
   int64_t fresh_halo_reads;    /* async: halo version changes observed */
+  int32_t resident_pattern;    /* RESIDENT path: 1 = row-pattern dictionary SpMV, 0 = SELL-Z / SELL stream */
+  int32_t reserved_s;
 } ras_stats_t;
 
 /* Fill *opt with defaults. */
@@ -261,6 +288,11 @@ ras_status ras_kernel_timing(ras_ctx* ctx, int32_t enable);
 ras_status ras_kernel_times(const ras_ctx* ctx, ras_kernel_time_t* out, int32_t max_entries, int32_t* n_out);
 
 int32_t ras_abi_version(void);
+
+/* Hash of the sources, headers, defines and flags this library was built from
+ * (paper_2003_05361_b200/build.py); the Python binding refuses a library whose
+ * hash differs from the tree it is loaded from.  Static string, never NULL. */
+const char* ras_build_hash(void);
 
 #ifdef __cplusplus
 }

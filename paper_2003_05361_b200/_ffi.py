@@ -18,7 +18,8 @@ RAS_SYNC, RAS_ASYNC = 0, 1
 RAS_LS_JACOBI_PCG, RAS_LS_IC0_PCG, RAS_LS_ILU0_PCG, RAS_LS_EXACT_PCG, RAS_LS_CHOLESKY = range(5)
 RAS_DET_CENTRAL, RAS_DET_DECENTRAL = 0, 1
 RAS_PCG_AUTO, RAS_PCG_TILED, RAS_PCG_BLOCK, RAS_PCG_RESIDENT = range(4)
-ABI_VERSION = 2  # include/ras.h RAS_ABI_VERSION
+RAS_TRANSPORT_NCCL, RAS_TRANSPORT_LOOPBACK = 0, 1
+ABI_VERSION = 3  # include/ras.h RAS_ABI_VERSION
 
 I32, I64, F64, U8 = C.c_int32, C.c_int64, C.c_double, C.c_uint8
 P = C.POINTER
@@ -37,7 +38,7 @@ class RasOptions(C.Structure):
     _fields_ = [("local_solver", I32), ("inner_iters", I32), ("inner_tol", F64), ("detector", I32),
                 ("local_crit_owned_only", I32), ("max_resumes", I32), ("use_graphs", I32), ("poll_interval", I32),
                 ("async_timeout_s", F64), ("scripted_flags", I32), ("fuse_p", I32), ("matrix_format", I32), ("stage_p", I32),
-                ("pcg_path", I32), ("async_persistent", I32), ("reserved_i", I32 * 2), ("robin", F64), ("reserved_d", F64 * 3)]
+                ("pcg_path", I32), ("async_persistent", I32), ("force_first_stop", I32), ("reserved_i", I32 * 1), ("robin", F64), ("reserved_d", F64 * 3)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -47,7 +48,7 @@ FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 class RasComm(C.Structure):
     _fields_ = [("rank", I32), ("world", I32), ("device", I32), ("nccl_unique_id", C.c_void_p),
                 ("cuda_stream", C.c_void_p), ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN),
-                ("alloc_user", C.c_void_p)]
+                ("alloc_user", C.c_void_p), ("transport", I32)]
 
 
 class RasStats(C.Structure):
@@ -58,7 +59,8 @@ class RasStats(C.Structure):
                 ("t_residual", F64), ("t_local_solve", F64), ("t_prolong", F64), ("t_exchange", F64),
                 ("t_convcheck", F64), ("model_bytes", F64), ("num_subdomains", I32), ("world", I32),
                 ("local_subdomains", I32), ("pcg_path", I32), ("rows_local", I64), ("halo_values", I64),
-                ("kernel_launches", I64), ("fresh_halo_reads", I64)]
+                ("kernel_launches", I64), ("fresh_halo_reads", I64), ("resident_pattern", I32),
+                ("reserved_s", I32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -79,6 +81,7 @@ class RasKernelTime(C.Structure):
 # (name, restype, argtypes) for every symbol declared in include/*.h
 SIGNATURES = [
     ("ras_abi_version", I32, []),
+    ("ras_build_hash", C.c_char_p, []),
     ("ras_options_default", I32, [P(RasOptions)]),
     ("ras_setup", I32, [P(C.c_void_p), P(RasCsr), P(F64), P(RasPartition), I32, P(RasOptions), P(RasComm)]),
     ("ras_set_rhs", I32, [C.c_void_p, P(F64)]),
@@ -131,6 +134,13 @@ def lib():
             f.argtypes = args
         if L.ras_abi_version() != ABI_VERSION:
             raise RuntimeError(f"{LIB_PATH} has ABI {L.ras_abi_version()}, the binding expects {ABI_VERSION}: rebuild it")
+        if not os.environ.get("RAS_LIB_PATH"):  # explicit variant builds (tuning sweeps) skip the check
+            from .build import source_hash
+
+            want, have = source_hash(), L.ras_build_hash().decode()
+            if have != want:
+                raise RuntimeError(f"{LIB_PATH} was built from other sources (hash {have}, tree {want}): "
+                                   "rebuild it with `python -c 'import __graft_entry__ as g; g.build()'`")
         _lib = L
     return _lib
 

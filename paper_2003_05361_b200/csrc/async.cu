@@ -53,7 +53,30 @@ struct DetDev {
   int32_t* const* boards; // [world] board base per rank (own + IPC-mapped peers)
   int32_t my_rank;
   int32_t owned_only;
+  const int32_t* force;   // test hook (ras_options.force_first_stop): nonzero -> every flag reads as set
+  double* phase;          // [nl][kNPhase] device seconds per phase (ras_stats_t t_*), summed over updates
+  unsigned long long* phase_last;  // [nl] globaltimer of the subdomain's last phase boundary
 };
+
+// Phase accounting of asynchronous updates (ras_stats_t t_residual ... t_convcheck,
+// Figs. 3a-7a): thread 0 reads %globaltimer at each phase boundary of subdomain
+// lp's update and charges the interval since the previous boundary to `ph`
+// (ph < 0: the update starts, nothing is charged).
+enum { PH_RES = 0, PH_SOLVE, PH_PROL, PH_EXCH, PH_CHECK, kNPhase };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void phase_mark(const DetDev& D, int lp, int ph) {
+  const unsigned long long t = gtimer();
+  if (ph >= 0) D.phase[lp * kNPhase + ph] += 1e-9 * (double)(t - D.phase_last[lp]);
+  D.phase_last[lp] = t;
+}
+static __global__ void k_phase(DetDev D, int lp, int ph, const int32_t* lstop) {
+  if (threadIdx.x || blockIdx.x || lstop[lp]) return;
+  phase_mark(D, lp, ph);
+}
 
 struct AsyncRt {
   std::vector<cudaStream_t> streams;
@@ -87,6 +110,8 @@ struct AsyncRt {
   int64_t scripted_n = 0;
   int32_t* h_kill = nullptr;      // mapped pinned: host watchdog -> persistent kernel
   int32_t* h_kill_dev = nullptr;
+  int32_t* d_force = nullptr;         // det.force (force_first_stop hook), set per detection round
+  double* d_b2 = nullptr;             // det.b2 (Eq. 2 ||b~_p||^2), rewritten by ras_set_rhs
   int64_t* d_put_off = nullptr;       // device copies of put_off / put_peer_off (persistent kernel)
   int32_t* d_put_peer_off = nullptr;
   // stream driver: one CUDA graph per local subdomain holding a whole update
@@ -163,6 +188,7 @@ __device__ int det_step(const DetDev& D, int lp, int c, const int32_t* in, int32
 
 // Eq. 2 (P337-340): ||r~_p||^2 < tau^2 ||b~_p||^2 (||b~_p|| = 0: ||r~_p|| = 0, R11).
 __device__ __forceinline__ int local_flag(const DetDev& D, const Scal& S, int lp, double tol) {
+  if (*(const volatile int32_t*)D.force) return 1;
   const double r2 = D.owned_only ? S.own2[lp] : S.rt2[lp];
   const double b2 = D.b2[lp];
   return b2 == 0.0 ? (r2 == 0.0) : (r2 < tol * tol * b2);
@@ -173,6 +199,7 @@ static __global__ void k_detect(int lp, DetDev D, Scal S, double tol, int64_t ma
                                 volatile int32_t* h_lstop, int64_t* updates, int32_t* noconv) {
   if (threadIdx.x || blockIdx.x) return;
   if (lstop[lp]) return;
+  phase_mark(D, lp, PH_RES);  // the residual kernels ended when this one started
   const int64_t u = ++updates[lp];
   const int c = local_flag(D, S, lp, tol);
   const int32_t* in = D.boards[D.my_rank];
@@ -188,6 +215,7 @@ static __global__ void k_detect(int lp, DetDev D, Scal S, double tol, int64_t ma
     lstop[lp] = 1;
     h_lstop[lp] = 1;
   }
+  phase_mark(D, lp, PH_CHECK);
 }
 
 // Scripted lock-step mode (test hook, SURVEY §8c "Detectors"): all local
@@ -214,7 +242,7 @@ static __global__ void k_put(int lp, int64_t e0, int64_t e1, const int32_t* __re
                              const int32_t* __restrict__ rank, const int64_t* __restrict__ ridx,
                              const double* __restrict__ x, double* const* peer_x, uint32_t* ticket,
                              const int32_t* peers, int npeers, int32_t* const* boards, int P, int gp,
-                             const int32_t* lstop) {
+                             const int32_t* lstop, DetDev D) {
   if (lstop[lp]) return;
   for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1; e += (int64_t)gridDim.x * blockDim.x)
     peer_x[rank[e]][ridx[e]] = x[slot[e]];
@@ -229,6 +257,7 @@ static __global__ void k_put(int lp, int64_t e0, int64_t e1, const int32_t* __re
     __threadfence_system();
     for (int i = 0; i < npeers; ++i) atomicAdd_system(boards[peers[i]] + 3 * P + gp, 1);
     ticket[lp] = 0u;
+    phase_mark(D, lp, PH_EXCH);
   }
 }
 
@@ -271,6 +300,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       __syncthreads();
       if (s_stop) continue;
       any = true;
+      if (threadIdx.x == 0) phase_mark(det, lp, -1);
       const int r0 = SS.row_off[lp], n = SS.nrows[lp];
       double* sp = smem;
       double* sr = smem + n;
@@ -292,6 +322,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       block_allsum<3>(v, red);
       // a6: Eq. 2 flag + one detection step (P331-357)
       if (threadIdx.x == 0) {
+        phase_mark(det, lp, PH_RES);
         S.rt2[lp] = v[1];
         S.own2[lp] = v[2];
         const int64_t u = ++updates[lp];
@@ -310,16 +341,19 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
           h_lstop[lp] = 1;
         }
         s_stop = stop;
+        phase_mark(det, lp, PH_CHECK);
       }
       __syncthreads();
       if (s_stop) continue;
       // a3: the whole local PCG in shared memory; a4: x[S_p] += d
       const int its = v[0] != 0.0 ? block_pcg<RPT, WL, Z>(L, D, r0, n, sp, sr, sd, v[0], v[1], m, inner_tol, red) : 0;
+      if (threadIdx.x == 0) phase_mark(det, lp, PH_SOLVE);
       if (its > 0)
         for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
           const int32_t sl = __ldg(&own_slot[r0 + i]);
           if (sl >= 0) __stcg(&x[sl], __ldcg(&x[sl]) + sd[i]);
         }
+      if (threadIdx.x == 0) phase_mark(det, lp, PH_PROL);
       // a5 (multi-GPU): owner values other GPUs need, stored straight into their
       // halo storage over NVLink; then a system-scope fence and a version bump in
       // each destination's board (MPI_Put + flush analogue, P394-396)
@@ -335,6 +369,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
             atomicAdd_system(det.boards[PD.peers[k]] + 3 * det.P + det.gid[lp], 1);
         }
       }
+      if (threadIdx.x == 0) phase_mark(det, lp, PH_EXCH);
       if (threadIdx.x == 0) S.inner_total[lp] += its;
       __syncthreads();
     }
@@ -361,13 +396,7 @@ static const void* async_persistent_kernel(int rpt, bool z, int wr, int wl) {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static ras_status barrier(ras_ctx* c) {
-  if (c->world == 1) return cudaDeviceSynchronize() == cudaSuccess ? RAS_OK : set_err(c, RAS_ECUDA, "sync");
-  RAS_CUDA(c, cudaDeviceSynchronize());
-  RAS_NCCL(c, ncclAllReduce(c->d_r2_global, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
-  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  return RAS_OK;
-}
+static ras_status barrier(ras_ctx* c) { return coll_barrier(c); }
 
 // subdomain adjacency (p ~ q iff p needs a value owned by q or vice versa),
 // assembled over all ranks with one NCCL sum
@@ -380,7 +409,7 @@ static ras_status subdomain_graph(ras_ctx* c, std::vector<std::vector<int32_t>>&
   if (c->world > 1) {
     int32_t* d;
     TRY(upload(c, &d, M));
-    RAS_NCCL(c, ncclAllReduce(d, d, M.size(), ncclInt32, ncclSum, c->nccl, c->stream));
+    TRY(coll_allreduce(c, d, d, M.size(), ncclInt32, ncclSum, c->stream));
     RAS_CUDA(c, cudaMemcpyAsync(M.data(), d, M.size() * 4, cudaMemcpyDeviceToHost, c->stream));
     RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   }
@@ -427,6 +456,21 @@ static ras_status setup_ipc(ras_ctx* c, AsyncRt* A) {
   A->peer_board[c->rank] = A->board;
   A->peer_x[c->rank] = c->d_x;
   if (W == 1) return RAS_OK;
+  if (c->loopback) {  // virtual ranks on one device: the peers' windows are plain pointers
+    std::vector<int64_t> mine{(int64_t)(uintptr_t)c->d_x, (int64_t)(uintptr_t)A->board};
+    int64_t *d_mine, *d_all;
+    TRY(upload(c, &d_mine, mine));
+    TRY(zalloc(c, &d_all, (size_t)2 * W));
+    TRY(coll_allgather(c, d_mine, d_all, 2, ncclInt64, c->stream));
+    std::vector<int64_t> all((size_t)2 * W);
+    RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int r = 0; r < W; ++r) {
+      A->peer_x[r] = (double*)(uintptr_t)all[2 * r];
+      A->peer_board[r] = (int32_t*)(uintptr_t)all[2 * r + 1];
+    }
+    return RAS_OK;
+  }
   cudaIpcMemHandle_t h[2];
   RAS_CUDA(c, cudaIpcGetMemHandle(&h[0], c->d_x));
   RAS_CUDA(c, cudaIpcGetMemHandle(&h[1], A->board));
@@ -435,7 +479,7 @@ static ras_status setup_ipc(ras_ctx* c, AsyncRt* A) {
   char *d_mine, *d_all;
   TRY(upload(c, &d_mine, mine));
   TRY(zalloc(c, &d_all, sizeof(h) * W));
-  RAS_NCCL(c, ncclAllGather(d_mine, d_all, sizeof(h), ncclChar, c->nccl, c->stream));
+  TRY(coll_allgather(c, d_mine, d_all, sizeof(h), ncclInt8, c->stream));
   std::vector<char> all(sizeof(h) * W);
   RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -520,6 +564,11 @@ ras_status async_setup(ras_ctx* c) {
   D.is_parent = dip;
   D.is_root = dir;
   D.b2 = db2;
+  A->d_b2 = db2;
+  TRY(zalloc(c, &A->d_force, 1));
+  D.force = A->d_force;
+  TRY(zalloc(c, &D.phase, (size_t)std::max(nl, 1) * kNPhase));
+  TRY(zalloc(c, &D.phase_last, (size_t)std::max(nl, 1)));
   D.boards = A->d_boards;
   TRY(zalloc(c, &A->d_lstop, nl));
   TRY(zalloc(c, &A->d_updates, nl));
@@ -538,7 +587,7 @@ ras_status async_setup(ras_ctx* c) {
   if (W > 1) {
     int64_t* d;
     TRY(upload(c, &d, n_own_all));
-    RAS_NCCL(c, ncclAllReduce(d, d, W, ncclInt64, ncclSum, c->nccl, c->stream));
+    TRY(coll_allreduce(c, d, d, W, ncclInt64, ncclSum, c->stream));
     RAS_CUDA(c, cudaMemcpyAsync(n_own_all.data(), d, W * 8, cudaMemcpyDeviceToHost, c->stream));
     RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   }
@@ -572,6 +621,17 @@ ras_status async_setup(ras_ctx* c) {
   TRY(upload(c, &A->d_put_peer_off, A->put_peer_off, 1));
   A->streams.resize(nl);
   for (auto& s : A->streams) RAS_CUDA(c, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return RAS_OK;
+}
+
+ras_status async_set_b2(ras_ctx* c) {
+  AsyncRt* A = c->async;
+  if (!A || !A->d_b2) return RAS_OK;
+  std::vector<double> b2(c->nl);
+  for (int lp = 0; lp < c->nl; ++lp)
+    b2[lp] = c->opt.local_crit_owned_only ? c->plan->subs[lp].b2_owned : c->plan->subs[lp].b2;
+  RAS_CUDA(c, cudaMemcpyAsync(A->d_b2, b2.data(), b2.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   return RAS_OK;
 }
 
@@ -609,18 +669,27 @@ static ras_status enqueue_sub_sweep(ras_ctx* c, int lp, cudaStream_t s, double t
   const auto& SP = pl->subs[lp];
   const Range R = range_sub(c, lp);
   Ctl C{A->d_lstop, 1};
+  k_phase<<<1, 32, 0, s>>>(A->det, lp, -1, A->d_lstop);
   TRY(enq_residual(c, s, R, C));
   k_detect<<<1, 32, 0, s>>>(lp, A->det, c->S, tol, max_iters, A->d_lstop, A->h_lstop_dev, A->d_updates,
                             A->d_noconv);
-  c->launches += 1;
+  c->launches += 2;
   TRY(enq_pcg(c, s, R, C, m, inner_tol, exact));
+  const bool fused_prolong = c->small || c->chol || c->path == RAS_PCG_RESIDENT;
+  if (!fused_prolong) {
+    k_phase<<<1, 32, 0, s>>>(A->det, lp, PH_SOLVE, A->d_lstop);
+    c->launches += 1;
+  }
   TRY(enq_prolong(c, s, R, C));
+  k_phase<<<1, 32, 0, s>>>(A->det, lp, fused_prolong ? PH_SOLVE : PH_PROL, A->d_lstop);
+  c->launches += 1;
   const int64_t e0 = A->put_off[lp], e1 = A->put_off[lp + 1];
   if (e1 > e0) {
     const unsigned pg = (unsigned)std::min<int64_t>((e1 - e0 + 255) / 256, 148 * 4);
     k_put<<<pg, 256, 0, s>>>(lp, e0, e1, A->d_put_slot, A->d_put_rank, A->d_put_ridx, c->d_x, A->d_peer_x,
                              A->d_put_ticket, A->d_put_peers + A->put_peer_off[lp],
-                             A->put_peer_off[lp + 1] - A->put_peer_off[lp], A->d_boards, pl->P, SP.p, A->d_lstop);
+                             A->put_peer_off[lp + 1] - A->put_peer_off[lp], A->d_boards, pl->P, SP.p, A->d_lstop,
+                             A->det);
     c->launches += 1;
   }
   return RAS_OK;
@@ -733,7 +802,9 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_SMALL, smem));
   RAS_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   if (per_sm < 1) return set_err(c, RAS_ESTATE, "persistent async kernel does not fit an SM");
-  int G = std::min(nl, per_sm * sms);
+  // loopback virtual ranks share one device: each persistent grid gets 1/world of
+  // it so that every rank's CTAs are resident at once (they wait on each other's flags)
+  int G = std::min(nl, std::max(1, per_sm * sms / (c->loopback ? c->world : 1)));
   *A->h_kill = 0;
   int nl_ = nl;
   Sell Rm = c->R, L = c->L;
@@ -873,6 +944,7 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
   const bool kt = c->kt.on;
   c->kt.on = false;  // per-kernel event timing is a sync-mode (single stream) facility
   RAS_CUDA(c, cudaMemsetAsync(A->d_updates, 0, nl * 8, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(A->det.phase, 0, (size_t)nl * kNPhase * 8, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   ras_status st = RAS_OK;
   double rel = INFINITY;
@@ -880,6 +952,10 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
   bool noconv_any = false, timeout = false;
   const double t0 = now_s();
   for (;;) {
+    {
+      const int32_t f = (c->opt.force_first_stop && resumes == 0) ? 1 : 0;
+      RAS_CUDA(c, cudaMemcpyAsync(A->d_force, &f, 4, cudaMemcpyHostToDevice, c->stream));
+    }
     TRY(reset_detection(c));
     if (c->opt.scripted_flags) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
@@ -905,10 +981,7 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
     noconv_any = local_nc || timeout;
     if (c->world > 1) {  // agree on "someone hit max_iters / the watchdog"
       double f = noconv_any ? 1.0 : 0.0;
-      RAS_CUDA(c, cudaMemcpy(c->d_r2_global, &f, 8, cudaMemcpyHostToDevice));
-      RAS_NCCL(c, ncclAllReduce(c->d_r2_global, c->d_r2_global, 1, ncclDouble, ncclMax, c->nccl, c->stream));
-      RAS_CUDA(c, cudaMemcpyAsync(&f, c->d_r2_global, 8, cudaMemcpyDeviceToHost, c->stream));
-      RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+      TRY(coll_allreduce_f64(c, &f, 1, true));
       noconv_any = f != 0.0;
     }
     if (rel < tol || noconv_any || c->opt.scripted_flags || resumes >= c->opt.max_resumes) break;
@@ -938,6 +1011,17 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
   int64_t fresh = 0;
   for (int v : ver) fresh += v;
   c->st.fresh_halo_reads = fresh;
+  // per-phase device time, summed over each subdomain's updates, mean over the local subdomains
+  std::vector<double> ph((size_t)nl * kNPhase);
+  RAS_CUDA(c, cudaMemcpy(ph.data(), A->det.phase, ph.size() * 8, cudaMemcpyDeviceToHost));
+  double tot[kNPhase] = {};
+  for (int lp = 0; lp < nl; ++lp)
+    for (int k = 0; k < kNPhase; ++k) tot[k] += ph[(size_t)lp * kNPhase + k] / nl;
+  c->st.t_residual = tot[PH_RES];
+  c->st.t_local_solve = tot[PH_SOLVE];
+  c->st.t_prolong = tot[PH_PROL];
+  c->st.t_exchange = tot[PH_EXCH];
+  c->st.t_convcheck = tot[PH_CHECK];
   if (c->st.converged) return RAS_OK;
   if (noconv_any || c->opt.scripted_flags) return RAS_ENOCONV;
   return set_err(c, RAS_EVERIFY,

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -21,7 +22,15 @@ struct DevBuf {
   bool raw = false;  // cudaMalloc'd IPC-capable window (never through the allocator hook)
 };
 
-struct AsyncRt;  // async-mode runtime (async.cu)
+struct AsyncRt;    // async-mode runtime (async.cu)
+struct LoopGroup;  // loopback transport group (comm.cu)
+
+// one side of a point-to-point transfer (device buffer, element count)
+struct Xfer {
+  int peer;
+  void* buf;
+  size_t count;
+};
 
 enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_ZDOT, K_SMALL, K_RESID, K_BAND, K_NKINDS };
 
@@ -66,6 +75,9 @@ struct ras_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ncclComm_t nccl = nullptr;
+  std::shared_ptr<ras::LoopGroup> loop;  // loopback transport (ras_comm.transport); null = NCCL
+  std::string loop_key;
+  bool loopback = false;
   void* (*dev_alloc)(size_t, void*) = nullptr;
   void (*dev_free)(void*, void*) = nullptr;
   void* alloc_user = nullptr;
@@ -159,6 +171,17 @@ ras_status set_err(ras_ctx* c, ras_status s, const std::string& m);
 ras_status cuda_err(ras_ctx* c, cudaError_t e, const char* what);
 void* dalloc(ras_ctx* c, size_t bytes);
 void* dalloc_raw(ras_ctx* c, size_t bytes);
+void dfree(ras_ctx* c, void* p);
+// collectives over the context's ranks (comm.cu): NCCL, or the loopback group
+ras_status loop_join(ras_ctx* c, const void* key128);
+void loop_leave(ras_ctx* c);
+ras_status coll_allreduce(ras_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t dt, ncclRedOp_t op,
+                          cudaStream_t s);
+ras_status coll_allgather(ras_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t dt, cudaStream_t s);
+ras_status coll_sendrecv(ras_ctx* c, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, ncclDataType_t dt,
+                         cudaStream_t s);
+ras_status coll_allreduce_f64(ras_ctx* c, double* v, int n, bool is_max);  // host values, in place
+ras_status coll_barrier(ras_ctx* c);  // device drained on every rank
 ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters);
 int kt_begin(ras_ctx* c, cudaStream_t s);
 void kt_end(ras_ctx* c, cudaStream_t s, int kind, int idx);
@@ -168,6 +191,7 @@ ras_status enq_residual(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C);
 ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, double inner_tol, bool exact);
 ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C);
 ras_status async_setup(ras_ctx* c);
+ras_status async_set_b2(ras_ctx* c);  // re-upload the Eq. 2 ||b~_p||^2 after ras_set_rhs
 void async_free(ras_ctx* c);
 }  // namespace ras
 
@@ -183,8 +207,12 @@ inline ras_status upload(ras_ctx* c, T** dst, const std::vector<T>& src, size_t 
   size_t n = std::max(src.size(), min_elems);
   *dst = (T*)dalloc(c, n * sizeof(T));
   if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
-  if (!src.empty() && cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
-    return set_err(c, RAS_ECUDA, "cudaMemcpy (upload) failed");
+  // on the library stream (the one NCCL and the kernels use), completed before
+  // return: the host vector may die and a collective may read *dst right away
+  if (!src.empty() &&
+      (cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+       cudaStreamSynchronize(c->stream) != cudaSuccess))
+    return set_err(c, RAS_ECUDA, "cudaMemcpyAsync (upload) failed");
   return RAS_OK;
 }
 
@@ -192,8 +220,9 @@ template <class T>
 inline ras_status zalloc(ras_ctx* c, T** dst, size_t n) {
   *dst = (T*)dalloc(c, n * sizeof(T));
   if (!*dst) return set_err(c, RAS_ENOMEM, "device allocation failed");
-  if (cudaMemset(*dst, 0, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess)
-    return set_err(c, RAS_ECUDA, "cudaMemset failed");
+  // stream-ordered before any later kernel / collective on the library stream
+  if (cudaMemsetAsync(*dst, 0, std::max<size_t>(n, 1) * sizeof(T), c->stream) != cudaSuccess)
+    return set_err(c, RAS_ECUDA, "cudaMemsetAsync failed");
   return RAS_OK;
 }
 

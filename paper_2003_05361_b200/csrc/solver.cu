@@ -54,11 +54,26 @@ void* dalloc(ras_ctx* c, size_t bytes) {
 
 // Always cudaMalloc (a base allocation that can be exported as a CUDA IPC
 // window to the peer GPUs: x storage and the detector board).
+void dfree(ras_ctx* c, void* p) {
+  for (size_t i = 0; i < c->bufs.size(); ++i)
+    if (c->bufs[i].ptr == p) {
+      if (c->dev_free && !c->bufs[i].raw)
+        c->dev_free(p, c->alloc_user);
+      else
+        cudaFree(p);
+      c->bufs.erase(c->bufs.begin() + i);
+      return;
+    }
+}
+
 void* dalloc_raw(ras_ctx* c, size_t bytes) {
   bytes = std::max<size_t>(256, (bytes + 255) / 256 * 256);
   void* p = nullptr;
   if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-  cudaMemset(p, 0, bytes);
+  if (cudaMemsetAsync(p, 0, bytes, c->stream) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    cudaFree(p);
+    return nullptr;
+  }
   c->bufs.push_back(DevBuf{p, bytes, true});
   return p;
 }
@@ -74,7 +89,7 @@ static ras_status exchange_requests(ras_ctx* c) {
   int64_t *d_counts = nullptr, *d_all = nullptr;
   TRY(upload(c, &d_counts, my_counts));
   TRY(zalloc(c, &d_all, (size_t)W * W));
-  RAS_NCCL(c, ncclAllGather(d_counts, d_all, W, ncclInt64, c->nccl, c->stream));
+  TRY(coll_allgather(c, d_counts, d_all, W, ncclInt64, c->stream));
   std::vector<int64_t> all((size_t)W * W);
   RAS_CUDA(c, cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -86,15 +101,15 @@ static ras_status exchange_requests(ras_ctx* c) {
   TRY(zalloc(c, &d_inc, std::max<int64_t>(tot_in, 1)));
   std::vector<int64_t> inc_off(W + 1, 0);
   for (int q = 0; q < W; ++q) inc_off[q + 1] = inc_off[q] + all[(size_t)q * W + me];
-  RAS_NCCL(c, ncclGroupStart());
+  std::vector<Xfer> snd, rcv;
   for (int r = 0; r < W; ++r) {
     if (r == me) continue;
     const int64_t cnt = pl->halo_off[r + 1] - pl->halo_off[r];
-    if (cnt) RAS_NCCL(c, ncclSend(d_req + pl->halo_off[r], cnt, ncclInt64, r, c->nccl, c->stream));
+    if (cnt) snd.push_back(Xfer{r, d_req + pl->halo_off[r], (size_t)cnt});
     const int64_t inc = all[(size_t)r * W + me];
-    if (inc) RAS_NCCL(c, ncclRecv(d_inc + inc_off[r], inc, ncclInt64, r, c->nccl, c->stream));
+    if (inc) rcv.push_back(Xfer{r, d_inc + inc_off[r], (size_t)inc});
   }
-  RAS_NCCL(c, ncclGroupEnd());
+  TRY(coll_sendrecv(c, snd, rcv, ncclInt64, c->stream));
   std::vector<int64_t> inc(std::max<int64_t>(tot_in, 1));
   RAS_CUDA(c, cudaMemcpyAsync(inc.data(), d_inc, inc.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -625,7 +640,11 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
     c->dev_free = comm->dev_free;
     c->alloc_user = comm->alloc_user;
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return set_err(c, RAS_EINVAL, "bad rank/world");
-    if (c->world > 1 && !comm->nccl_unique_id) return set_err(c, RAS_EINVAL, "world > 1 needs nccl_unique_id");
+    if (c->world > 1 && !comm->nccl_unique_id)
+      return set_err(c, RAS_EINVAL, "world > 1 needs nccl_unique_id (the loopback group key in loopback mode)");
+    if (comm->transport != RAS_TRANSPORT_NCCL && comm->transport != RAS_TRANSPORT_LOOPBACK)
+      return set_err(c, RAS_EINVAL, "unknown ras_comm.transport");
+    c->loopback = c->world > 1 && comm->transport == RAS_TRANSPORT_LOOPBACK;
     RAS_CUDA(c, cudaSetDevice(c->device));
   } else {
     RAS_CUDA(c, cudaGetDevice(&c->device));
@@ -642,9 +661,13 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
   ras_status s = ras_plan_build(&c->plan, A, b, part, overlap, c->rank, c->world);
   if (s != RAS_OK) return set_err(c, s, tls_error());
   if (c->world > 1) {
-    ncclUniqueId id;
-    std::memcpy(&id, comm->nccl_unique_id, sizeof(id));
-    RAS_NCCL(c, ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+    if (c->loopback) {
+      TRY(loop_join(c, comm->nccl_unique_id));
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, comm->nccl_unique_id, sizeof(id));
+      RAS_NCCL(c, ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+    }
     TRY(exchange_requests(c));
   } else {
     // nothing to exchange: single rank
@@ -658,14 +681,7 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
   TRY(upload_plan(c));
   // ||b||^2 over all ranks (owned rows), fixed order on one rank, NCCL sum across ranks
   c->b2_global = c->plan->b2_global_local;
-  if (c->world > 1) {
-    std::vector<double> v{c->b2_global};
-    double* d;
-    TRY(upload(c, &d, v));
-    RAS_NCCL(c, ncclAllReduce(d, d, 1, ncclDouble, ncclSum, c->nccl, c->stream));
-    RAS_CUDA(c, cudaMemcpyAsync(&c->b2_global, d, 8, cudaMemcpyDeviceToHost, c->stream));
-    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  }
+  TRY(coll_allreduce_f64(c, &c->b2_global, 1, false));
   if (c->opt.local_solver == RAS_LS_IC0_PCG || c->opt.local_solver == RAS_LS_ILU0_PCG) {
     TRY(upload_factors(c));
   } else if (c->opt.local_solver == RAS_LS_CHOLESKY) {
@@ -1094,28 +1110,52 @@ ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C) {
 
 // check_only: the sweep at k == max_iters only evaluates x^{max_iters} (the
 // device stops there whatever the residual), so its local solve is not enqueued.
+// Phase events of one sync sweep (ras_stats_t t_*): boundaries recorded on the
+// library stream, read back when the host next waits on the sweep's slot.
+struct PhaseEv {
+  cudaEvent_t e[6];  // start | residual | convcheck | local solve | prolong | exchange
+  int n = 0;         // boundaries recorded in the sweep (3 for a check-only sweep)
+};
+
+static void phase_collect(ras_ctx* c, PhaseEv& P) {
+  double* t[5] = {&c->st.t_residual, &c->st.t_convcheck, &c->st.t_local_solve, &c->st.t_prolong, &c->st.t_exchange};
+  for (int i = 0; i + 1 < P.n; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, P.e[i], P.e[i + 1]) == cudaSuccess) *t[i] += 1e-3 * ms;
+  }
+  P.n = 0;
+}
+
 static ras_status sync_sweep(ras_ctx* c, double tol, int64_t max_iters, int m, double inner_tol, bool exact, int slot,
-                             bool check_only) {
+                             bool check_only, PhaseEv& P) {
   Ctl C{c->d_stop, 0};
   const Range R = range_all(c);
+  RAS_CUDA(c, cudaEventRecord(P.e[0], c->stream));
   // a1+a2
   TRY(enq_residual(c, c->stream, R, C));
+  RAS_CUDA(c, cudaEventRecord(P.e[1], c->stream));
   // a6 (global criterion on x^k, P344-346)
   LAUNCH(K_CTRL, k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local));
   const double* r2g = c->d_r2_local;
   if (c->world > 1) {
-    RAS_NCCL(c, ncclAllReduce(c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    TRY(coll_allreduce(c, c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->stream));
     r2g = c->d_r2_global;
   }
   LAUNCH(K_CTRL, k_sync_check<<<1, 32, 0, c->stream>>>(r2g, c->b2_global, tol, max_iters, c->d_sync, c->d_stop,
                                                        c->h_stop_dev + slot));
+  RAS_CUDA(c, cudaEventRecord(P.e[2], c->stream));
+  P.n = 3;
   if (check_only) return RAS_OK;
-  // a3
+  // a3 (BLOCK / RESIDENT / direct: the prolongation is fused into the same launch)
   TRY(enq_pcg(c, c->stream, R, C, m, inner_tol, exact));
+  RAS_CUDA(c, cudaEventRecord(P.e[3], c->stream));
   // a4
   TRY(enq_prolong(c, c->stream, R, C));
+  RAS_CUDA(c, cudaEventRecord(P.e[4], c->stream));
   // a5
   TRY(exchange(c, C));
+  RAS_CUDA(c, cudaEventRecord(P.e[5], c->stream));
+  P.n = 6;
   RAS_CUDA(c, cudaGetLastError());
   return RAS_OK;
 }
@@ -1128,16 +1168,13 @@ static ras_status exchange(ras_ctx* c, Ctl C) {
     LAUNCH(K_PACK, k_pack<<<(unsigned)std::min<int64_t>((c->n_send + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
                        c->n_send, c->d_send_slot, c->d_x, c->d_sendbuf, C));
   }
-  RAS_NCCL(c, ncclGroupStart());
+  std::vector<Xfer> snd, rcv;
   for (int r = 0; r < c->world; ++r) {
     if (r == c->rank) continue;
-    if (c->send_cnt[r])
-      RAS_NCCL(c, ncclSend(c->d_sendbuf + c->send_off[r], c->send_cnt[r], ncclDouble, r, c->nccl, c->stream));
-    if (c->recv_cnt[r])
-      RAS_NCCL(c, ncclRecv(c->d_x + c->n_own + c->recv_off[r], c->recv_cnt[r], ncclDouble, r, c->nccl, c->stream));
+    if (c->send_cnt[r]) snd.push_back(Xfer{r, c->d_sendbuf + c->send_off[r], (size_t)c->send_cnt[r]});
+    if (c->recv_cnt[r]) rcv.push_back(Xfer{r, c->d_x + c->n_own + c->recv_off[r], (size_t)c->recv_cnt[r]});
   }
-  RAS_NCCL(c, ncclGroupEnd());
-  return RAS_OK;
+  return coll_sendrecv(c, snd, rcv, ncclFloat64, c->stream);
 }
 
 ras_status sync_exchange(ras_ctx* c) { return exchange(c, Ctl{nullptr, 0}); }
@@ -1150,7 +1187,7 @@ ras_status global_residual(ras_ctx* c, double* rel) {
   LAUNCH(K_CTRL, k_sum_own<<<1, 32, 0, c->stream>>>(c->nl, c->S.own2, c->d_r2_local));
   const double* r2g = c->d_r2_local;
   if (c->world > 1) {
-    RAS_NCCL(c, ncclAllReduce(c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    TRY(coll_allreduce(c, c->d_r2_local, c->d_r2_global, 1, ncclDouble, ncclSum, c->stream));
     r2g = c->d_r2_global;
   }
   double r2 = 0.0;
@@ -1198,7 +1235,7 @@ static ras_status gather(ras_ctx* c, double* x_out) {
   const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n_own + 255) / 256, 148 * 16));
   LAUNCH(K_CTRL, k_gather_x<<<g, 256, 0, c->stream>>>(c->n_own, c->d_own_gid, c->d_x, c->d_xglob));
   if (c->world > 1)
-    RAS_NCCL(c, ncclAllReduce(c->d_xglob, c->d_xglob, (size_t)pl->n, ncclDouble, ncclSum, c->nccl, c->stream));
+    TRY(coll_allreduce(c, c->d_xglob, c->d_xglob, (size_t)pl->n, ncclDouble, ncclSum, c->stream));
   RAS_CUDA(c, cudaMemcpyAsync(x_out, c->d_xglob, (size_t)pl->n * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   return RAS_OK;
@@ -1218,6 +1255,9 @@ static ras_status solve_sync(ras_ctx* c, double tol, int64_t max_iters) {
   if (Q > 32) return set_err(c, RAS_EINVAL, "poll_interval must be <= 32");
   std::vector<cudaEvent_t> ev(Q);
   for (auto& e : ev) RAS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  std::vector<PhaseEv> ph(Q);
+  for (auto& P : ph)
+    for (auto& e : P.e) RAS_CUDA(c, cudaEventCreate(&e));
   for (int i = 0; i < 32; ++i) c->h_stop[i] = 0;
   ras_status st = RAS_OK;
   for (int64_t k = 0;; ++k) {
@@ -1227,14 +1267,19 @@ static ras_status solve_sync(ras_ctx* c, double tol, int64_t max_iters) {
         st = cuda_err(c, cudaGetLastError(), "sweep");
         break;
       }
+      phase_collect(c, ph[slot]);
       if (((volatile int32_t*)c->h_stop)[slot]) break;
     }
     if (k > max_iters) break;  // sweep max_iters only checks x^{max_iters}; the device stops there
-    st = sync_sweep(c, tol, max_iters, m, inner_tol, exact, slot, k == max_iters);
+    st = sync_sweep(c, tol, max_iters, m, inner_tol, exact, slot, k == max_iters, ph[slot]);
     if (st != RAS_OK) break;
     RAS_CUDA(c, cudaEventRecord(ev[slot], c->stream));
   }
   cudaStreamSynchronize(c->stream);
+  for (auto& P : ph) {
+    phase_collect(c, P);
+    for (auto& e : P.e) cudaEventDestroy(e);
+  }
   for (auto& e : ev) cudaEventDestroy(e);
   return st;
 }
@@ -1246,6 +1291,11 @@ using namespace ras;
 extern "C" {
 
 int32_t ras_abi_version(void) { return RAS_ABI_VERSION; }
+
+#ifndef RAS_BUILD_HASH
+#define RAS_BUILD_HASH "unstamped"
+#endif
+const char* ras_build_hash(void) { return RAS_BUILD_HASH; }
 
 ras_status ras_options_default(ras_options* o) {
   if (!o) return RAS_EINVAL;
@@ -1291,23 +1341,29 @@ ras_status ras_setup(ras_ctx** out, const ras_csr* A, const double* b, const ras
 
 ras_status ras_set_rhs(ras_ctx* c, const double* b) {
   if (!c || !b) return RAS_EINVAL;
+  RAS_CUDA(c, cudaSetDevice(c->device));
   ras_plan* pl = c->plan;
   std::vector<double> bl(pl->rows_pad, 0.0);
+  // same accumulation order as the plan (per-subdomain sums, then the owned total)
   double b2 = 0.0;
-  for (auto& S : pl->subs)
+  for (auto& S : pl->subs) {
+    S.b2 = S.b2_owned = 0.0;
     for (int64_t i = 0; i < S.nrows; ++i) {
       const double v = b[S.omega[i] - pl->row_begin];
       bl[S.row_off + i] = v;
-      if (S.owned[i]) b2 += v * v;
+      S.b2 += v * v;
+      if (S.owned[i]) S.b2_owned += v * v;
     }
-  RAS_CUDA(c, cudaMemcpy(c->d_b, bl.data(), bl.size() * 8, cudaMemcpyHostToDevice));
-  c->b2_global = b2;
-  if (c->world > 1) {
-    RAS_CUDA(c, cudaMemcpy(c->d_r2_global, &b2, 8, cudaMemcpyHostToDevice));
-    RAS_NCCL(c, ncclAllReduce(c->d_r2_global, c->d_r2_global, 1, ncclDouble, ncclSum, c->nccl, c->stream));
-    RAS_CUDA(c, cudaMemcpyAsync(&c->b2_global, c->d_r2_global, 8, cudaMemcpyDeviceToHost, c->stream));
-    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+    b2 += S.b2_owned;
   }
+  pl->b_loc = bl;
+  pl->b2_global_local = b2;
+  RAS_CUDA(c, cudaMemcpyAsync(c->d_b, bl.data(), bl.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->b2_global = b2;
+  if (c->world > 1) TRY(coll_allreduce_f64(c, &c->b2_global, 1, false));
+  // async Eq. 2 compares against the per-subdomain ||b~_p||^2 (or the owned-only variant)
+  TRY(async_set_b2(c));
   return RAS_OK;
 }
 
@@ -1351,11 +1407,11 @@ static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   c->st.num_subdomains = c->plan->P;
   c->st.world = c->world;
   c->st.local_subdomains = c->nl;
-  c->st.pcg_path = c->chol ? RAS_PCG_BLOCK
-                  : c->ic  ? RAS_PCG_TILED
-                  : c->small ? RAS_PCG_BLOCK
-                  : mode == RAS_SYNC ? c->path
-                                     : RAS_PCG_TILED;
+  // the path both modes ran on: async BLOCK-sized subdomains use k_small_pcg (streams)
+  // or its block_pcg (persistent kernel), RESIDENT-sized ones the sequential on-chip
+  // schedule (R34), everything else the streaming kernels
+  c->st.pcg_path = c->chol ? RAS_PCG_BLOCK : c->ic ? RAS_PCG_TILED : c->path;
+  c->st.resident_pattern = c->path == RAS_PCG_RESIDENT && c->resid_pat;
   c->st.rows_local = c->plan->rows_local;
   c->st.halo_values = c->n_halo;
   c->st.kernel_launches = c->launches;
@@ -1481,6 +1537,7 @@ void ras_free(ras_ctx* c) {
   if (c->h_stop) cudaFreeHost(c->h_stop);
   if (c->h_nactive) cudaFreeHost(c->h_nactive);
   if (c->nccl) ncclCommDestroy(c->nccl);
+  loop_leave(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   ras_plan_free(c->plan);
   delete c;

@@ -194,7 +194,9 @@ class Solver:
 
     A: full CSR (ras_inputs.CSR / scipy) or a row window with .row0 / .n.
     b: RHS for the same rows as A.  owner: len-n owner array.
-    comm: None (1 GPU) or dict(rank, world, device, nccl_id=bytes, stream=int).
+    comm: None (1 GPU) or dict(rank, world, device, nccl_id=bytes, stream=int, transport="nccl"|"loopback").
+    Loopback (ras_comm.transport): `world` virtual ranks on one device, one host thread per
+    rank; nccl_id is then any 128-byte group key shared by the group's ranks.
     """
 
     def __init__(self, A, b, owner, overlap, opts=None, comm=None, num_subdomains=None, sub_to_rank=None):
@@ -213,6 +215,7 @@ class Solver:
                 self._id = C.create_string_buffer(bytes(comm["nccl_id"]), 128)
                 cm.nccl_unique_id = C.cast(self._id, C.c_void_p)
             cm.cuda_stream = comm.get("stream") or None
+            cm.transport = F.RAS_TRANSPORT_LOOPBACK if comm.get("transport") == "loopback" else F.RAS_TRANSPORT_NCCL
             self.rank, self.world = cm.rank, cm.world
         else:
             self.rank, self.world = 0, 1

@@ -30,6 +30,7 @@ __all__ = [
     "laplace_3d_rows",
     "rhs",
     "rhs_rows",
+    "varcoef_2d",
     "voronoi_partition",
     "read_partition_file",
     "write_partition_file",
@@ -132,6 +133,33 @@ def laplace_3d(nx: int, ny: int | None = None, nz: int | None = None) -> CSR:
 
 def laplace_3d_rows(nx: int, ny: int, nz: int, r0: int, r1: int) -> CSR:
     return _stencil_rows(r0, r1, (nx, ny, nz), 6.0)
+
+
+def varcoef_2d(nx: int, ny: int, levels=(1.0, 2.0, 3.0, 4.0), seed: int = 3) -> CSR:
+    """Variable-coefficient 5-point diffusion on an nx-by-ny grid: an irregular
+    sparse SPD M-matrix of the paper's problem class (A x = b, A sparse SPD,
+    P114-118) for exercising the matrix formats, not one of its workloads.
+
+    Every grid edge (x,y)-(x+1,y) / (x,y)-(x,y+1) and every Dirichlet boundary
+    edge gets a weight drawn uniformly from `levels` (default_rng(seed)); row i
+    holds -w_e for each interior edge e at i and, on the diagonal, the sum of
+    the weights of all four edges at i (the 2D Laplacian is every w_e = 1).
+    Few distinct values, many distinct rows."""
+    rng = np.random.default_rng(seed)
+    lv = np.asarray(levels, dtype=np.float64)
+    wx = lv[rng.integers(0, len(lv), size=(ny, nx + 1))]  # wx[y, x]: edge left of (x, y); x = nx: right boundary
+    wy = lv[rng.integers(0, len(lv), size=(ny + 1, nx))]  # wy[y, x]: edge below (x, y); y = ny: top boundary
+    n = nx * ny
+    yy, xx = np.divmod(np.arange(n, dtype=np.int64), nx)
+    diag = wx[yy, xx] + wx[yy, xx + 1] + wy[yy, xx] + wy[yy + 1, xx]
+    # column slots ascending: -nx, -1, 0, +1, +nx
+    offs = np.array([-nx, -1, 0, 1, nx], dtype=np.int64)
+    M = np.stack([yy > 0, xx > 0, np.ones(n, bool), xx < nx - 1, yy < ny - 1], axis=1)
+    V = np.stack([-wy[yy, xx], -wx[yy, xx], diag, -wx[yy, xx + 1], -wy[yy + 1, xx]], axis=1)
+    cols = np.arange(n, dtype=np.int64)[:, None] + offs[None, :]
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(M.sum(axis=1), out=indptr[1:])
+    return CSR(indptr, cols[M].astype(np.int32), V[M], n, 0)
 
 
 def rhs(n: int, seed: int = 0) -> np.ndarray:

@@ -100,3 +100,48 @@ def test_async_3d(kind):
     st, x = s.solve(1e-8, 20000, "async")
     assert st == 0 and O.verify_global(A, x, b, 1e-8)[0]
     s.close()
+
+
+@pytest.mark.parametrize("path", ["block", "tiled"])
+def test_set_rhs_async_uses_new_eq2_norms(path):
+    # ras_set_rhs must refresh the per-subdomain ||b~_p||^2 that the async Eq. 2
+    # flags compare against (P337-340): with a 1000x larger RHS the old norms would
+    # let the flags fire far too late / the new ones must still verify first time
+    A, b, owner, gamma, m = setup()
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, path=path, max_resumes=0))
+    b2 = 1e3 * ri.rhs(A.n, 7)
+    s.set_rhs(b2)
+    st, x = s.solve(1e-8, 50000, "async")
+    stt = s.stats()
+    assert st == 0 and stt["resumes"] == 0, stt
+    assert O.verify_global(A, x, b2, 1e-8)[0]
+    # and back to a small RHS: stale (large) norms would stop at once and fail verification
+    s.set_rhs(1e-3 * b)
+    st, x = s.solve(1e-8, 50000, "async")
+    assert st == 0 and s.stats()["resumes"] == 0
+    assert O.verify_global(A, x, 1e-3 * b, 1e-8)[0]
+    s.close()
+
+
+@pytest.mark.parametrize("mode", ["sync", "async"])
+@pytest.mark.parametrize("path", ["block", "tiled", "resident"])
+def test_phase_times_populated(mode, path):
+    # ras_stats_t per-phase times (Figs. 3a-7a): nonzero where the phase runs, and
+    # (sync) their sum is the device part of the time to solution
+    N, P = (48, 6) if path != "resident" else (200, 4)
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 0)
+    owner = ri.voronoi_partition(N, N, P, seed=5) if path != "resident" else O.partition_regular(N, N, 1, 2, 2, 1)
+    s = R.Solver(A, b, owner, 2, R.options("jacobi", 8, path=path))
+    st, x = s.solve(1e-8, 50000, mode)
+    t = s.stats()
+    assert st == 0
+    assert t["t_residual"] > 0 and t["t_local_solve"] > 0 and t["t_convcheck"] > 0
+    assert t["t_exchange"] >= 0 and t["t_prolong"] >= 0
+    if path == "tiled":
+        assert t["t_prolong"] > 0  # separate k_prolong (fused into the solve kernel on BLOCK / RESIDENT)
+    tot = t["t_residual"] + t["t_local_solve"] + t["t_prolong"] + t["t_exchange"] + t["t_convcheck"]
+    assert tot <= 1.05 * t["time_to_solution_s"] + 1e-3
+    if mode == "sync":
+        assert tot >= 0.5 * t["time_to_solution_s"], t
+    s.close()

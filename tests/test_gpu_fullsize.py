@@ -70,3 +70,40 @@ def test_c2_reported_residual_matches_host_recomputation(c2):
     host = np.linalg.norm(b - As @ x) / np.linalg.norm(b)
     assert abs(stats["final_rel_residual"] - host) <= 1e-10 * host
     assert host < 1.0
+
+
+def test_c2_second_sweep_matches_oracle_on_interior_subdomain(c2):
+    # sweep 2 element by element on the interior subdomain p = 5: x^2[S_p] =
+    # x^1[S_p] + delta_p[S_p], delta_p = PCG_m(A_p, r~_p(x^1)), where x^1 on
+    # Omega_p u Gamma_p comes from the first-sweep local solves of p and of its
+    # eight neighbours (every owner of a value p reads; P147-153, P294-297)
+    A, b, owner, s = c2
+    st, x2 = s.solve(1e-300, 2, "sync")
+    assert s.stats()["sweeps"] == 2
+    As = O.as_scipy(A)
+    oowner = O.partition_regular(NX, NY, 1, PX, PY, 1)
+    zero = np.zeros(NX * NY)
+
+    def sub_of(q):
+        om, ow, gh = O.overlap_sets(As, oowner, q, GAMMA)
+        rows = As[om]
+        sb = O.Subdomain(q, om, ow, gh, rows[:, om].tocsr(), rows[:, gh].tocsr(), b[om].copy())
+        O.make_local_solver(sb, "jacobi", M)
+        return sb
+
+    p = 5
+    # owners of Omega_5 u Gamma_5: p and its 8 neighbours in the 4x4 block grid
+    sp_ = sub_of(p)
+    need = np.concatenate([sp_.omega, sp_.ghosts])
+    owners = np.unique(oowner[need])
+    assert len(owners) == 9
+    x1 = np.zeros(NX * NY)
+    for q in owners:
+        sq = sp_ if q == p else sub_of(q)
+        d = sq.solver(O.local_residual(sq, zero))
+        x1[sq.owned_global] = d[sq.owned]
+    d2 = sp_.solver(O.local_residual(sp_, x1))
+    ref = x1[sp_.owned_global] + d2[sp_.owned]
+    got = x2[sp_.owned_global]
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= 1e-10, err

@@ -57,3 +57,34 @@ def test_ic0_converges_sync_and_async():
         assert st == 0, mode
         assert O.verify_global(A, x, b, 1e-8)[0]
     s.close()
+
+
+@pytest.mark.parametrize("kind", ["ic0", "ilu0"])
+@pytest.mark.parametrize("case", ["3d", "2d"])
+def test_ic_multi_chunk_levels_match_oracle(kind, case):
+    # levels wider than one 256-row chunk of k_trsv: the level-wait across >= 2
+    # chunks per level (P320-323 level-set solves).  3D 64^3 in 2x2x2 with
+    # overlap 2: 34^3-row subdomains whose widest level has ~870 rows (4 chunks);
+    # 2D 600^2 in 2x2: 302^2-row subdomains, levels up to 302 rows (2 chunks).
+    if case == "3d":
+        A = ri.laplace_3d(64)
+        owner = O.partition_regular(64, 64, 64, 2, 2, 2)
+        gamma, m, K = 2, 3, 2
+    else:
+        A = ri.laplace_2d(600)
+        owner = O.partition_regular(600, 600, 1, 2, 2, 1)
+        gamma, m, K = 2, 3, 2
+    b = ri.rhs(A.n, 0)
+    subs = O.setup(A, b, owner, gamma)
+    for s in subs:
+        O.make_local_solver(s, kind, m)
+    # the premise: some level of the forward solve spans more than one chunk
+    L0 = subs[0].extra["L"]
+    widest = np.bincount(O.level_sets(L0, lower=True)).max()
+    assert widest > 256, widest
+    ref = O.ras_sync(A, b, subs, 1e-300, K, record_iterates=True)
+    s = R.Solver(A, b, owner, gamma, R.options(kind, m))
+    for k in (1, K):
+        st, x = s.solve(1e-300, k, "sync")
+        assert rel(x, ref.iterates[k]) <= 1e-10, (kind, case, k, rel(x, ref.iterates[k]))
+    s.close()

@@ -109,3 +109,16 @@ def test_rhs_rows_window_equals_slice():
     full = ri.rhs(5000, 3)
     assert np.array_equal(ri.rhs_rows(5000, 1234, 4321, 3), full[1234:4321])
     assert np.array_equal(ri.rhs_rows(5000, 0, 5000, 3), full)
+
+
+def test_varcoef_2d_is_spd_m_matrix_and_reduces_to_laplacian():
+    A = ri.varcoef_2d(9, 7, seed=4)
+    S = A.to_scipy().toarray()
+    assert np.array_equal(S, S.T)
+    off = S - np.diag(np.diag(S))
+    assert (off <= 0).all()  # M-matrix sign pattern
+    # strictly diagonally dominant on boundary rows, weakly inside: SPD
+    assert (np.diag(S) >= -off.sum(axis=1)).all() and np.linalg.eigvalsh(S).min() > 0
+    assert len(np.unique(A.data)) <= 4 + 13  # few distinct values (4 weights, sums of 4 of them)
+    one = ri.varcoef_2d(6, 5, levels=(1.0,))
+    np.testing.assert_array_equal(one.to_scipy().toarray(), ri.laplace_2d(6, 5).to_scipy().toarray())

@@ -78,3 +78,36 @@ def test_bfs_tree_and_default_central_tree():
     adj = [[1, 2], [0, 3], [0, 3], [1, 2]]
     assert O.bfs_tree(adj) == [-1, 0, 0, 1]
     assert O.default_central_tree([0, 0, 1, 1, 2]) == [-1, 0, 0, 2, 0]
+
+
+def test_tree_depth_and_diameter_hand_values():
+    # Hand-computed on explicit trees (edges counted): a path of 5 nodes rooted
+    # at one end has depth 4 and diameter 4; rooted in the middle, depth 2 and
+    # the same diameter 4; a star of 5 has depth 1 and diameter 2 (leaf-centre-
+    # leaf); a single node has 0 / 0; the "broom" 0-1-2 with 2 -> {3, 4} and
+    # 0 -> 5 has depth 3 (0-1-2-3) and diameter 4 (5-0-1-2-3).
+    assert (O.tree_depth(path_parent(5)), O.tree_diameter(path_parent(5))) == (4, 4)
+    mid = [1, 2, -1, 2, 3]  # 0-1-2-3-4 rooted at node 2
+    assert (O.tree_depth(mid), O.tree_diameter(mid)) == (2, 4)
+    star = [-1, 0, 0, 0, 0]
+    assert (O.tree_depth(star), O.tree_diameter(star)) == (1, 2)
+    assert (O.tree_depth([-1]), O.tree_diameter([-1])) == (0, 0)
+    broom = [-1, 0, 1, 2, 2, 0]
+    assert (O.tree_depth(broom), O.tree_diameter(broom)) == (3, 4)
+    # two deep branches under the root: depth 3, diameter 6 (leaf to leaf through the root)
+    two = [-1, 0, 1, 2, 0, 4, 5]
+    assert (O.tree_depth(two), O.tree_diameter(two)) == (3, 6)
+
+
+def test_detector_bounds_are_attained_on_paths():
+    # The S435 bounds are tight for a path rooted at one end: every node
+    # converged from sweep t0 -> the centralized root hears the far leaf after
+    # depth sweeps and STOP needs depth more to reach it (t0 + 2 depth); the
+    # decentralized saturation meets in the middle and floods back out.
+    for P in (2, 3, 5, 8):
+        parent = path_parent(P)
+        f = all_from(4 * P + 6, P, 1)
+        sc = O.detector_sim_centralized(parent, f)
+        assert max(sc) == 1 + 2 * O.tree_depth(parent)
+        assert sc == [1 + (P - 1) + d for d in range(P)]  # root at t0 + depth, then one hop per sweep
+        assert O.tree_depth(parent) == P - 1 and O.tree_diameter(parent) == P - 1

@@ -26,7 +26,11 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert {n for n, _, _ in R._ffi.SIGNATURES} == names
-    assert lib.ras_abi_version() == R._ffi.ABI_VERSION == 2
+    assert lib.ras_abi_version() == R._ffi.ABI_VERSION == 3
+    # provenance: the loaded library was built from exactly this tree
+    from paper_2003_05361_b200.build import source_hash
+
+    assert lib.ras_build_hash().decode() == source_hash()
 
 
 @pytest.mark.parametrize("dims,parts", [((10, 1, 1), (3, 1, 1)), ((64, 64, 1), (2, 2, 1)), ((17, 9, 1), (4, 3, 1)),
