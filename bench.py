@@ -7,10 +7,16 @@ GPU (4x4 tiles at N=1: 4096^2 = 16.8M unknowns), overlap 8, Jacobi-PCG m=20,
 synchronous RAS.  One "step" = one RAS sweep over the whole problem (restrict,
 residual, local solves, restricted prolongation, exchange, global check).
 
-value     = aggregate subdomain updates / s (= subdomains x sweeps / s, max over ranks)
+value     = RAS iterations/s = sync sweeps / s (max over ranks); the aggregate
+            subdomain updates/s (subdomains x sweeps/s) is the extra key `subdomain_updates_per_s`
 e2e       = the same through ras_solve() with pinned HOST x0 / x_out, copies inside
 roofline  = dominant kernel: algorithmic bytes / CUDA-event duration vs measured HBM copy peak
-cpu_baseline = the oracle on a bounded sample (rank 0, N=1)
+spmv_gbs  = the residual SpMV (k_residual, a1+a2): algorithmic bytes / event time
+tts       = time-to-solution to rel. residual 1e-8 (P474-480) on C1 and the 256^2 / 512^2
+            analogues of C2 (sync and async), with the oracle's full TTS beside it where it
+            finishes in seconds (C1, 256^2)
+cpu_baseline = the oracle (rank 0, N=1): K=3 full sync sweeps of this workload, plus the oracle
+            TTS above and an extrapolated C2 TTS (labelled)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode sync|async]
 """
@@ -53,6 +59,7 @@ def parse():
     ap.add_argument("--mode", default="sync", choices=["sync", "async"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tts", action="store_true", help="skip the small-config time-to-solution runs")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--tts", action="store_true", help="also run to rel. residual 1e-8 (long)")
     ap.add_argument("--scale", type=int, default=SUB, help="owned side per subdomain (debug)")
@@ -187,6 +194,58 @@ def build_rank_problem(N, rank, scale=SUB):
 # ----------------------------------------------------------------------------
 # reference arm and cpu baseline: the oracle, as it stands, on host cores
 # ----------------------------------------------------------------------------
+def oracle_setup(nx, ny, px, py, gamma, kind, m):
+    import oracle as O
+
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 0)
+    owner = O.partition_regular(nx, ny, 1, px, py, 1)
+    subs = O.setup(A, b, owner, gamma)
+    for s_ in subs:
+        O.make_local_solver(s_, kind, m)
+    return A, b, subs
+
+
+def oracle_sweeps(nx, ny, px, py, K=3):
+    """K full synchronous oracle sweeps of the workload (Alg. 1 loop: global check,
+    every subdomain's residual + Jacobi-PCG(m) + restricted prolongation), one BLAS
+    thread; setup untimed (P229-231).  Returns (sweeps/s, details)."""
+    from threadpoolctl import threadpool_limits
+
+    import oracle as O
+
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        A, b, subs = oracle_setup(nx, ny, px, py, GAMMA, "jacobi", M_INNER)
+        t1 = time.perf_counter()
+        O.ras_sync(A, b, subs, 1e-300, K)
+        t2 = time.perf_counter()
+    return K / (t2 - t1), {"sweeps": K, "solve_s": t2 - t1, "setup_s": t1 - t0}
+
+
+def oracle_tts(nx, ny, px, py, gamma, kind, m, tol=1e-8):
+    """Full oracle time-to-solution (sync, setup untimed), one BLAS thread."""
+    from threadpoolctl import threadpool_limits
+
+    import oracle as O
+
+    with threadpool_limits(1):
+        A, b, subs = oracle_setup(nx, ny, px, py, gamma, kind, m)
+        t0 = time.perf_counter()
+        r = O.ras_sync(A, b, subs, tol, 200000)
+        t1 = time.perf_counter()
+    return {"time_s": t1 - t0, "sweeps": r.sweeps, "cores": 1}
+
+
+# time-to-solution configurations (SURVEY §8d): C1 and analogues of C2 at smaller N
+TTS_CFGS = [
+    # name, N, tiles per side, overlap, local solver, m, oracle TTS in the default run
+    ("C1", 64, 2, 2, "exact", 0, True),
+    ("C2@256", 256, 4, 8, "jacobi", 20, True),
+    ("C2@512", 512, 4, 8, "jacobi", 20, False),  # oracle: 1914 sweeps, ~175 s on one core (DESIGN.md §6)
+]
+
+
 def oracle_sample(nx, ny, P, px, sample_subs, sweeps_per_sub, budget_s=25.0):
     """Time the oracle's per-subdomain work of a sync sweep (local residual +
     Jacobi-PCG(m) + restricted prolongation) on `sample_subs` subdomains of the
@@ -236,36 +295,44 @@ def run_reference(args):
     P = px * py
     steps = max(1, args.steps)
     warm = max(0, args.warmup)
-    # one reference "step" = one sampled subdomain update (+1/P of the global residual)
+    # one reference "step" = one sampled subdomain update (+1/P of the global residual);
+    # a full oracle sweep of C2 (16 updates + the global check) takes ~5 s on one core
     t0 = time.perf_counter()
-    val, det = oracle_sample(nx, ny, P, px, [5, 6], max(1, (steps + warm + 1) // 2), budget_s=120.0)
+    upd, det = oracle_sample(nx, ny, P, px, [5, 6], max(1, (steps + warm + 1) // 2), budget_s=120.0)
     wall = time.perf_counter() - t0
+    val = 1.0 / det["sweep_s"]  # sweeps/s
     line = {
-        "impl": "reference", "metric": "RAS iterations/s (aggregate subdomain updates/s)", "value": val,
-        "unit": "updates/s", "n_gpus": N, "steps": steps, "warmup": warm,
+        "impl": "reference", "metric": METRIC, "value": val,
+        "unit": "sweeps/s", "n_gpus": N, "steps": steps, "warmup": warm,
         "ms_per_step": det["sweep_s"] * 1000.0 / P, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(N, nx, ny, P, "sync"),
-        "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle",
+        "subdomain_updates_per_s": upd,
+        "cpu_baseline": {"value": val, "unit": "sweeps/s", "cores": 1, "kind": "oracle",
                          "sample": f"oracle (NumPy/SciPy, 1 thread) local residual + Jacobi-PCG(m={M_INNER}) + prolong "
-                                   f"on subdomains 5,6 of the workload, {det['samples']} updates, plus one global "
-                                   f"residual; sweep time = P*t_update + t_residual = {det['sweep_s']:.2f} s",
+                                   f"on subdomains 5,6 of the workload, {det['samples']} updates (one per step), plus one "
+                                   f"global residual; sweep time = P*t_update + t_residual = {det['sweep_s']:.2f} s",
                          "host_cores_available": os.cpu_count()},
-        "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": val, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_dict(N, nx, ny, P, mode, ws_bytes=None):
+METRIC = "RAS iterations/s (sync sweeps/s); time-to-solution to 1e-8 in `tts`; SpMV GB/s in `spmv_gbs`"
+
+
+def config_dict(N, nx, ny, P, mode):
+    # identical in both arms (the driver compares them); the working set of the
+    # sweep (r, p, d, b, x, matrix ~ 12 B/row) is >= 1.3 GB per GPU at C2 >> 126 MB L2
+    ws = 8.0 * nx * ny * 10
     return {"workload": (f"{'C2' if N == 1 else 'C3-weak'}: 2D 5-pt Laplacian {nx}x{ny} ({nx * ny / 1e6:.1f}M unknowns), "
                          f"{P} subdomains of {SUB}^2 ({P // N}/GPU), overlap {GAMMA}, Jacobi-PCG m={M_INNER}, {mode} RAS"),
             "grid": [nx, ny], "subdomains": P, "subdomains_per_gpu": P // N, "overlap": GAMMA,
             "inner_iters": M_INNER, "mode": mode, "precision": "fp64",
             "parallelism": f"domain decomposition, {P // N} subdomains per GPU x {N} GPU",
-            "l2": (f"working set {ws_bytes / 1e9:.2f} GB per GPU >> 126 MB L2, no flush needed"
-                   if ws_bytes else "working set >> 126 MB L2")}
+            "l2": f"inputs > L2: working set ~{ws / N / 1e9:.1f} GB per GPU >> 126 MB L2, no flush needed"}
 
 
 # ----------------------------------------------------------------------------
@@ -350,7 +417,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     sweeps = stats["sweeps"] if mode == "sync" else stats["updates_max"]
-    value = P * args.steps / (ms / 1e3)  # aggregate subdomain updates / s
+    value = args.steps / (ms / 1e3)  # RAS iterations (sync sweeps) / s, Q27
+    updates_per_s = P * value      # aggregate subdomain updates / s (all ranks)
 
     # roofline: dominant kernel by event time.  A whole-solve kernel (RESIDENT /
     # BLOCK path: every PCG iteration of every subdomain in one launch) is rated
@@ -402,39 +470,58 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
         d2h = n * 8  # x_out: the assembled global vector (NCCL allreduce on device, one D2H copy)
-        e2e = {"value": P * args.e2e_steps / el, "unit": "updates/s", "h2d_bytes_per_step": n * 8,
+        e2e = {"value": args.e2e_steps / el, "unit": "sweeps/s", "h2d_bytes_per_step": n * 8,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "note": "each step = ras_solve(x0=pinned host, max_iters=1, x_out=pinned host): H2D x0, one sweep + "
                        "final check, gather, D2H x"}
-    # optional time-to-solution
-    tts = None
+    # time-to-solution (P474-480): the bench workload itself only with --tts (C2 needs
+    # ~1e5 sweeps, ~7 min); C1 and the 256^2 / 512^2 analogues always at N=1
+    tts = {}
     if args.tts:
         barrier()
         t0 = time.perf_counter()
         st = solver.solve_device(1e-8, 200000, mode)
         barrier()
         s2 = solver.stats()
-        tts = {"time_s": time.perf_counter() - t0, "device_time_s": s2["time_to_solution_s"],
-               "sweeps": s2["sweeps"], "inner_iters_total": s2["inner_iters_total"],
-               "final_rel_residual": s2["final_rel_residual"], "converged": bool(s2["converged"])}
+        tts["bench_workload"] = {"time_s": time.perf_counter() - t0, "device_time_s": s2["time_to_solution_s"],
+                                 "sweeps": s2["sweeps"], "inner_iters_total": s2["inner_iters_total"],
+                                 "final_rel_residual": s2["final_rel_residual"], "converged": bool(s2["converged"])}
+    do_small = rank == 0 and N == 1 and not args.no_tts
+    if do_small:
+        tts.update(gpu_tts_small(R))
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        val, det = oracle_sample(nx, ny, P, prob["px"], [5, 6], 2)
-        cpu = {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle",
-               "sample": f"oracle (NumPy/SciPy, BLAS limited to 1 thread) local residual + Jacobi-PCG(m={M_INNER}) + "
-                         f"prolong on subdomains 5,6 of this workload ({det['samples']} updates, "
-                         f"{det['t_sub_update_s']:.2f} s each) + one global residual ({det['t_global_residual_s']:.2f} s); "
-                         f"sweep = {P}*t_update + t_residual = {det['sweep_s']:.1f} s",
-               "host_cores_available": os.cpu_count()}
+        val, det = oracle_sweeps(nx, ny, prob["px"], prob["py"], K=3)
+        o_tts = {}
+        if do_small:
+            for name, Nn, tiles, g, kind, m, run_oracle in TTS_CFGS:
+                if run_oracle:
+                    o_tts[name] = oracle_tts(Nn, Nn, tiles, tiles, g, kind, m)
+                    tts[name]["oracle"] = o_tts[name]
+                    tts[name]["speedup_vs_oracle"] = o_tts[name]["time_s"] / tts[name]["sync"]["time_s"]
+        c2_sweeps = committed_c2_sweeps()
+        cpu = {"value": val, "unit": "sweeps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{det['sweeps']} full synchronous oracle sweeps of this workload (NumPy/SciPy, BLAS limited "
+                         f"to 1 thread; {det['solve_s']:.1f} s, setup {det['setup_s']:.1f} s untimed); oracle full "
+                         f"time-to-solution on C1 and the 256^2 analogue in tts.*.oracle",
+               "host_cores_available": os.cpu_count(),
+               "oracle_tts": o_tts,
+               "c2_tts_extrapolated_s": (c2_sweeps / val) if c2_sweeps else None,
+               "c2_tts_extrapolation": (f"EXTRAPOLATED: {c2_sweeps} sweeps (GPU sync run to 1e-8, "
+                                        "profiles/bench_r01_tts_c2.json) / oracle sweeps per s" if c2_sweeps else None)}
     clocks = clk.summary()
     if rank == 0:
-        ws = 8.0 * info["rows_padded"] * 6 + 12.0 * (info["sell_residual"] + info["sell_local"])
+        res = kern.get("k_residual")
         line = {
-            "metric": "RAS iterations/s (aggregate subdomain updates/s)", "value": value, "unit": "updates/s",
+            "metric": METRIC, "value": value, "unit": "sweeps/s",
             "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(N, nx, ny, P, mode, ws),
-            "ras_iters_per_s": args.steps / (ms / 1e3),
+            "config": config_dict(N, nx, ny, P, mode),
+            "subdomain_updates_per_s": updates_per_s,
+            "spmv_gbs": res["gbs"] if res else None,
+            "spmv_frac": (res["gbs"] / peak) if res else None,
+            "spmv_note": "k_residual (a1+a2: restrict + [A_p | B_p] SpMV + Eq. 2 / owned norms), algorithmic bytes "
+                         "(DESIGN.md §5) / CUDA-event launch time",
             "sweeps_done": sweeps,
             "inner_iters_total": stats["inner_iters_total"],
             "pcg_path": ["auto", "tiled", "block", "resident"][stats["pcg_path"]],
@@ -448,7 +535,8 @@ def main():
             "clocks": clocks,
             "gpu_launches": stats["kernel_launches"],
             "setup_s": setup_s,
-            "tts": tts,
+            "tts": tts or None,
+            "phase_s": {k: stats[k] for k in ("t_residual", "t_local_solve", "t_prolong", "t_exchange", "t_convcheck")},
         }
         print(json.dumps(line), flush=True)
     solver.close()
@@ -456,6 +544,48 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def committed_c2_sweeps():
+    """GPU sweep count of the committed C2 sync run to 1e-8 (for the labelled extrapolation)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "bench_r01_tts_c2.json")) as f:
+            d = json.load(f)
+        t = d.get("tts") or {}
+        t = t.get("bench_workload", t)
+        return int(t["sweeps"]) if t.get("converged") else None
+    except (OSError, ValueError, KeyError, TypeError):
+        return None
+
+
+def gpu_tts_small(R):
+    """Time-to-solution to 1e-8 on C1 and the C2 analogues (sync and async), one GPU."""
+    import torch
+
+    out = {}
+    for name, Nn, tiles, g, kind, m, _ in TTS_CFGS:
+        A = ri.laplace_2d(Nn)
+        b = ri.rhs(Nn * Nn, 0)
+        owner = R.partition_regular(Nn, Nn, 1, tiles, tiles, 1)
+        s = R.Solver(A, b, owner, g, R.options(kind, max(m, 1)))
+        rec = {"config": f"{Nn}x{Nn} 2D Laplacian, {tiles}x{tiles} subdomains, overlap {g}, "
+                         f"{'exact (PCG to 1e-14)' if kind == 'exact' else f'Jacobi-PCG m={m}'}"}
+        for mode in ("sync", "async"):
+            s.solve(1e-8, 200000, mode, gather=False)  # warm-up (graphs, first-use buffers)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st, _ = s.solve(1e-8, 200000, mode, gather=False)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            t = s.stats()
+            rec[mode] = {"time_s": el, "device_tts_s": t["time_to_solution_s"], "sweeps": t["sweeps"],
+                         "updates_min": t["updates_min"], "updates_max": t["updates_max"],
+                         "inner_iters_total": t["inner_iters_total"], "final_rel_residual": t["final_rel_residual"],
+                         "converged": bool(t["converged"]), "verified": bool(t["verified"]),
+                         "pcg_path": ["auto", "tiled", "block", "resident"][t["pcg_path"]]}
+        s.close()
+        out[name] = rec
+    return out
 
 
 def _solve_host(solver, x0, xo, mode):

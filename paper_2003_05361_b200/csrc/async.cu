@@ -797,7 +797,7 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   const bool dl2 = c->small_nmax > kSmallSmemDRows;  // d in L2 (row space d_d) for the larger subdomains
   const size_t smem = (size_t)(dl2 ? 2 : 3) * c->small_nmax * sizeof(double);
   double* dglob = dl2 ? c->d_d : nullptr;
-  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TRY(allow_smem(c, fn));
   int per_sm = 0, sms = 0;
   RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_SMALL, smem));
   RAS_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));

@@ -172,6 +172,7 @@ ras_status cuda_err(ras_ctx* c, cudaError_t e, const char* what);
 void* dalloc(ras_ctx* c, size_t bytes);
 void* dalloc_raw(ras_ctx* c, size_t bytes);
 void dfree(ras_ctx* c, void* p);
+ras_status allow_smem(ras_ctx* c, const void* fn);  // dynamic smem cap = device maximum
 // collectives over the context's ranks (comm.cu): NCCL, or the loopback group
 ras_status loop_join(ras_ctx* c, const void* key128);
 void loop_leave(ras_ctx* c);

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -54,6 +55,19 @@ void* dalloc(ras_ctx* c, size_t bytes) {
 
 // Always cudaMalloc (a base allocation that can be exported as a CUDA IPC
 // window to the peer GPUs: x storage and the detector board).
+// Raise a kernel's dynamic shared-memory cap to everything the device allows.
+// The attribute is per function and process-wide: setting it to the launch's own
+// size would race between contexts (e.g. loopback ranks on host threads) that
+// launch the same kernel with different sizes; the device maximum never shrinks.
+ras_status allow_smem(ras_ctx* c, const void* fn) {
+  int optin = 0;
+  RAS_CUDA(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  cudaFuncAttributes fa{};
+  RAS_CUDA(c, cudaFuncGetAttributes(&fa, fn));
+  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+  return RAS_OK;
+}
+
 void dfree(ras_ctx* c, void* p) {
   for (size_t i = 0; i < c->bufs.size(); ++i)
     if (c->bufs[i].ptr == p) {
@@ -320,7 +334,7 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
   if (smem + 2048 > (size_t)smem_optin) return RAS_OK;  // ghost zones too wide: TILED
   const bool tol = c->opt.local_solver == RAS_LS_EXACT_PCG || c->opt.inner_tol > 0.0;
   const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol, pat);
-  RAS_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TRY(allow_smem(c, fn));
   int per_sm = 0;
   RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_RESID, smem));
   if (per_sm < 1) return RAS_OK;
@@ -468,8 +482,7 @@ static ras_status upload_band(ras_ctx* c) {
   int nmax = 0;
   for (const auto& S : pl->subs) nmax = std::max<int>(nmax, (int)S.nrows_pad);
   c->band_smem = (size_t)nmax * sizeof(double);
-  RAS_CUDA(c, cudaFuncSetAttribute((const void*)k_band_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)c->band_smem));
+  TRY(allow_smem(c, (const void*)k_band_chol));
   c->chol = true;
   c->mb.band = 16.0 * (double)H.off.back() + (double)pl->rows_local * 12.0 + (double)pl->n_own * 16.0;
   return RAS_OK;
@@ -899,12 +912,9 @@ static ras_status poll_inactive(ras_ctx* c, cudaStream_t s, const Range& R, bool
 
 // a3: local PCG solve (m iterations; exact mode polls every 16 iterations)
 template <int RPT, int W, bool Z>
-static void small_attr(size_t smem) {
-  static size_t set = 0;  // per instantiation: raise the dynamic shared-memory limit once
-  if (smem > set) {
-    cudaFuncSetAttribute((const void*)k_small_pcg<RPT, W, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = smem;
-  }
+static void small_attr(ras_ctx* c) {
+  static std::once_flag once;  // per instantiation; the cap (device maximum) is the same for every context
+  std::call_once(once, [c] { allow_smem(c, (const void*)k_small_pcg<RPT, W, Z>); });
 }
 
 // f2 regime: one CTA runs a subdomain's whole PCG + prolongation (k_small_pcg)
@@ -916,7 +926,7 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
   double* dglob = dl2 ? c->d_d : nullptr;
   const int rpt = (c->small_nmax + kNT_SMALL - 1) / kNT_SMALL;
 #define RAS_SMALL(RPT, W, Z)                                                                                     \
-  small_attr<RPT, W, Z>(smem);                                                                                   \
+  small_attr<RPT, W, Z>(c);                                                                                      \
   g_launch_smem = smem;                                                                                          \
   KL(s, K_SMALL, nsub, kNT_SMALL, (k_small_pcg<RPT, W, Z>), lp0, c->SS, c->L, c->D, (const double*)c->d_r,      \
      (const double*)c->d_p, (const int32_t*)c->d_own_slot, c->d_x, c->S, C, m, inner_tol, dglob)
