@@ -265,6 +265,16 @@ ras_status ras_nccl_unique_id(void* out128);
  * sweep k is flags[k * nlocal + i] (k >= nsweeps -> last row). */
 ras_status ras_set_scripted_flags(ras_ctx* ctx, const uint8_t* flags, int64_t nsweeps);
 
+/* Debug / stress test of the one-sided put path (reading R17: 8-byte single-copy
+ * atomicity of remote stores + release-published versions; P389-397).  COLLECTIVE
+ * over a world == 2 context: rank 0 writes `epochs` epochs of `words` epoch-tagged
+ * 8-byte words into rank 1's x window (the stores the async puts use), each
+ * followed by a system-scope fence + version increment; rank 1 polls the version
+ * (acquire) and checks the window after every observation.  out4 (rank 1):
+ * {torn words, stale words, version regressions, observations}; zeros on rank 0.
+ * words <= the reader's storage (owned + halo).  Destroys both ranks' iterate. */
+ras_status ras_debug_put_stress(ras_ctx* ctx, int64_t epochs, int64_t words, int64_t* out4);
+
 /* Per-subdomain stop sweep of the last scripted run (len local subdomains). */
 ras_status ras_detector_stops(const ras_ctx* ctx, int64_t* stop_out);
 

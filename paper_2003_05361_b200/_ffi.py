@@ -97,6 +97,7 @@ SIGNATURES = [
     ("ras_nccl_unique_id", I32, [C.c_void_p]),
     ("ras_set_scripted_flags", I32, [C.c_void_p, P(U8), I64]),
     ("ras_detector_stops", I32, [C.c_void_p, P(I64)]),
+    ("ras_debug_put_stress", I32, [C.c_void_p, I64, I64, P(I64)]),
     ("ras_kernel_timing", I32, [C.c_void_p, I32]),
     ("ras_kernel_times", I32, [C.c_void_p, P(RasKernelTime), I32, P(I32)]),
     # ras_plan.h

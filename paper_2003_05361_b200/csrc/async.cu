@@ -933,6 +933,87 @@ static ras_status run_scripted(ras_ctx* c, double tol, int64_t max_iters, int m,
   return RAS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Put / version stress test (reading R17, Q17; P389-397): the writer rank stores
+// epoch-tagged 8-byte words into the reader rank's x window with the same plain
+// stores the async puts use, then fences and bumps the reader's version counter
+// with a system-scope atomic (the put + flush analogue).  The reader polls the
+// counter with ld.acquire.sys and, after observing version v, reads the window:
+// a word whose two halves differ is TORN (8-byte stores not single-copy atomic
+// over the link), a word older than epoch v-1 is STALE (the release/acquire
+// publication failed).  Destroys the x storage of both ranks (debug only).
+// ---------------------------------------------------------------------------
+static __global__ void k_stress_write(unsigned long long* win, int64_t words, int64_t epochs, int32_t* ver) {
+  for (int64_t e = 0; e < epochs; ++e) {
+    const unsigned long long tag = ((unsigned long long)(e + 1) << 32) | (unsigned long long)(e + 1);
+    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) win[i] = tag;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      atomicAdd_system(ver, 1);
+    }
+    __syncthreads();
+  }
+}
+
+static __global__ void k_stress_read(const unsigned long long* win, int64_t words, int64_t epochs, const int32_t* ver,
+                                     unsigned long long* out /* torn, stale, regress, observations */) {
+  __shared__ int s_v;
+  __shared__ unsigned long long s_cnt[3];
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  int last = 0;
+  unsigned long long obs = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_v = ld_acquire_sys(ver);
+    __syncthreads();
+    const int v = s_v;
+    if (v < last && threadIdx.x == 0) atomicAdd(&s_cnt[2], 1ull);
+    last = v;
+    unsigned long long torn = 0, stale = 0;
+    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) {
+      const unsigned long long w = __ldcv(win + i);
+      const unsigned hi = (unsigned)(w >> 32), lo = (unsigned)w;
+      torn += hi != lo;
+      stale += (int64_t)lo < (int64_t)v;  // tag of epoch e is e + 1: version v => every tag >= v
+    }
+    if (torn) atomicAdd(&s_cnt[0], torn);
+    if (stale) atomicAdd(&s_cnt[1], stale);
+    ++obs;
+    if (v >= epochs) break;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) out[threadIdx.x] = s_cnt[threadIdx.x];
+  if (threadIdx.x == 0) out[3] = obs;
+}
+
+ras_status put_stress(ras_ctx* c, int64_t epochs, int64_t words, int64_t* out4) {
+  AsyncRt* A = c->async;
+  if (c->world != 2) return set_err(c, RAS_EINVAL, "put stress test needs world == 2");
+  if (words < 1 || words > c->n_own + c->n_halo || epochs < 1 || epochs > (1 << 30))
+    return set_err(c, RAS_EINVAL, "put stress test: words must be in [1, storage of the reader], epochs >= 1");
+  int32_t* ver = A->board + 3 * c->plan->P;  // VER section of this rank's board, word 0
+  RAS_CUDA(c, cudaMemsetAsync(ver, 0, 4, c->stream));
+  RAS_CUDA(c, cudaMemsetAsync(c->d_x, 0, (size_t)words * 8, c->stream));
+  TRY(coll_barrier(c));  // the reader's window and counter are clear before the writer starts
+  unsigned long long* d_out = nullptr;
+  TRY(zalloc(c, &d_out, 4));
+  if (c->rank == 0) {
+    k_stress_write<<<1, 1024, 0, c->stream>>>((unsigned long long*)A->peer_x[1], words, epochs,
+                                              A->peer_board[1] + 3 * c->plan->P);
+  } else {
+    k_stress_read<<<1, 1024, 0, c->stream>>>((const unsigned long long*)c->d_x, words, epochs, ver, d_out);
+  }
+  RAS_CUDA(c, cudaGetLastError());
+  std::vector<unsigned long long> h(4, 0);
+  RAS_CUDA(c, cudaMemcpyAsync(h.data(), d_out, 32, cudaMemcpyDeviceToHost, c->stream));
+  RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  dfree(c, d_out);
+  TRY(coll_barrier(c));
+  for (int i = 0; i < 4; ++i) out4[i] = (int64_t)h[i];
+  return RAS_OK;
+}
+
 ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
   AsyncRt* A = c->async;
   const int nl = c->nl;

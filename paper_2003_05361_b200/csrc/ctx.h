@@ -161,6 +161,11 @@ struct ras_ctx {
   int32_t* d_own_gid = nullptr;
   int32_t* d_halo_gid = nullptr;
   double* d_xglob = nullptr;  // len n, allocated on first host-buffer solve
+  // N-GPU gather: owned values allgathered in padded segments of gmax (ensure_xglob)
+  int64_t gmax = 0;
+  int32_t* d_gid_all = nullptr;  // [world * gmax] global id of every gathered slot (-1 = padding)
+  double* d_gsend = nullptr;     // [gmax]
+  double* d_grecv = nullptr;     // [world * gmax]
 
   std::vector<uint8_t> scripted;
   int64_t scripted_sweeps = 0;
@@ -194,6 +199,7 @@ ras_status enq_prolong(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C);
 ras_status async_setup(ras_ctx* c);
 ras_status async_set_b2(ras_ctx* c);  // re-upload the Eq. 2 ||b~_p||^2 after ras_set_rhs
 void async_free(ras_ctx* c);
+ras_status put_stress(ras_ctx* c, int64_t epochs, int64_t words, int64_t* out4);  // R17 stress test
 }  // namespace ras
 
 #define TRY(x)                   \

@@ -1760,6 +1760,16 @@ static __global__ void k_scatter_x0(int64_t n_own, int64_t n_halo, const int32_t
     x[i] = i < n_own ? xg[own_gid[i]] : xg[halo_gid[i - n_own]];
 }
 
+// every rank's owned values, allgathered in padded per-rank segments -> global
+// order (x_out gather on N GPUs, P242); padding slots carry gid -1
+static __global__ void k_gather_all(int64_t count, const int32_t* __restrict__ gid_all, const double* __restrict__ v,
+                                    double* __restrict__ xg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = gid_all[i];
+    if (g >= 0) xg[g] = v[i];
+  }
+}
+
 // owned storage -> global order (x_out gather, P242)
 static __global__ void k_gather_x(int64_t n_own, const int32_t* __restrict__ own_gid, const double* __restrict__ x,
                                   double* __restrict__ xg) {

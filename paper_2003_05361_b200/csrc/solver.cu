@@ -1215,6 +1215,20 @@ static ras_status ensure_xglob(ras_ctx* c) {
   TRY(upload(c, &c->d_halo_gid, hg, 1));
   c->d_xglob = (double*)dalloc(c, (size_t)pl->n * 8);
   if (!c->d_xglob) return set_err(c, RAS_ENOMEM, "device allocation failed (global x buffer)");
+  if (c->world > 1) {
+    // padded segment size and every rank's owned global ids, exchanged once
+    double g = (double)c->n_own;
+    TRY(coll_allreduce_f64(c, &g, 1, true));
+    c->gmax = std::max<int64_t>((int64_t)g, 1);
+    std::vector<int32_t> mine((size_t)c->gmax, -1);
+    std::copy(og.begin(), og.end(), mine.begin());
+    int32_t* d_mine;
+    TRY(upload(c, &d_mine, mine));
+    TRY(zalloc(c, &c->d_gid_all, (size_t)c->world * c->gmax));
+    TRY(coll_allgather(c, d_mine, c->d_gid_all, (size_t)c->gmax, ncclInt32, c->stream));
+    TRY(zalloc(c, &c->d_gsend, (size_t)c->gmax));
+    TRY(zalloc(c, &c->d_grecv, (size_t)c->world * c->gmax));
+  }
   return RAS_OK;
 }
 
@@ -1234,18 +1248,24 @@ static ras_status load_x0(ras_ctx* c, const double* x0) {
   return RAS_OK;
 }
 
-// Gather owner values to x_out (len n) on every rank (P242): every rank
-// scatters its owned values into a zeroed global-order vector on the device and
-// one NCCL sum-allreduce over NVLink assembles it (the owned sets partition the
-// index space, so each entry is one rank's value plus zeros: exact).
+// Gather owner values to x_out (len n) on every rank (P242).  One rank: owned
+// storage -> global order on the device.  N ranks: one NCCL allgather of the
+// owned values in padded per-rank segments (each rank receives only the other
+// ranks' owned values, ~n words over NVLink), then one scatter into global order
+// through the allgathered global ids (exchanged once); one D2H copy.
 static ras_status gather(ras_ctx* c, double* x_out) {
   const ras_plan* pl = c->plan;
   TRY(ensure_xglob(c));
-  if (c->world > 1) RAS_CUDA(c, cudaMemsetAsync(c->d_xglob, 0, (size_t)pl->n * 8, c->stream));
-  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n_own + 255) / 256, 148 * 16));
-  LAUNCH(K_CTRL, k_gather_x<<<g, 256, 0, c->stream>>>(c->n_own, c->d_own_gid, c->d_x, c->d_xglob));
-  if (c->world > 1)
-    TRY(coll_allreduce(c, c->d_xglob, c->d_xglob, (size_t)pl->n, ncclDouble, ncclSum, c->stream));
+  if (c->world == 1) {
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n_own + 255) / 256, 148 * 16));
+    LAUNCH(K_CTRL, k_gather_x<<<g, 256, 0, c->stream>>>(c->n_own, c->d_own_gid, c->d_x, c->d_xglob));
+  } else {
+    RAS_CUDA(c, cudaMemcpyAsync(c->d_gsend, c->d_x, (size_t)c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(coll_allgather(c, c->d_gsend, c->d_grecv, (size_t)c->gmax, ncclFloat64, c->stream));
+    const int64_t tot = (int64_t)c->world * c->gmax;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 16));
+    LAUNCH(K_CTRL, k_gather_all<<<g, 256, 0, c->stream>>>(tot, c->d_gid_all, c->d_grecv, c->d_xglob));
+  }
   RAS_CUDA(c, cudaMemcpyAsync(x_out, c->d_xglob, (size_t)pl->n * 8, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   return RAS_OK;
@@ -1581,6 +1601,12 @@ ras_status ras_set_scripted_flags(ras_ctx* c, const uint8_t* flags, int64_t nswe
   c->scripted.assign(flags, flags + nsweeps * c->nl);
   c->scripted_sweeps = nsweeps;
   return RAS_OK;
+}
+
+ras_status ras_debug_put_stress(ras_ctx* c, int64_t epochs, int64_t words, int64_t* out4) {
+  if (!c || !out4) return RAS_EINVAL;
+  RAS_CUDA(c, cudaSetDevice(c->device));
+  return put_stress(c, epochs, words, out4);
 }
 
 ras_status ras_detector_stops(const ras_ctx* c, int64_t* out) {

@@ -290,6 +290,12 @@ class Solver:
         f = np.ascontiguousarray(flags, dtype=np.uint8)
         _check(F.lib().ras_set_scripted_flags(self._h, F.ptr(f, F.U8), f.shape[0]), self._h)
 
+    def put_stress(self, epochs, words) -> dict:
+        """ras_debug_put_stress (collective, world == 2): torn / stale words seen by rank 1."""
+        out = np.zeros(4, np.int64)
+        _check(F.lib().ras_debug_put_stress(self._h, int(epochs), int(words), F.ptr(out, F.I64)), self._h)
+        return dict(zip(("torn", "stale", "regress", "observations"), out.tolist()))
+
     def detector_stops(self) -> np.ndarray:
         nl = self.plan().info()["local_subdomains"]
         out = np.empty(nl, np.int64)

@@ -175,3 +175,33 @@ def test_loopback_async_forced_stop_resumes():
         assert st == 0, stats
         assert stats["resumes"] == 1 and stats["verified"] == 1
         assert O.verify_global(A, x, b, 1e-8)[0]
+
+
+def test_loopback_put_stress_versions_and_words():
+    # R17 machinery on one device: epoch-tagged words + release-published versions
+    # (the NVLink variant of the same test runs in test_gpu_multi.py)
+    nx = ny = 128
+    owner = O.partition_regular(nx, ny, 1, 1, 2, 1)
+    key = os.urandom(128)
+    out, errs = {}, {}
+
+    def worker(rank):
+        try:
+            s = R.Solver(ri.laplace_2d(nx, ny), ri.rhs(nx * ny, 0), owner, 2, R.options("jacobi", 4),
+                         comm={"rank": rank, "world": 2, "device": 0, "nccl_id": key, "transport": "loopback"})
+            out[rank] = s.put_stress(2000, 4096)
+            s.close()
+        except Exception:
+            import traceback
+
+            errs[rank] = traceback.format_exc()
+
+    ts = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(300)
+    assert not errs, errs
+    r1 = out[1]
+    assert r1["torn"] == 0 and r1["stale"] == 0 and r1["regress"] == 0, r1
+    assert r1["observations"] >= 1

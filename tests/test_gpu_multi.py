@@ -155,3 +155,47 @@ def test_multi_gpu_async_resident_sequential():
         assert st == 0, stats
         assert O.verify_global(A, x, b, 1e-8)[0]
         assert stats["pcg_path"] == 3  # RESIDENT: the sequential on-chip schedule ran (R34)
+
+
+def _stress_worker(rank, world, nccl_id, q):
+    try:
+        import paper_2003_05361_b200 as R
+
+        nx = ny = 256
+        owner = O.partition_regular(nx, ny, 1, 1, 2, 1)
+        s = R.Solver(ri.laplace_2d(nx, ny), ri.rhs(nx * ny, 0), owner, 2, R.options("jacobi", 4),
+                     comm={"rank": rank, "world": world, "device": rank, "nccl_id": nccl_id})
+        res = s.put_stress(20000, 30000)
+        s.close()
+        q.put((rank, "ok", res))
+    except Exception:
+        import traceback
+
+        q.put((rank, "err", traceback.format_exc()))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
+def test_multi_gpu_nvlink_put_stress():
+    # Q17 / R17 over NVLink: 20000 epochs of 30000 epoch-tagged 8-byte words stored
+    # into the peer GPU's window, each published by fence + system-scope version
+    # increment; the reader must never see a torn word, a stale word after an
+    # acquired version, or a version going backwards
+    import paper_2003_05361_b200 as R
+
+    nid = R.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_stress_worker, args=(r, 2, nid, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, st, out = q.get(timeout=600)
+        assert st == "ok", out
+        res[r] = out
+    for p in ps:
+        p.join(60)
+    r1 = res[1]
+    print("nvlink put stress:", r1)
+    assert r1["torn"] == 0 and r1["stale"] == 0 and r1["regress"] == 0, r1
+    assert r1["observations"] >= 100
