@@ -139,7 +139,10 @@ typedef struct {
   int32_t force_first_stop;      /* test hook (async): in the first detection round every Eq. 2 flag reads
                                     as set, so detection terminates after a few updates and the
                                     post-termination verification fails -> the R20 resume path runs */
-  int32_t reserved_i[1];
+  int32_t persistent_grid;       /* persistent async kernel: at most this many CTAs (0 = one per subdomain up to
+                                    the co-resident limit).  1 = ONE CTA updating every subdomain in turn, each
+                                    update reading the latest x: the sequential schedule the oracle's
+                                    ras_schedule reproduces (parity hook for the persistent kernel) */
   /* Optimized RAS (NEXT f3, PAPER P760-763, R30): Robin-type transmission condition in algebraic
    * form -- the local solve uses A~_p = A_p - robin * diag(sum_{j not in Omega_p} |a_ij|) (rows
    * coupled outside Omega_p); the residual keeps A.  0 = RAS (Dirichlet truncation, default);

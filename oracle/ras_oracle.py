@@ -54,6 +54,7 @@ __all__ = [
     "RasResult",
     "ras_sync",
     "verify_global",
+    "ras_schedule",
     "bfs_tree",
     "tree_depth",
     "tree_diameter",
@@ -524,6 +525,34 @@ def ras_sync(A, b, subs, tol, max_iters, x0=None, record_iterates=False):
     res = RasResult(x, k, True, hist, sum(s.extra.get("inner", 0) for s in subs))
     res.iterates = iterates
     return res
+
+
+def ras_schedule(A, b, subs, schedule, x0=None):
+    """One admissible ASYNCHRONOUS schedule of RAS updates (P163-176: every
+    process updates with the data available to it, no waiting), written out as a
+    sequence: `schedule` is a list of steps, each a list of subdomain indices that
+    read the same current x and then all write their owned rows:
+
+        for step in schedule:
+            x_read = x                           (the data available at the step)
+            for p in step: d_p = LocalSolve_p(r~_p(x_read))
+            for p in step: x[S_p] = x_read[S_p] + d_p[S_p]
+
+    [[0..P-1]] * K is K synchronous sweeps (ras_sync without the stopping test);
+    [[0], [1], ..., [P-1]] * K is the sequential (multiplicative-Schwarz ordered)
+    schedule that one processor updating its subdomains one after another in
+    subdomain order produces (R34).  Returns x after the schedule."""
+    A = as_scipy(A)
+    n = A.shape[0]
+    x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
+    for step in schedule:
+        x_read = x.copy()
+        for p in step:
+            s = subs[p]
+            d = s.solver(local_residual(s, x_read))
+            og = s.owned_global
+            x[og] = x_read[og] + d[s.owned]
+    return x
 
 
 def verify_global(A, x, b, tol):

@@ -38,7 +38,7 @@ class RasOptions(C.Structure):
     _fields_ = [("local_solver", I32), ("inner_iters", I32), ("inner_tol", F64), ("detector", I32),
                 ("local_crit_owned_only", I32), ("max_resumes", I32), ("use_graphs", I32), ("poll_interval", I32),
                 ("async_timeout_s", F64), ("scripted_flags", I32), ("fuse_p", I32), ("matrix_format", I32), ("stage_p", I32),
-                ("pcg_path", I32), ("async_persistent", I32), ("force_first_stop", I32), ("reserved_i", I32 * 1), ("robin", F64), ("reserved_d", F64 * 3)]
+                ("pcg_path", I32), ("async_persistent", I32), ("force_first_stop", I32), ("persistent_grid", I32), ("robin", F64), ("reserved_d", F64 * 3)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)

@@ -805,6 +805,7 @@ static ras_status run_async_persistent(ras_ctx* c, double tol, int64_t max_iters
   // loopback virtual ranks share one device: each persistent grid gets 1/world of
   // it so that every rank's CTAs are resident at once (they wait on each other's flags)
   int G = std::min(nl, std::max(1, per_sm * sms / (c->loopback ? c->world : 1)));
+  if (c->opt.persistent_grid > 0) G = std::min(G, c->opt.persistent_grid);
   *A->h_kill = 0;
   int nl_ = nl;
   Sell Rm = c->R, L = c->L;
