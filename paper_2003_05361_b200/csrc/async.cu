@@ -146,6 +146,19 @@ __device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
   asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Iterate values shared between concurrently running CTAs / GPUs inside ONE
+// launch (persistent kernel): morally strong (relaxed, system scope) accesses.
+// Weak loads (ld.global.cg) of data another SM keeps rewriting are a data race
+// in the PTX memory model -- they may be served from a stale copy for an
+// unbounded time, i.e. an asynchronous iteration with UNBOUNDED delays (R33).
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 
 // One detection step of local subdomain lp (P331-357).  `in` is the board the
 // reports / stop words are read from, `out` the boards they are written to
@@ -309,7 +322,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       double v[3] = {0.0, 0.0, 0.0};
       for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
         const int64_t row = (int64_t)r0 + i;
-        const double ax = resident_row<WR, Z>(Rm, row, tabR, [&](int32_t c) { return __ldcg(&x[c]); });
+        const double ax = resident_row<WR, Z>(Rm, row, tabR, [&](int32_t c) { return ld_relaxed_f64(&x[c]); });
         const double ri = __ldg(&b[row]) - ax;
         const double zi = __drcp_rn(diag_at<Z>(D, row)) * ri;
         sr[i] = ri;
@@ -351,7 +364,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       if (its > 0)
         for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
           const int32_t sl = __ldg(&own_slot[r0 + i]);
-          if (sl >= 0) __stcg(&x[sl], __ldcg(&x[sl]) + sd[i]);
+          if (sl >= 0) st_relaxed_f64(&x[sl], ld_relaxed_f64(&x[sl]) + sd[i]);
         }
       if (threadIdx.x == 0) phase_mark(det, lp, PH_PROL);
       // a5 (multi-GPU): owner values other GPUs need, stored straight into their
@@ -361,7 +374,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       if (its > 0 && e1 > e0) {
         __syncthreads();  // this CTA's x[S_p] stores before the reads below
         for (int64_t e = e0 + threadIdx.x; e < e1; e += kNT_SMALL)
-          PD.peer_x[PD.rank[e]][PD.ridx[e]] = __ldcg(&x[PD.slot[e]]);
+          st_relaxed_f64(&PD.peer_x[PD.rank[e]][PD.ridx[e]], ld_relaxed_f64(&x[PD.slot[e]]));
         __syncthreads();
         if (threadIdx.x == 0) {
           __threadfence_system();
