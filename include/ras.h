@@ -205,7 +205,8 @@ typedef struct {
   int64_t kernel_launches;     /* kernels launched by the last ras_solve on this rank */
   int64_t fresh_halo_reads;    /* async: halo version changes observed */
   int32_t resident_pattern;    /* RESIDENT path: 1 = row-pattern dictionary SpMV, 0 = SELL-Z / SELL stream */
-  int32_t reserved_s;
+  int32_t resident_lanes;      /* RESIDENT path: 0 = k_resident_pcg (r, d in shared memory); 1 / 2 =
+                                  k_resident2 (r, d in tensor memory) with that many subdomains per CTA */
 } ras_stats_t;
 
 /* Fill *opt with defaults. */

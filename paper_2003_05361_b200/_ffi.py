@@ -60,7 +60,7 @@ class RasStats(C.Structure):
                 ("t_convcheck", F64), ("model_bytes", F64), ("num_subdomains", I32), ("world", I32),
                 ("local_subdomains", I32), ("pcg_path", I32), ("rows_local", I64), ("halo_values", I64),
                 ("kernel_launches", I64), ("fresh_halo_reads", I64), ("resident_pattern", I32),
-                ("reserved_s", I32)]
+                ("resident_lanes", I32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

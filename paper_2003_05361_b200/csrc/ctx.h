@@ -117,6 +117,7 @@ struct ras_ctx {
   int resid_chunk = 0;      // rows per CTA of the largest subdomain
   int resid_glo = 0, resid_ghi = 0;  // widest ghost zones below / above a chunk (rows)
   bool resid_pat = false;   // row-pattern dictionary SpMV (no matrix stream)
+  int resid_lanes = 0;      // 0: k_resident_pcg (v1); 1 / 2: k_resident2 with NL lanes (TMEM)
   bool resid_seq = false;   // async sequential schedule: per-subdomain calls use k_resident_pcg
   unsigned long long* d_resid_slots = nullptr;
   double* d_q = nullptr;

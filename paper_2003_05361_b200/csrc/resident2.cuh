@@ -1,0 +1,429 @@
+// RESIDENT path, version 2 (k_resident2): the on-chip fixed-m Jacobi-PCG of
+// k_resident_pcg (same recurrences R28 / R29, same row-pattern dictionary SpMV,
+// bitwise the same iterates) with the per-thread vectors r and d moved from
+// shared memory into TENSOR MEMORY (TMEM, 256 KB per SM, used here as a private
+// register-file extension: tcgen05.st / tcgen05.ld of 32-bit columns of the
+// thread's own TMEM lane) and NL subdomains interleaved per CTA.
+//
+// Why (profiles/r01_resident_ncu_summary.md): k_resident_pcg runs
+// one group-wide reduction per PCG iteration whose latency (~3.9 us at 148 CTAs)
+// is about a third of the iteration, and its shared memory (p, r, d: 24 B/row +
+// ghosts) caps a CTA's chunk at ~7.7 K rows.  With r and d in TMEM a chunk row
+// costs 9 B of shared memory (p + pattern id), so
+//   NL = 2: two subdomains live on chip at once and the reduction of one is in
+//           flight while the CTA runs the other's passes (software pipelining
+//           across independent local problems -- the subdomains of a sweep);
+//   NL = 1: chunks up to 768 x 16 rows (C5's 1.56 M-row Voronoi cells on 148 SMs).
+//
+// Per lane (subdomain) L and iteration it, exactly as k_resident_pcg:
+//   pass A   q = A_p p_it (pattern SpMV from shared memory), partials
+//            (p, q), (z, q), (q, D^-1 q); publish them (slot ring, no wait)
+//   wait     the lane's group-wide sum -> alpha, rho' (R28), beta
+//   pass B   d += alpha p, r -= alpha q, p_{it+1} = D^-1 r + beta p; export band
+//            published; ghost zones recomputed (R29)
+// Schedule with NL = 2: A(0) pub(0) A(1) pub(1) | wait(0) B(0) A(0) pub(0) wait(1) B(1) A(1) pub(1) | ...
+//
+// TMEM layout: warp w addresses the 32 lanes of quadrant w % 4 (its lane = its
+// thread's lane), columns [kR2ColBlk * (w / 4), +kR2ColBlk); thread column
+// ((L * 2 + V) * RPT + j) * 2 holds vector V (0 = r, 1 = d) of chunk row
+// j * NT + tid of lane L as two 32-bit halves.  tcgen05.ld/st are warp-wide
+// (.sync.aligned): they are executed unconditionally, also for rows past the
+// chunk end (private slots, harmless).
+#pragma once
+
+namespace ras {
+
+constexpr int kNT_R2 = 512;     // threads per CTA: 16 warps, 4 per TMEM lane quadrant, 128 registers per thread
+constexpr int kR2ColBlk = 128;  // TMEM columns per warp (4 warps per quadrant: 512 columns)
+constexpr int kR2MaxRPT = 24;   // rows per thread of one lane (q in registers)
+
+__device__ __forceinline__ void tm_st(uint32_t taddr, double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"((uint32_t)u),
+               "r"((uint32_t)(u >> 32))
+               : "memory");
+}
+__device__ __forceinline__ double tm_ld(uint32_t taddr) {
+  uint32_t lo, hi;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(taddr) : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+__device__ __forceinline__ void tm_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// First half of group_allsum: CTA partials -> this CTA's slot of reduction `seq`
+// (the next ring sector reset first, one release fence, relaxed stores).
+template <int NV, int NT>
+__device__ __forceinline__ void group_publish(const double (&v)[NV], double (*red)[NT / 32],
+                                              unsigned long long* slots, int gs, int c, unsigned seq) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double s = warp_sum(v[j]);
+    if (lane == 0) red[j][w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long* const ring = slots + (size_t)(seq % 3) * gs * 4;
+    unsigned long long* const nxt = slots + (size_t)((seq + 1) % 3) * gs * 4;
+    double s[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) s[j] = warp_sum(lane < NW ? red[j][lane] : 0.0);
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) st_relaxed_gpu_u64(&nxt[c * 4 + j], kSlotEmpty);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release: export-band stores before the values
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        unsigned long long u = (unsigned long long)__double_as_longlong(s[j]);
+        if (u == kSlotEmpty) u = 0x7ff8000000000000ull;
+        st_relaxed_gpu_u64(&ring[c * 4 + j], u);
+      }
+    }
+  }
+  // red[] is reused by the next publish only after a later CTA barrier
+}
+
+// Second half: poll every CTA's slot of reduction `seq`, fixed-order sum; every
+// thread returns the identical values.
+template <int NV>
+__device__ __forceinline__ void group_wait(double (&v)[NV], double* bc, const unsigned long long* slots, int gs,
+                                           unsigned seq) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w == 0) {
+    const unsigned long long* const ring = slots + (size_t)(seq % 3) * gs * 4;
+    constexpr int KS = (kMaxGroupCTAs + 31) / 32;
+    unsigned long long u[KS][NV];
+#pragma unroll
+    for (int t = 0; t < KS; ++t)
+#pragma unroll
+      for (int j = 0; j < NV; ++j) u[t][j] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
+    for (;;) {
+      bool done = true;
+#pragma unroll
+      for (int t = 0; t < KS; ++t)
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (u[t][j] == kSlotEmpty) u[t][j] = ld_relaxed_gpu_u64(&ring[(lane + 32 * t) * 4 + j]);
+#pragma unroll
+      for (int t = 0; t < KS; ++t)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) done = done && u[t][j] != kSlotEmpty;
+      if (__all_sync(0xffffffffu, done)) break;
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the peers' export-band stores
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < KS; ++t) acc += __longlong_as_double((long long)u[t][j]);
+      acc = warp_allsum(acc);
+      if (lane == 0) bc[j] = acc;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = bc[j];
+}
+
+// Shared-memory words (doubles) of one lane: p with ghost zones, pattern ids,
+// pattern table (values [kMaxPat][W], diagonal, its reciprocal, int32 deltas [kMaxPat][W]).
+__host__ __device__ constexpr int r2_lane_words(int glo, int chunk, int ghi, int W) {
+  return (glo + chunk + ghi) + ((chunk + 7) & ~7) / 8 + kMaxPat * (W + 2) + (kMaxPat * W + 1) / 2;
+}
+
+// Per-lane state kept in shared memory (registers are for the rows' q).
+struct R2Lane {
+  int lp, rb, nr, live;  // subdomain, chunk's first row-space row, chunk rows, still iterating
+  int4 band;             // {lo_end, hi_begin, glo, ghi}
+  double rho, alpha, beta;
+  int its;
+  unsigned seq;
+};
+
+template <int RPT, int W, int NL>
+static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int nsub, SmallSubs SS, ResidentCtl RC,
+                                                                   Diag D, const int32_t* __restrict__ own_slot,
+                                                                   double* __restrict__ x, Scal S, Ctl C, int32_t m,
+                                                                   int32_t chunk_max, int32_t glo_max, int32_t ghi_max,
+                                                                   int32_t ntable) {
+  constexpr int NT = kNT_R2;
+  static_assert(2 * 2 * NL * RPT <= kR2ColBlk, "r, d of NL lanes x RPT rows must fit the warp's TMEM columns");
+  extern __shared__ double smem[];
+  __shared__ double red[kResidNV][NT / 32];
+  __shared__ double bc[kResidNV];
+  __shared__ double sinv[256];  // __drcp_rn of every dictionary value (ghost rows' D^-1)
+  __shared__ R2Lane st[NL];
+  __shared__ uint32_t s_tbase;
+  // per-lane shared memory: p (+ ghost zones) | pattern ids | pattern table
+  const int pstride = glo_max + chunk_max + ghi_max;
+  const int idbytes = (chunk_max + 7) & ~7;
+  const int lane_words = r2_lane_words(glo_max, chunk_max, ghi_max, W);
+  auto lane_sp = [&](int L) { return smem + (size_t)L * lane_words + glo_max; };
+  auto lane_id = [&](int L) { return reinterpret_cast<uint8_t*>(smem + (size_t)L * lane_words + pstride); };
+  auto lane_pv = [&](int L) { return smem + (size_t)L * lane_words + pstride + idbytes / 8; };  // [kMaxPat][W]
+  auto lane_pdg = [&](int L) { return lane_pv(L) + kMaxPat * W; };
+  auto lane_pdi = [&](int L) { return lane_pdg(L) + kMaxPat; };
+  auto lane_pdl = [&](int L) { return reinterpret_cast<int32_t*>(lane_pdi(L) + kMaxPat); };  // [kMaxPat][W]
+
+  const int w = threadIdx.x >> 5;
+  // ---- TMEM: 512 columns for this CTA (one CTA per SM) ----
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < ntable; i += NT) sinv[i] = __drcp_rn(__ldg(&D.table[i]));
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmy = s_tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(kR2ColBlk * (w >> 2));
+  auto tcol = [&](int L, int V, int j) { return tmy + (uint32_t)(((L * 2 + V) * RPT + j) * 2); };
+
+  const int gs = RC.gs;
+  const int g = blockIdx.x / gs, c = blockIdx.x - g * gs;
+  double q[NL][RPT];
+
+  // published arrays re-based to a chunk (select, not index)
+#define R2_PUB(arr, par, rb) (((par) ? RC.arr[1] : RC.arr[0]) + (rb))
+
+  for (int pair = g; pair * NL < nsub; pair += RC.ngroups) {
+    // ---- lane set-up: load p_1, r_0, pattern ids and the chunk's pattern table ----
+#pragma unroll
+    for (int L = 0; L < NL; ++L) {
+      const int lp = lp_base + pair * NL + L;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const bool valid = pair * NL + L < nsub;
+        st[L].lp = lp;
+        st[L].live = valid && !stopped(C, lp) && S.active[lp];
+        st[L].its = 0;
+        st[L].seq = 0;
+        st[L].alpha = st[L].beta = 0.0;
+        if (st[L].live) {
+          const int r0 = SS.row_off[lp], n = SS.nrows[lp];
+          const int chunk = ((n / 32 + gs - 1) / gs) * 32;
+          const int a = min(n, c * chunk);
+          st[L].rb = r0 + a;
+          st[L].nr = min(n, a + chunk) - a;
+          st[L].band = RC.band[lp * gs + c];
+          st[L].rho = S.rho[lp];
+        }
+      }
+      __syncthreads();
+      if (!st[L].live) continue;
+      const int rb = st[L].rb, nr = st[L].nr;
+      const int4 band = st[L].band;
+      double* sp = lane_sp(L);
+      uint8_t* sdc = lane_id(L);
+      const int ng = band.z + band.w;
+      for (int t = threadIdx.x; t < ng; t += NT) {
+        const int li = t < band.z ? t - band.z : nr + (t - band.z);
+        sp[li] = __ldcg(&R2_PUB(pub_p, 1, rb)[li]);  // p_1 of the ghost rows
+      }
+      for (int i = threadIdx.x; i < nr; i += NT) {
+        sp[i] = __ldcg(&R2_PUB(pub_p, 1, rb)[i]);  // p_1 = z_0
+        sdc[i] = __ldg(&RC.pid[rb + i]);
+      }
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int i = j * NT + threadIdx.x;
+        tm_st(tcol(L, 0, j), i < nr ? __ldcg(&R2_PUB(pub_r, 0, rb)[i]) : 0.0);  // r_0
+      }
+      const int p0 = RC.pat_off[lp * gs + c], np = RC.pat_cnt[lp * gs + c];
+      double* spv = lane_pv(L);
+      int32_t* spdl = lane_pdl(L);
+      for (int t = threadIdx.x; t < np * W; t += NT) {
+        spv[t] = __ldg(&RC.pat_val[(size_t)p0 * W + t]);
+        spdl[t] = __ldg(&RC.pat_dlt[(size_t)p0 * W + t]);
+      }
+      for (int t = threadIdx.x; t < np; t += NT) {
+        const double dg = __ldg(&RC.pat_diag[p0 + t]);
+        lane_pdg(L)[t] = dg;
+        lane_pdi(L)[t] = __drcp_rn(dg);
+      }
+    }
+    tm_st_wait();
+    __syncthreads();
+
+    // ---- pass A of lane L at iteration it: q = A_p p_it, partials, publish ----
+    auto pass_a = [&](int L, int it) {
+      const int rb = st[L].rb, nr = st[L].nr;
+      const int4 band = st[L].band;
+      const double* sp = lane_sp(L);
+      const uint8_t* sdc = lane_id(L);
+      const double* spv = lane_pv(L);
+      const int32_t* spdl = lane_pdl(L);
+      const double* spdg = lane_pdg(L);
+      const double* spdi = lane_pdi(L);
+      double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int jo = 0; jo < RPT; ++jo) {
+        const int j = band_first<RPT>(jo);
+        const int i = j * NT + threadIdx.x;
+        const double ri = tm_ld(tcol(L, 0, j));
+        if (i < nr) {
+          const double pi = sp[i];
+          const int pt = sdc[i];
+          double off = 0.0;
+#pragma unroll
+          for (int k = 0; k < W; ++k) off += spv[pt * W + k] * sp[i + spdl[pt * W + k]];
+          const double qi = __fma_rn(spdg[pt], pi, off);
+          q[L][j] = qi;
+          const double di = spdi[pt];
+          const double zi = __dmul_rn(di, ri);
+          const double dq = __dmul_rn(di, qi);
+          v[0] += pi * qi;
+          v[1] += zi * qi;
+          v[2] += qi * dq;
+          if (i < band.x || i >= band.y) __stcg(&R2_PUB(pub_q, it & 1, rb)[i], qi);
+        }
+      }
+      unsigned long long* slots = RC.slots + (size_t)3 * kResidNV * gs * (g * NL + L);
+      group_publish<3, NT>(v, red, slots, gs, c, st[L].seq);
+    };
+
+#pragma unroll
+    for (int L = 0; L < NL; ++L)
+      if (st[L].live) pass_a(L, 1);
+
+    // ---- iterations: wait(L) -> pass B(L) -> pass A(L) -> publish(L), lanes in turn ----
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int L = 0; L < NL; ++L) {
+        if (!st[L].live) continue;
+        any = true;
+        double v[3];
+        unsigned long long* slots = RC.slots + (size_t)3 * kResidNV * gs * (g * NL + L);
+        group_wait<3>(v, bc, slots, gs, st[L].seq);
+        const int it = st[L].its + 1;
+        const double sigma = v[0];
+        const int rb = st[L].rb, nr = st[L].nr;
+        const int4 band = st[L].band;
+        double* sp = lane_sp(L);
+        const uint8_t* sdc = lane_id(L);
+        const double* spdi = lane_pdi(L);
+        bool stop = true, fin = false;
+        double alpha = 0.0, beta = 0.0;
+        if (sigma == 0.0) {  // R7: breakdown, d as it stands
+          fin = true;
+        } else {
+          const double rho = st[L].rho;
+          alpha = rho / sigma;
+          const double rho_new = rho - 2.0 * alpha * v[1] + alpha * alpha * v[2];
+          stop = it >= m || !(rho_new > 0.0);  // R7
+          beta = rho_new / rho;
+          // every thread computed the same values; one writes the lane state
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            st[L].its = it;
+            st[L].rho = rho_new;
+            st[L].alpha = alpha;
+            st[L].beta = beta;
+            st[L].seq = st[L].seq + 1;
+          }
+          // ghost rows of p_{it+1} (R29): loads issued before pass B
+          constexpr int kGR = 2;
+          const int ng = band.z + band.w;
+          double gq[kGR], gr[kGR], gpv[kGR];
+          uint32_t gc[kGR];
+          auto ghost_row = [&](int t) { return t < band.z ? t - band.z : nr + (t - band.z); };
+          if (!stop) {
+#pragma unroll
+            for (int u = 0; u < kGR; ++u) {
+              const int t = threadIdx.x + u * NT;
+              if (t < ng) {
+                const int li = ghost_row(t);
+                gq[u] = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
+                gr[u] = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
+                gpv[u] = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
+                gc[u] = __ldg(&D.code[rb + li]);
+              }
+            }
+          }
+          // pass B: d += alpha p, r -= alpha q, p_{it+1} = D^-1 r + beta p (own rows)
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            const int i = j * NT + threadIdx.x;
+            const double dold = it == 1 ? 0.0 : tm_ld(tcol(L, 1, j));
+            const double rold = tm_ld(tcol(L, 0, j));
+            double dn = dold, rn = rold;
+            if (i < nr) {
+              const double pi = sp[i];
+              dn = it == 1 ? alpha * pi : __fma_rn(alpha, pi, dold);
+              if (!stop) {
+                rn = __fma_rn(-alpha, q[L][j], rold);
+                const double pn = __fma_rn(beta, pi, __dmul_rn(spdi[sdc[i]], rn));
+                sp[i] = pn;
+                if (i < band.x || i >= band.y) {
+                  __stcg(&R2_PUB(pub_r, it & 1, rb)[i], rn);
+                  __stcg(&R2_PUB(pub_p, (it + 1) & 1, rb)[i], pn);
+                }
+              }
+            }
+            tm_st(tcol(L, 1, j), dn);
+            tm_st(tcol(L, 0, j), rn);
+          }
+          if (!stop) {
+#pragma unroll
+            for (int u = 0; u < kGR; ++u) {
+              const int t = threadIdx.x + u * NT;
+              if (t < ng)
+                sp[ghost_row(t)] = __fma_rn(beta, gpv[u], __dmul_rn(sinv[gc[u]], __fma_rn(-alpha, gq[u], gr[u])));
+            }
+            for (int t = threadIdx.x + kGR * NT; t < ng; t += NT) {
+              const int li = ghost_row(t);
+              const double q_ = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
+              const double r_ = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
+              const double p_ = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
+              sp[li] = __fma_rn(beta, p_, __dmul_rn(sinv[__ldg(&D.code[rb + li])], __fma_rn(-alpha, q_, r_)));
+            }
+          }
+          tm_st_wait();
+          fin = stop;
+        }
+        if (fin) {
+          // a4: restricted prolongation of the chunk's owned rows
+          __syncthreads();
+          const int its = sigma == 0.0 ? st[L].its : it;
+          if (its > 0) {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+              const int i = j * NT + threadIdx.x;
+              const double dj = tm_ld(tcol(L, 1, j));
+              if (i < nr) {
+                const int32_t s = __ldg(&own_slot[rb + i]);
+                if (s >= 0) x[s] = x[s] + dj;
+              }
+            }
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const int lp = st[L].lp;
+            if (c == 0) {
+              S.its[lp] = its;
+              S.inner_total[lp] += its;
+              S.active[lp] = 0;
+            }
+            st[L].live = 0;
+          }
+          __syncthreads();
+          continue;
+        }
+        __syncthreads();  // p_{it+1} (own rows + ghosts) complete before the gathers
+        pass_a(L, it + 1);
+      }
+      if (!any) break;
+    }
+  }
+#undef R2_PUB
+  // ---- release TMEM ----
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tbase));
+}
+
+}  // namespace ras

@@ -17,6 +17,7 @@
 
 #include "ctx.h"
 #include "kernels.cuh"
+#include "resident2.cuh"
 #include "plan_internal.h"
 #include "ras.h"
 #include "ras_plan.h"
@@ -206,36 +207,46 @@ static const void* resident_kernel(int rpt, bool z, int w, bool tol, bool pat) {
 #undef RAS_RK
 }
 
-static ras_status setup_resident(ras_ctx* c, int nmax) {
-  const ras_plan* pl = c->plan;
-  int sms = 0, smem_optin = 0;
-  RAS_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  RAS_CUDA(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-  // shared memory per chunk row: p, r, d (24 B) + diagonal (SELL-Z: 1 B code, plain: 8 B);
-  // + the dictionary and its reciprocals (4 KB)
-  const int row_b = c->z ? 25 : 32;
-  const int cap = std::min(kResidMaxRPT * kNT_RESID, ((smem_optin - 4096 - 2048) / row_b) / 32 * 32);
-  auto chunk_of = [](int n, int gs) { return ((n / 32 + gs - 1) / gs) * 32; };
-  const int nl = c->nl;
-  int kfit = 0;  // most groups (concurrent subdomains) whose chunks still fit
-  for (int k = 1; k <= std::min(nl, sms); ++k)
-    if (chunk_of(nmax, sms / k) <= cap) kfit = k;
-  if (kfit == 0) return RAS_OK;
-  const int waves = (nl + kfit - 1) / kfit;
-  int k = kfit;  // fewest groups with the same number of waves = most CTAs per subdomain
-  while (k > 1 && (nl + k - 2) / (k - 1) == waves) --k;
-  const int gs = std::min(sms / k, kMaxGroupCTAs);
-  const int chunk = chunk_of(nmax, gs);
-  if (chunk > cap) return RAS_OK;
-  const int need = (chunk + kNT_RESID - 1) / kNT_RESID;
-  const int rpt = need <= 4 ? 4 : need <= 8 ? 8 : kResidMaxRPT;
-  // export bands (chunk rows other CTAs of the group read) and ghost zones (the
-  // columns outside the chunk its rows read), from the CSR of A_p
-  std::vector<int4> band((size_t)nl * gs);
+// k_resident2 instantiations: rows per thread x SELL-Z width (4 / 8) x lanes
+static const void* resident2_kernel(int rpt, int w, int lanes) {
+#define RAS_R2(RPT)                                                                                   \
+  if (lanes == 2) return w == 4 ? (const void*)k_resident2<RPT, 4, 2> : (const void*)k_resident2<RPT, 8, 2>; \
+  return w == 4 ? (const void*)k_resident2<RPT, 4, 1> : (const void*)k_resident2<RPT, 8, 1>;
+  if (rpt <= 4) {
+    RAS_R2(4)
+  } else if (rpt <= 8) {
+    RAS_R2(8)
+  } else if (rpt <= 12) {
+    RAS_R2(12)
+  } else if (rpt <= 16) {
+    RAS_R2(16)
+  }
+  if (lanes == 2) return nullptr;
+  return w == 4 ? (const void*)k_resident2<kR2MaxRPT, 4, 1> : (const void*)k_resident2<kR2MaxRPT, 8, 1>;
+#undef RAS_R2
+}
+
+// Per-chunk export bands / ghost zones and (PAT) row-pattern tables of every
+// local subdomain for a group of gs CTAs (chunk = the rows of one CTA).
+struct ResidLayout {
+  std::vector<int4> band;
   int glo_max = 0, ghi_max = 0;
+  bool pat = false;
+  std::vector<int32_t> pat_off, pat_cnt, pat_dlt;
+  std::vector<double> pat_val, pat_diag;
+  std::vector<uint8_t> pid;
+};
+
+static int chunk_rows(int n, int gs) { return ((n / 32 + gs - 1) / gs) * 32; }
+
+static void resident_layout(const ras_ctx* c, int gs, bool want_pat, ResidLayout& Lo) {
+  const ras_plan* pl = c->plan;
+  const int nl = c->nl;
+  Lo.band.assign((size_t)nl * gs, make_int4(0, 0, 0, 0));
+  Lo.glo_max = Lo.ghi_max = 0;
   for (int lp = 0; lp < nl; ++lp) {
     const auto& S = pl->subs[lp];
-    const int n = (int)S.nrows_pad, ch = chunk_of(n, gs);
+    const int n = (int)S.nrows_pad, ch = chunk_rows(n, gs);
     std::vector<int> lo(gs, 0), hi(gs), len(gs), glo(gs, 0), ghi(gs, 0);
     for (int cc = 0; cc < gs; ++cc) {
       const int a = std::min(n, cc * ch);
@@ -260,33 +271,32 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
       }
     }
     for (int cc = 0; cc < gs; ++cc) {
-      band[(size_t)lp * gs + cc] = make_int4(lo[cc], hi[cc], glo[cc], ghi[cc]);
-      glo_max = std::max(glo_max, glo[cc]);
-      ghi_max = std::max(ghi_max, ghi[cc]);
+      Lo.band[(size_t)lp * gs + cc] = make_int4(lo[cc], hi[cc], glo[cc], ghi[cc]);
+      Lo.glo_max = std::max(Lo.glo_max, glo[cc]);
+      Lo.ghi_max = std::max(Lo.ghi_max, ghi[cc]);
     }
   }
   // row-pattern dictionary per chunk (PAT): SELL-Z matrices whose every chunk has
   // <= kMaxPat distinct rows (diagonal + (delta, value) list); then no matrix
   // stream from L2 in the SpMV
-  std::vector<int32_t> pat_off((size_t)nl * gs, 0), pat_cnt((size_t)nl * gs, 0), pat_dlt;
-  std::vector<double> pat_val, pat_diag;
-  std::vector<uint8_t> pid;
-#ifdef RAS_NO_PAT  // timing experiment: force the SELL-Z stream
-  bool pat = false;
-#else
-  bool pat = c->z;
-#endif
+  Lo.pat_off.assign((size_t)nl * gs, 0);
+  Lo.pat_cnt.assign((size_t)nl * gs, 0);
+  Lo.pat_dlt.clear();
+  Lo.pat_val.clear();
+  Lo.pat_diag.clear();
+  Lo.pid.clear();
+  bool pat = want_pat && c->z;
   if (pat) {
     const int W = c->zwL;
-    pid.assign((size_t)c->rows_pad, 0);
+    Lo.pid.assign((size_t)c->rows_pad, 0);
     std::vector<uint64_t> key;
     for (int lp = 0; lp < nl && pat; ++lp) {
       const auto& S = pl->subs[lp];
-      const int n = (int)S.nrows_pad, ch = chunk_of(n, gs);
+      const int n = (int)S.nrows_pad, ch = chunk_rows(n, gs);
       for (int cc = 0; cc < gs && pat; ++cc) {
         const int a = std::min(n, cc * ch), e = std::min(n, a + ch);
         std::vector<std::vector<uint64_t>> keys;  // this chunk's distinct patterns
-        pat_off[(size_t)lp * gs + cc] = (int32_t)pat_diag.size();
+        Lo.pat_off[(size_t)lp * gs + cc] = (int32_t)Lo.pat_diag.size();
         for (int i = a; i < e; ++i) {
           const int64_t row = S.row_off + i;
           key.assign(1 + 2 * W, 0);
@@ -314,50 +324,125 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
               break;
             }
             keys.push_back(key);
-            pat_diag.push_back(dg);
+            Lo.pat_diag.push_back(dg);
             for (int t = 0; t < W; ++t) {
-              pat_dlt.push_back((int32_t)(uint32_t)key[1 + t]);
+              Lo.pat_dlt.push_back((int32_t)(uint32_t)key[1 + t]);
               double v;
               std::memcpy(&v, &key[1 + W + t], 8);
-              pat_val.push_back(v);
+              Lo.pat_val.push_back(v);
             }
           }
-          pid[(size_t)row] = (uint8_t)id;
+          Lo.pid[(size_t)row] = (uint8_t)id;
         }
-        pat_cnt[(size_t)lp * gs + cc] = (int32_t)keys.size();
+        Lo.pat_cnt[(size_t)lp * gs + cc] = (int32_t)keys.size();
       }
     }
   }
-  const size_t pat_smem = pat ? (size_t)kMaxPat * (8 * (size_t)c->zwL + 8 + 8 + 4 * (size_t)c->zwL) + 8 : 0;
-  const size_t smem = (size_t)8 * (glo_max + ghi_max) + (size_t)24 * chunk +
-                      (c->z ? 4096 + (size_t)((chunk + 7) & ~7) : (size_t)8 * chunk) + pat_smem;
-  if (smem + 2048 > (size_t)smem_optin) return RAS_OK;  // ghost zones too wide: TILED
+  Lo.pat = pat;
+}
+
+// RESIDENT path setup: group count / size, kernel version and rows per thread,
+// export bands, barrier counters and partial-sum slots.  Leaves c->path alone
+// when no configuration fits (the caller falls back to TILED).
+//   v2 (k_resident2, r and d in tensor memory): fixed-m solves on row-pattern
+//      matrices; NL = 2 interleaved subdomains when two lanes fit a CTA, else
+//      NL = 1 with chunks up to kR2MaxRPT x 768 rows;
+//   v1 (k_resident_pcg): everything else that fits (tolerance solves, SELL-Z
+//      stream / plain SELL matrices).  RAS_RESIDENT_KERNEL=1 forces v1 (A/B runs).
+static ras_status setup_resident(ras_ctx* c, int nmax) {
+  int sms = 0, smem_optin = 0;
+  RAS_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  RAS_CUDA(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const int nl = c->nl;
   const bool tol = c->opt.local_solver == RAS_LS_EXACT_PCG || c->opt.inner_tol > 0.0;
-  const void* fn = resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol, pat);
+  const char* env = getenv("RAS_RESIDENT_KERNEL");
+  const bool v2_ok = c->z && !tol && !(env && env[0] == '1');
+  // fewest groups with the largest concurrency that fits `cap` rows per CTA
+  auto pick = [&](int units, int cap, int* k_out, int* gs_out) {
+    int kfit = 0;
+    for (int k = 1; k <= std::min(units, sms); ++k)
+      if (chunk_rows(nmax, std::min(sms / k, kMaxGroupCTAs)) <= cap) kfit = k;
+    if (kfit == 0) return false;
+    const int waves = (units + kfit - 1) / kfit;
+    int k = kfit;
+    while (k > 1 && (units + k - 2) / (k - 1) == waves) --k;
+    *k_out = k;
+    *gs_out = std::min(sms / k, kMaxGroupCTAs);
+    return true;
+  };
+  ResidLayout Lo;
+  int k = 0, gs = 0, chunk = 0, lanes = 0;
+  size_t smem = 0;
+  const size_t r2_static = 8 * (kResidNV * (kNT_R2 / 32) + kResidNV + 256) + sizeof(R2Lane) * 2 + 64;
+  if (v2_ok) {
+    for (int NL = 2; NL >= 1 && !lanes; --NL) {
+      const int maxrpt = std::min(kR2ColBlk / 4 / NL, kR2MaxRPT);
+      if (!pick((nl + NL - 1) / NL, maxrpt * kNT_R2, &k, &gs)) continue;
+      chunk = chunk_rows(nmax, gs);
+      resident_layout(c, gs, true, Lo);
+      if (!Lo.pat) break;  // not a row-pattern matrix: v1 below
+      const size_t need = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL) + r2_static;
+      if (need + 1024 <= (size_t)smem_optin) {
+        lanes = NL;
+        smem = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL);
+      }
+    }
+  }
+  if (!lanes) {
+    // v1: shared memory per chunk row p, r, d (24 B) + diagonal (SELL-Z: 1 B code, plain: 8 B)
+    const int row_b = c->z ? 25 : 32;
+    const int cap = std::min(kResidMaxRPT * kNT_RESID, ((smem_optin - 4096 - 2048) / row_b) / 32 * 32);
+    if (!pick(nl, cap, &k, &gs)) return RAS_OK;
+    chunk = chunk_rows(nmax, gs);
+    if (chunk > cap) return RAS_OK;
+#ifdef RAS_NO_PAT  // timing experiment: force the SELL-Z stream
+    resident_layout(c, gs, false, Lo);
+#else
+    resident_layout(c, gs, true, Lo);
+#endif
+    const size_t pat_smem = Lo.pat ? (size_t)kMaxPat * (8 * (size_t)c->zwL + 8 + 8 + 4 * (size_t)c->zwL) + 8 : 0;
+    smem = (size_t)8 * (Lo.glo_max + Lo.ghi_max) + (size_t)24 * chunk +
+           (c->z ? 4096 + (size_t)((chunk + 7) & ~7) : (size_t)8 * chunk) + pat_smem;
+    if (smem + 2048 > (size_t)smem_optin) return RAS_OK;  // ghost zones too wide: TILED
+  }
+  const int nt = lanes ? kNT_R2 : kNT_RESID;
+  const int need = (chunk + nt - 1) / nt;
+  int rpt;
+  if (lanes) {
+    rpt = need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : kR2MaxRPT;
+    if (lanes == 2 && rpt > 16) return set_err(c, RAS_ESTATE, "resident v2: two lanes need <= 16 rows per thread");
+  } else {
+    rpt = need <= 4 ? 4 : need <= 8 ? 8 : kResidMaxRPT;
+  }
+  const void* fn = lanes ? resident2_kernel(rpt, c->zwL, lanes)
+                         : resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol, Lo.pat);
+  if (!fn) return RAS_OK;
   TRY(allow_smem(c, fn));
   int per_sm = 0;
-  RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT_RESID, smem));
+  RAS_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem));
   if (per_sm < 1) return RAS_OK;
   int4* dband;
-  TRY(upload(c, &dband, band));
-  c->resid_glo = glo_max;
-  c->resid_ghi = ghi_max;
-  TRY(zalloc(c, &c->d_resid_slots, (size_t)k * 3 * kResidNV * gs));
+  TRY(upload(c, &dband, Lo.band));
+  c->resid_glo = Lo.glo_max;
+  c->resid_ghi = Lo.ghi_max;
+  // slot rings: one per (group, lane)
+  TRY(zalloc(c, &c->d_resid_slots, (size_t)k * std::max(lanes, 1) * 3 * kResidNV * gs));
   double* q2;
   TRY(zalloc(c, &q2, (size_t)c->rows_pad));
   // published export-band values (kernels.cuh): pub_p[1] = k_residual's p, pub_r[0] = its r
   int32_t *dpo = nullptr, *dpc = nullptr, *dpd = nullptr;
   double *dpv = nullptr, *dpg = nullptr;
   uint8_t* dpid = nullptr;
-  if (pat) {
-    TRY(upload(c, &dpo, pat_off));
-    TRY(upload(c, &dpc, pat_cnt));
-    TRY(upload(c, &dpd, pat_dlt, 1));
-    TRY(upload(c, &dpv, pat_val, 1));
-    TRY(upload(c, &dpg, pat_diag, 1));
-    TRY(upload(c, &dpid, pid, 1));
+  if (Lo.pat) {
+    TRY(upload(c, &dpo, Lo.pat_off));
+    TRY(upload(c, &dpc, Lo.pat_cnt));
+    TRY(upload(c, &dpd, Lo.pat_dlt, 1));
+    TRY(upload(c, &dpv, Lo.pat_val, 1));
+    TRY(upload(c, &dpg, Lo.pat_diag, 1));
+    TRY(upload(c, &dpid, Lo.pid, 1));
   }
-  c->resid_pat = pat;
+  c->resid_pat = Lo.pat;
+  c->resid_lanes = lanes;
   c->RC = ResidentCtl{dband, c->d_resid_slots, dpo, dpc, dpv, dpd, dpg, dpid,
                       {c->d_p2, c->d_p}, {c->d_r, c->d_d}, {c->d_q, q2}, k, gs};
   c->resid_rpt = rpt;
@@ -961,18 +1046,23 @@ static ras_status enq_small_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl 
 static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m, double inner_tol, int lp_first,
                                    int nsub_) {
   // every reduction slot starts empty (kSlotEmpty = all ones)
-  RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff, (size_t)c->RC.ngroups * 3 * kResidNV * c->RC.gs * 8, s));
-  const void* fn = resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0, c->resid_pat);
+  RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff,
+                              (size_t)c->RC.ngroups * std::max(c->resid_lanes, 1) * 3 * kResidNV * c->RC.gs * 8, s));
+  const bool v2 = c->resid_lanes > 0 && !(inner_tol > 0.0);
+  const void* fn = v2 ? resident2_kernel(c->resid_rpt, c->zwL, c->resid_lanes)
+                      : resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0, c->resid_pat);
   int lp0 = lp_first, nsub = nsub_;
   const int32_t* own = c->d_own_slot;
   double* x = c->d_x;
   int32_t chunk_max = c->resid_chunk, glo = c->resid_glo, ghi = c->resid_ghi;
   int32_t ntable = c->z ? (int32_t)c->plan->z_table.size() : 0;
-  void* args[] = {&lp0, &nsub, &c->SS, &c->RC, &c->L,      &c->D,      &own, &x,  &c->S,
-                  &C,   &m,    &inner_tol,     &chunk_max, &glo,       &ghi, &ntable};
+  void* args1[] = {&lp0, &nsub, &c->SS, &c->RC, &c->L,      &c->D,      &own, &x,  &c->S,
+                   &C,   &m,    &inner_tol,     &chunk_max, &glo,       &ghi, &ntable};
+  void* args2[] = {&lp0, &nsub, &c->SS, &c->RC, &c->D, &own, &x, &c->S, &C, &m, &chunk_max, &glo, &ghi, &ntable};
+  void** args = v2 ? args2 : args1;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(c->RC.ngroups * c->RC.gs));
-  cfg.blockDim = dim3(kNT_RESID);
+  cfg.blockDim = dim3(v2 ? kNT_R2 : kNT_RESID);
   cfg.dynamicSmemBytes = c->resid_smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -1442,6 +1532,7 @@ static void finish_stats(ras_ctx* c, ras_mode mode, double t) {
   // schedule (R34), everything else the streaming kernels
   c->st.pcg_path = c->chol ? RAS_PCG_BLOCK : c->ic ? RAS_PCG_TILED : c->path;
   c->st.resident_pattern = c->path == RAS_PCG_RESIDENT && c->resid_pat;
+  c->st.resident_lanes = c->path == RAS_PCG_RESIDENT ? c->resid_lanes : 0;
   c->st.rows_local = c->plan->rows_local;
   c->st.halo_values = c->n_halo;
   c->st.kernel_launches = c->launches;

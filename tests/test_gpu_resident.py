@@ -42,6 +42,46 @@ def test_resident_branches_match_oracle(matrix, pattern, part):
     s.close()
 
 
+@pytest.mark.parametrize("kernel", ["v1", "v2"])
+@pytest.mark.parametrize("shape", ["c2like", "big_chunks", "odd_count"])
+def test_resident_kernels_match_oracle(kernel, shape, monkeypatch):
+    # k_resident_pcg (v1: r, d in shared memory) and k_resident2 (v2: r, d in tensor
+    # memory; two subdomains interleaved per CTA when they fit, else one lane with
+    # chunks up to 512 x 24 rows) on row-pattern matrices, 1e-10 vs the oracle
+    if kernel == "v1":
+        monkeypatch.setenv("RAS_RESIDENT_KERNEL", "1")
+    else:
+        monkeypatch.delenv("RAS_RESIDENT_KERNEL", raising=False)
+    if shape == "c2like":    # 4 x 4 subdomains of 256^2 (+ overlap): two lanes per CTA
+        N, px, gamma, m, owner = 1024, 4, 8, 20, None
+    elif shape == "big_chunks":  # one subdomain of 1300^2 rows on the whole GPU: one lane, > 7.7 K rows per CTA
+        N, px, gamma, m, owner = 1300, 1, 0, 6, None
+    else:                    # 5 irregular subdomains: the last pair has one live lane
+        N, px, gamma, m = 600, 0, 3, 8
+        owner = ri.voronoi_partition(N, N, 5, seed=4)
+    A = ri.laplace_2d(N)
+    b = ri.rhs(A.n, 0)
+    if owner is None:
+        owner = O.partition_regular(N, N, 1, px, px, 1)
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, path="resident"))
+    K = 2
+    st, x = s.solve(1e-300, K, "sync")
+    t = s.stats()
+    assert t["pcg_path"] == 3 and t["resident_pattern"] == 1, t
+    if kernel == "v1":
+        assert t["resident_lanes"] == 0
+    else:
+        assert t["resident_lanes"] == (1 if shape == "big_chunks" else 2), t
+    s.close()
+    # oracle: sampled subdomains at the larger sizes would be slow; the whole
+    # problem at these sizes runs in seconds with scipy
+    subs = O.setup(A, b, owner, gamma)
+    for sb in subs:
+        O.make_local_solver(sb, "jacobi", m)
+    ref = O.ras_sync(A, b, subs, 1e-300, K, record_iterates=True)
+    assert rel(x, ref.iterates[K]) <= 1e-10, rel(x, ref.iterates[K])
+
+
 def test_resident_irregular_converges_sync_and_async():
     nx, ny = 260, 250
     A = ri.varcoef_2d(nx, ny, seed=11)
