@@ -188,6 +188,9 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
   // published arrays re-based to a chunk (select, not index)
 #define R2_PUB(arr, par, rb) (((par) ? RC.arr[1] : RC.arr[0]) + (rb))
 
+  // reduction counters run over the whole launch (like k_resident_pcg's): the
+  // 3-deep slot ring of a lane is only safe while every CTA agrees on its position
+  if (threadIdx.x < NL) st[threadIdx.x].seq = 0;
   for (int pair = g; pair * NL < nsub; pair += RC.ngroups) {
     // ---- lane set-up: load p_1, r_0, pattern ids and the chunk's pattern table ----
 #pragma unroll
@@ -199,7 +202,6 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
         st[L].lp = lp;
         st[L].live = valid && !stopped(C, lp) && S.active[lp];
         st[L].its = 0;
-        st[L].seq = 0;
         st[L].alpha = st[L].beta = 0.0;
         if (st[L].live) {
           const int r0 = SS.row_off[lp], n = SS.nrows[lp];
