@@ -142,18 +142,58 @@ struct R2Lane {
   unsigned seq;
 };
 
+// Named barriers (id 0 is __syncthreads): compute warps only; partials of lane
+// L ready (compute arrive, reduction warp waits); result of lane L ready
+// (reduction warp arrives, compute warps wait).
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+constexpr int kBarCompute = 1;
+__device__ __forceinline__ int bar_part(int L) { return 2 + L; }
+__device__ __forceinline__ int bar_res(int L) { return 4 + L; }
+
+// four consecutive TMEM doubles (8 columns) of this thread's lane
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, double (&v)[4]) {
+  uint32_t a[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = __longlong_as_double((long long)(((unsigned long long)a[2 * k + 1] << 32) | a[2 * k]));
+}
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const double (&v)[4]) {
+  uint32_t a[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(v[k]);
+    a[2 * k] = (uint32_t)u;
+    a[2 * k + 1] = (uint32_t)(u >> 32);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a[0]),
+               "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Warp-specialised CTA: warp 0 is the REDUCTION warp (sums the compute warps'
+// partials, publishes them to the group's slot ring, polls it, computes alpha /
+// beta / the stop decision); warps 1..15 are COMPUTE warps (rows j * kNC + ct,
+// ct = threadIdx.x - 32).  They meet only at named barriers, so the compute warps
+// never wait for the release fence or the poll of a reduction they do not need yet.
+constexpr int kNC_R2 = kNT_R2 - 32;  // compute threads
+
 template <int RPT, int W, int NL>
 static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int nsub, SmallSubs SS, ResidentCtl RC,
                                                                    Diag D, const int32_t* __restrict__ own_slot,
                                                                    double* __restrict__ x, Scal S, Ctl C, int32_t m,
                                                                    int32_t chunk_max, int32_t glo_max, int32_t ghi_max,
                                                                    int32_t ntable) {
-  constexpr int NT = kNT_R2;
+  constexpr int NT = kNT_R2, NC = kNC_R2, NCW = NC / 32;
+  static_assert(RPT % 4 == 0, "TMEM rows move in groups of four");
   static_assert(2 * 2 * NL * RPT <= kR2ColBlk, "r, d of NL lanes x RPT rows must fit the warp's TMEM columns");
   extern __shared__ double smem[];
-  __shared__ double red[kResidNV][NT / 32];
-  __shared__ double bc[kResidNV];
-  __shared__ double sinv[256];  // __drcp_rn of every dictionary value (ghost rows' D^-1)
+  __shared__ double red[NL][3][NCW];  // compute warps' partials per lane
+  __shared__ double sinv[256];         // __drcp_rn of every dictionary value (ghost rows' D^-1)
   __shared__ R2Lane st[NL];
   __shared__ uint32_t s_tbase;
   // per-lane shared memory: p (+ ghost zones) | pattern ids | pattern table
@@ -167,7 +207,8 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
   auto lane_pdi = [&](int L) { return lane_pdg(L) + kMaxPat; };
   auto lane_pdl = [&](int L) { return reinterpret_cast<int32_t*>(lane_pdi(L) + kMaxPat); };  // [kMaxPat][W]
 
-  const int w = threadIdx.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ct = threadIdx.x - 32;  // compute thread index (< 0 in the reduction warp)
   // ---- TMEM: 512 columns for this CTA (one CTA per SM) ----
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -183,7 +224,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
 
   const int gs = RC.gs;
   const int g = blockIdx.x / gs, c = blockIdx.x - g * gs;
-  double q[NL][RPT];
+  auto lane_slots = [&](int L) { return RC.slots + (size_t)3 * kResidNV * gs * (g * NL + L); };
 
   // published arrays re-based to a chunk (select, not index)
 #define R2_PUB(arr, par, rb) (((par) ? RC.arr[1] : RC.arr[0]) + (rb))
@@ -192,7 +233,8 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
   // 3-deep slot ring of a lane is only safe while every CTA agrees on its position
   if (threadIdx.x < NL) st[threadIdx.x].seq = 0;
   for (int pair = g; pair * NL < nsub; pair += RC.ngroups) {
-    // ---- lane set-up: load p_1, r_0, pattern ids and the chunk's pattern table ----
+    // ---- lane set-up (all warps): p_1, r_0, pattern ids and the chunk's pattern table ----
+    bool live[NL];
 #pragma unroll
     for (int L = 0; L < NL; ++L) {
       const int lp = lp_base + pair * NL + L;
@@ -214,7 +256,8 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
         }
       }
       __syncthreads();
-      if (!st[L].live) continue;
+      live[L] = st[L].live;
+      if (!live[L]) continue;
       const int rb = st[L].rb, nr = st[L].nr;
       const int4 band = st[L].band;
       double* sp = lane_sp(L);
@@ -228,10 +271,17 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
         sp[i] = __ldcg(&R2_PUB(pub_p, 1, rb)[i]);  // p_1 = z_0
         sdc[i] = __ldg(&RC.pid[rb + i]);
       }
+      if (ct >= 0) {
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int i = j * NT + threadIdx.x;
-        tm_st(tcol(L, 0, j), i < nr ? __ldcg(&R2_PUB(pub_r, 0, rb)[i]) : 0.0);  // r_0
+        for (int b = 0; b < RPT / 4; ++b) {
+          double rr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = (4 * b + u) * NC + ct;
+            rr[u] = i < nr ? __ldcg(&R2_PUB(pub_r, 0, rb)[i]) : 0.0;  // r_0
+          }
+          tm_st4(tcol(L, 0, 4 * b), rr);
+        }
       }
       const int p0 = RC.pat_off[lp * gs + c], np = RC.pat_cnt[lp * gs + c];
       double* spv = lane_pv(L);
@@ -249,176 +299,274 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
     tm_st_wait();
     __syncthreads();
 
-    // ---- pass A of lane L at iteration it: q = A_p p_it, partials, publish ----
-    auto pass_a = [&](int L, int it) {
-      const int rb = st[L].rb, nr = st[L].nr;
-      const int4 band = st[L].band;
-      const double* sp = lane_sp(L);
-      const uint8_t* sdc = lane_id(L);
-      const double* spv = lane_pv(L);
-      const int32_t* spdl = lane_pdl(L);
-      const double* spdg = lane_pdg(L);
-      const double* spdi = lane_pdi(L);
-      double v[3] = {0.0, 0.0, 0.0};
+    if (w == 0) {
+      // ================= reduction warp =================
+      auto publish = [&](int L) {  // the compute warps' partials of lane L -> slot ring
+        nbar_sync(bar_part(L), NT);
+        double s3[3];
 #pragma unroll
-      for (int jo = 0; jo < RPT; ++jo) {
-        const int j = band_first<RPT>(jo);
-        const int i = j * NT + threadIdx.x;
-        const double ri = tm_ld(tcol(L, 0, j));
-        if (i < nr) {
-          const double pi = sp[i];
-          const int pt = sdc[i];
-          double off = 0.0;
+        for (int j = 0; j < 3; ++j) s3[j] = warp_sum(lane < NCW ? red[L][j][lane] : 0.0);
+        unsigned long long* slots = lane_slots(L);
+        const unsigned seq = st[L].seq;
+        unsigned long long* const ring = slots + (size_t)(seq % 3) * gs * 4;
+        unsigned long long* const nxt = slots + (size_t)((seq + 1) % 3) * gs * 4;
+        if (lane == 0) {
 #pragma unroll
-          for (int k = 0; k < W; ++k) off += spv[pt * W + k] * sp[i + spdl[pt * W + k]];
-          const double qi = __fma_rn(spdg[pt], pi, off);
-          q[L][j] = qi;
-          const double di = spdi[pt];
-          const double zi = __dmul_rn(di, ri);
-          const double dq = __dmul_rn(di, qi);
-          v[0] += pi * qi;
-          v[1] += zi * qi;
-          v[2] += qi * dq;
-          if (i < band.x || i >= band.y) __stcg(&R2_PUB(pub_q, it & 1, rb)[i], qi);
-        }
-      }
-      unsigned long long* slots = RC.slots + (size_t)3 * kResidNV * gs * (g * NL + L);
-      group_publish<3, NT>(v, red, slots, gs, c, st[L].seq);
-    };
-
+          for (int j = 0; j < 3; ++j) st_relaxed_gpu_u64(&nxt[c * 4 + j], kSlotEmpty);
+          // release: the compute warps' export-band stores (ordered before this
+          // thread by the named barrier) before the partial sums
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #pragma unroll
-    for (int L = 0; L < NL; ++L)
-      if (st[L].live) pass_a(L, 1);
-
-    // ---- iterations: wait(L) -> pass B(L) -> pass A(L) -> publish(L), lanes in turn ----
-    for (;;) {
-      bool any = false;
-#pragma unroll
-      for (int L = 0; L < NL; ++L) {
-        if (!st[L].live) continue;
-        any = true;
-        double v[3];
-        unsigned long long* slots = RC.slots + (size_t)3 * kResidNV * gs * (g * NL + L);
-        group_wait<3>(v, bc, slots, gs, st[L].seq);
-        const int it = st[L].its + 1;
-        const double sigma = v[0];
-        const int rb = st[L].rb, nr = st[L].nr;
-        const int4 band = st[L].band;
-        double* sp = lane_sp(L);
-        const uint8_t* sdc = lane_id(L);
-        const double* spdi = lane_pdi(L);
-        bool stop = true, fin = false;
-        double alpha = 0.0, beta = 0.0;
-        if (sigma == 0.0) {  // R7: breakdown, d as it stands
-          fin = true;
-        } else {
-          const double rho = st[L].rho;
-          alpha = rho / sigma;
-          const double rho_new = rho - 2.0 * alpha * v[1] + alpha * alpha * v[2];
-          stop = it >= m || !(rho_new > 0.0);  // R7
-          beta = rho_new / rho;
-          // every thread computed the same values; one writes the lane state
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            st[L].its = it;
-            st[L].rho = rho_new;
-            st[L].alpha = alpha;
-            st[L].beta = beta;
-            st[L].seq = st[L].seq + 1;
+          for (int j = 0; j < 3; ++j) {
+            unsigned long long u = (unsigned long long)__double_as_longlong(s3[j]);
+            if (u == kSlotEmpty) u = 0x7ff8000000000000ull;
+            st_relaxed_gpu_u64(&ring[c * 4 + j], u);
           }
-          // ghost rows of p_{it+1} (R29): loads issued before pass B
-          constexpr int kGR = 2;
-          const int ng = band.z + band.w;
-          double gq[kGR], gr[kGR], gpv[kGR];
-          uint32_t gc[kGR];
-          auto ghost_row = [&](int t) { return t < band.z ? t - band.z : nr + (t - band.z); };
-          if (!stop) {
+        }
+        __syncwarp();
+      };
 #pragma unroll
-            for (int u = 0; u < kGR; ++u) {
-              const int t = threadIdx.x + u * NT;
-              if (t < ng) {
-                const int li = ghost_row(t);
-                gq[u] = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
-                gr[u] = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
-                gpv[u] = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
-                gc[u] = __ldg(&D.code[rb + li]);
-              }
+      for (int L = 0; L < NL; ++L)
+        if (live[L]) publish(L);
+      for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int L = 0; L < NL; ++L) {
+          if (!live[L]) continue;
+          any = true;
+          double v[3];
+          // poll every CTA's slot of this lane's reduction, fixed-order sum (group_wait)
+          {
+            const unsigned long long* const ring = lane_slots(L) + (size_t)(st[L].seq % 3) * gs * 4;
+            constexpr int KS = (kMaxGroupCTAs + 31) / 32;
+            unsigned long long u[KS][3];
+#pragma unroll
+            for (int t = 0; t < KS; ++t)
+#pragma unroll
+              for (int j = 0; j < 3; ++j) u[t][j] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
+            for (;;) {
+              bool done = true;
+#pragma unroll
+              for (int t = 0; t < KS; ++t)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                  if (u[t][j] == kSlotEmpty) u[t][j] = ld_relaxed_gpu_u64(&ring[(lane + 32 * t) * 4 + j]);
+#pragma unroll
+              for (int t = 0; t < KS; ++t)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) done = done && u[t][j] != kSlotEmpty;
+              if (__all_sync(0xffffffffu, done)) break;
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the peers' export-band stores
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              double acc = 0.0;
+#pragma unroll
+              for (int t = 0; t < KS; ++t) acc += __longlong_as_double((long long)u[t][j]);
+              v[j] = warp_allsum(acc);
             }
           }
-          // pass B: d += alpha p, r -= alpha q, p_{it+1} = D^-1 r + beta p (own rows)
+          // PCG scalars of iteration it (R28; R7 breakdowns)
+          const int it = st[L].its + 1;
+          const double sigma = v[0];
+          if (lane == 0) {
+            if (sigma == 0.0) {
+              st[L].seq = st[L].seq + 1;
+              st[L].live = 2;  // breakdown: prolong d as it stands
+            } else {
+              const double rho = st[L].rho;
+              const double alpha = rho / sigma;
+              const double rho_new = rho - 2.0 * alpha * v[1] + alpha * alpha * v[2];
+              const bool stop = it >= m || !(rho_new > 0.0);
+              st[L].alpha = alpha;
+              st[L].beta = rho_new / rho;
+              st[L].rho = rho_new;
+              st[L].its = it;
+              st[L].seq = st[L].seq + 1;
+              st[L].live = stop ? 3 : 1;  // 3: last pass B, then prolong
+            }
+          }
+          __syncwarp();
+          const int phase = st[L].live;
+          nbar_arrive(bar_res(L), NT);
+          if (phase == 1) {
+            publish(L);
+          } else {
+            live[L] = false;
+          }
+        }
+        if (!any) break;
+      }
+    } else {
+      // ================= compute warps =================
+      double q[NL][RPT];
+      auto pass_a = [&](int L, int it) {
+        const int rb = st[L].rb, nr = st[L].nr;
+        const int4 band = st[L].band;
+        const double* sp = lane_sp(L);
+        const uint8_t* sdc = lane_id(L);
+        const double* spv = lane_pv(L);
+        const int32_t* spdl = lane_pdl(L);
+        const double* spdg = lane_pdg(L);
+        const double* spdi = lane_pdi(L);
+        double v[3] = {0.0, 0.0, 0.0};
+        double rr[2][4];
+        tm_ld4(tcol(L, 0, 0), rr[0]);
+        tm_ld_wait();
 #pragma unroll
-          for (int j = 0; j < RPT; ++j) {
-            const int i = j * NT + threadIdx.x;
-            const double dold = it == 1 ? 0.0 : tm_ld(tcol(L, 1, j));
-            const double rold = tm_ld(tcol(L, 0, j));
-            double dn = dold, rn = rold;
+        for (int b = 0; b < RPT / 4; ++b) {
+          if (b + 1 < RPT / 4) tm_ld4(tcol(L, 0, 4 * (b + 1)), rr[(b + 1) & 1]);  // in flight during rows of b
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * b + u;
+            const int i = j * NC + ct;
             if (i < nr) {
               const double pi = sp[i];
-              dn = it == 1 ? alpha * pi : __fma_rn(alpha, pi, dold);
-              if (!stop) {
-                rn = __fma_rn(-alpha, q[L][j], rold);
-                const double pn = __fma_rn(beta, pi, __dmul_rn(spdi[sdc[i]], rn));
-                sp[i] = pn;
-                if (i < band.x || i >= band.y) {
-                  __stcg(&R2_PUB(pub_r, it & 1, rb)[i], rn);
-                  __stcg(&R2_PUB(pub_p, (it + 1) & 1, rb)[i], pn);
+              const int pt = sdc[i];
+              double off = 0.0;
+#pragma unroll
+              for (int k = 0; k < W; ++k) off += spv[pt * W + k] * sp[i + spdl[pt * W + k]];
+              const double qi = __fma_rn(spdg[pt], pi, off);
+              q[L][j] = qi;
+              const double di = spdi[pt];
+              const double zi = __dmul_rn(di, rr[b & 1][u]);
+              const double dq = __dmul_rn(di, qi);
+              v[0] += pi * qi;
+              v[1] += zi * qi;
+              v[2] += qi * dq;
+              if (i < band.x || i >= band.y) __stcg(&R2_PUB(pub_q, it & 1, rb)[i], qi);
+            }
+          }
+          tm_ld_wait();
+        }
+        // this warp's partials -> shared memory, then hand them to the reduction warp
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double s = warp_sum(v[j]);
+          if (lane == 0) red[L][j][w - 1] = s;
+        }
+        nbar_arrive(bar_part(L), NT);
+      };
+#pragma unroll
+      for (int L = 0; L < NL; ++L)
+        if (live[L]) pass_a(L, 1);
+      for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int L = 0; L < NL; ++L) {
+          if (!live[L]) continue;
+          any = true;
+          nbar_sync(bar_res(L), NT);  // the reduction warp's scalars of this iteration
+          const int phase = st[L].live;
+          const int it = st[L].its;    // the iteration just reduced (unchanged on breakdown)
+          const double alpha = st[L].alpha, beta = st[L].beta;
+          const int rb = st[L].rb, nr = st[L].nr;
+          const int4 band = st[L].band;
+          double* sp = lane_sp(L);
+          const uint8_t* sdc = lane_id(L);
+          const double* spdi = lane_pdi(L);
+          if (phase != 2) {
+            const bool stop = phase == 3;
+            // ghost rows of p_{it+1} (R29): loads issued before pass B
+            constexpr int kGR = 2;
+            const int ng = band.z + band.w;
+            double gq[kGR], gr[kGR], gpv[kGR];
+            uint32_t gc[kGR];
+            auto ghost_row = [&](int t) { return t < band.z ? t - band.z : nr + (t - band.z); };
+            if (!stop) {
+#pragma unroll
+              for (int u = 0; u < kGR; ++u) {
+                const int t = ct + u * NC;
+                if (t < ng) {
+                  const int li = ghost_row(t);
+                  gq[u] = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
+                  gr[u] = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
+                  gpv[u] = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
+                  gc[u] = __ldg(&D.code[rb + li]);
                 }
               }
             }
-            tm_st(tcol(L, 1, j), dn);
-            tm_st(tcol(L, 0, j), rn);
-          }
-          if (!stop) {
+            // pass B: d += alpha p, r -= alpha q, p_{it+1} = D^-1 r + beta p (own rows)
 #pragma unroll
-            for (int u = 0; u < kGR; ++u) {
-              const int t = threadIdx.x + u * NT;
-              if (t < ng)
-                sp[ghost_row(t)] = __fma_rn(beta, gpv[u], __dmul_rn(sinv[gc[u]], __fma_rn(-alpha, gq[u], gr[u])));
-            }
-            for (int t = threadIdx.x + kGR * NT; t < ng; t += NT) {
-              const int li = ghost_row(t);
-              const double q_ = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
-              const double r_ = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
-              const double p_ = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
-              sp[li] = __fma_rn(beta, p_, __dmul_rn(sinv[__ldg(&D.code[rb + li])], __fma_rn(-alpha, q_, r_)));
-            }
-          }
-          tm_st_wait();
-          fin = stop;
-        }
-        if (fin) {
-          // a4: restricted prolongation of the chunk's owned rows
-          __syncthreads();
-          const int its = sigma == 0.0 ? st[L].its : it;
-          if (its > 0) {
+            for (int b = 0; b < RPT / 4; ++b) {
+              double dd[4], rr[4];
+              if (it > 1) tm_ld4(tcol(L, 1, 4 * b), dd);
+              tm_ld4(tcol(L, 0, 4 * b), rr);
+              tm_ld_wait();
 #pragma unroll
-            for (int j = 0; j < RPT; ++j) {
-              const int i = j * NT + threadIdx.x;
-              const double dj = tm_ld(tcol(L, 1, j));
-              if (i < nr) {
-                const int32_t s = __ldg(&own_slot[rb + i]);
-                if (s >= 0) x[s] = x[s] + dj;
+              for (int u = 0; u < 4; ++u) {
+                const int j = 4 * b + u;
+                const int i = j * NC + ct;
+                if (it == 1) dd[u] = 0.0;
+                if (i < nr) {
+                  const double pi = sp[i];
+                  dd[u] = it == 1 ? alpha * pi : __fma_rn(alpha, pi, dd[u]);
+                  if (!stop) {
+                    const double rn = __fma_rn(-alpha, q[L][j], rr[u]);
+                    rr[u] = rn;
+                    const double pn = __fma_rn(beta, pi, __dmul_rn(spdi[sdc[i]], rn));
+                    sp[i] = pn;
+                    if (i < band.x || i >= band.y) {
+                      __stcg(&R2_PUB(pub_r, it & 1, rb)[i], rn);
+                      __stcg(&R2_PUB(pub_p, (it + 1) & 1, rb)[i], pn);
+                    }
+                  }
+                }
+              }
+              tm_st4(tcol(L, 1, 4 * b), dd);
+              tm_st4(tcol(L, 0, 4 * b), rr);
+            }
+            if (!stop) {
+#pragma unroll
+              for (int u = 0; u < kGR; ++u) {
+                const int t = ct + u * NC;
+                if (t < ng)
+                  sp[ghost_row(t)] = __fma_rn(beta, gpv[u], __dmul_rn(sinv[gc[u]], __fma_rn(-alpha, gq[u], gr[u])));
+              }
+              for (int t = ct + kGR * NC; t < ng; t += NC) {
+                const int li = ghost_row(t);
+                const double q_ = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
+                const double r_ = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
+                const double p_ = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
+                sp[li] = __fma_rn(beta, p_, __dmul_rn(sinv[__ldg(&D.code[rb + li])], __fma_rn(-alpha, q_, r_)));
               }
             }
+            tm_st_wait();
           }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            const int lp = st[L].lp;
-            if (c == 0) {
-              S.its[lp] = its;
-              S.inner_total[lp] += its;
+          if (phase != 1) {
+            // a4: restricted prolongation of the chunk's owned rows (d of the rows this thread owns)
+            if (it > 0) {
+#pragma unroll
+              for (int b = 0; b < RPT / 4; ++b) {
+                double dd[4];
+                tm_ld4(tcol(L, 1, 4 * b), dd);
+                tm_ld_wait();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int i = (4 * b + u) * NC + ct;
+                  if (i < nr) {
+                    const int32_t s = __ldg(&own_slot[rb + i]);
+                    if (s >= 0) x[s] = x[s] + dd[u];
+                  }
+                }
+              }
+            }
+            if (ct == 0 && c == 0) {
+              const int lp = st[L].lp;
+              S.its[lp] = it;
+              S.inner_total[lp] += it;
               S.active[lp] = 0;
             }
-            st[L].live = 0;
+            live[L] = false;
+            continue;
           }
-          __syncthreads();
-          continue;
+          nbar_sync(kBarCompute, NC);  // p_{it+1} (own rows + ghosts) complete before the gathers
+          pass_a(L, it + 1);
         }
-        __syncthreads();  // p_{it+1} (own rows + ghosts) complete before the gathers
-        pass_a(L, it + 1);
+        if (!any) break;
       }
-      if (!any) break;
     }
+    __syncthreads();  // both roles finished the pair (lane state and shared memory reused next)
   }
 #undef R2_PUB
   // ---- release TMEM ----

@@ -373,11 +373,11 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
   ResidLayout Lo;
   int k = 0, gs = 0, chunk = 0, lanes = 0;
   size_t smem = 0;
-  const size_t r2_static = 8 * (kResidNV * (kNT_R2 / 32) + kResidNV + 256) + sizeof(R2Lane) * 2 + 64;
+  const size_t r2_static = 8 * (2 * 3 * (kNC_R2 / 32) + 256) + sizeof(R2Lane) * 2 + 64;
   if (v2_ok) {
     for (int NL = 2; NL >= 1 && !lanes; --NL) {
       const int maxrpt = std::min(kR2ColBlk / 4 / NL, kR2MaxRPT);
-      if (!pick((nl + NL - 1) / NL, maxrpt * kNT_R2, &k, &gs)) continue;
+      if (!pick((nl + NL - 1) / NL, maxrpt * kNC_R2, &k, &gs)) continue;
       chunk = chunk_rows(nmax, gs);
       resident_layout(c, gs, true, Lo);
       if (!Lo.pat) break;  // not a row-pattern matrix: v1 below
@@ -406,7 +406,8 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
     if (smem + 2048 > (size_t)smem_optin) return RAS_OK;  // ghost zones too wide: TILED
   }
   const int nt = lanes ? kNT_R2 : kNT_RESID;
-  const int need = (chunk + nt - 1) / nt;
+  const int ntr = lanes ? kNC_R2 : kNT_RESID;  // threads that own rows
+  const int need = (chunk + ntr - 1) / ntr;
   int rpt;
   if (lanes) {
     rpt = need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : kR2MaxRPT;

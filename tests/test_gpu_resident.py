@@ -60,9 +60,9 @@ def test_resident_kernels_match_oracle(kernel, shape, monkeypatch):
         N, px, gamma, m, owner = 2048, 4, 8, 8, None
     elif shape == "big_chunks":  # one subdomain of 1300^2 rows on the whole GPU: one lane, > 7.7 K rows per CTA
         N, px, gamma, m, owner = 1300, 1, 0, 6, None
-    else:                    # 5 irregular subdomains: the last pair has one live lane
+    else:                    # 5 strips: the last pair has one live lane
         N, px, gamma, m = 600, 0, 3, 8
-        owner = ri.voronoi_partition(N, N, 5, seed=4)
+        owner = O.partition_regular(N, N, 1, 1, 5, 1)
     A = ri.laplace_2d(N)
     b = ri.rhs(A.n, 0)
     if owner is None:
