@@ -301,101 +301,131 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
 
     if (w == 0) {
       // ================= reduction warp =================
-      auto publish = [&](int L) {  // the compute warps' partials of lane L -> slot ring
+      // The compute warps run, per live lane L in turn: sync RES(L); pass B;
+      // pass A; arrive PART(L) -- and then immediately need RES(next lane).  So
+      // on PART(L) this warp first releases RES(next) (polled while the compute
+      // warps were busy with L), then publishes L's partials, then polls the next
+      // result it will need: the compute warps never wait for a fence or a poll.
+      double part[3];
+      auto take_part = [&](int L) {  // the compute warps' partials of lane L
         nbar_sync(bar_part(L), NT);
-        double s3[3];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) s3[j] = warp_sum(lane < NCW ? red[L][j][lane] : 0.0);
+        for (int j2 = 0; j2 < 3; ++j2) part[j2] = warp_sum(lane < NCW ? red[L][j2][lane] : 0.0);
+      };
+      auto publish = [&](int L) {  // part -> this CTA's slot of the lane's current reduction
         unsigned long long* slots = lane_slots(L);
         const unsigned seq = st[L].seq;
         unsigned long long* const ring = slots + (size_t)(seq % 3) * gs * 4;
         unsigned long long* const nxt = slots + (size_t)((seq + 1) % 3) * gs * 4;
         if (lane == 0) {
 #pragma unroll
-          for (int j = 0; j < 3; ++j) st_relaxed_gpu_u64(&nxt[c * 4 + j], kSlotEmpty);
+          for (int j2 = 0; j2 < 3; ++j2) st_relaxed_gpu_u64(&nxt[c * 4 + j2], kSlotEmpty);
           // release: the compute warps' export-band stores (ordered before this
           // thread by the named barrier) before the partial sums
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            unsigned long long u = (unsigned long long)__double_as_longlong(s3[j]);
+          for (int j2 = 0; j2 < 3; ++j2) {
+            unsigned long long u = (unsigned long long)__double_as_longlong(part[j2]);
             if (u == kSlotEmpty) u = 0x7ff8000000000000ull;
-            st_relaxed_gpu_u64(&ring[c * 4 + j], u);
+            st_relaxed_gpu_u64(&ring[c * 4 + j2], u);
           }
         }
         __syncwarp();
       };
+      bool polled[NL];
+      auto poll = [&](int L) {  // every CTA's slot of the lane's reduction -> PCG scalars in st[L]
+        double v[3];
+        const unsigned long long* const ring = lane_slots(L) + (size_t)(st[L].seq % 3) * gs * 4;
+        constexpr int KS = (kMaxGroupCTAs + 31) / 32;
+        unsigned long long u[KS][3];
 #pragma unroll
-      for (int L = 0; L < NL; ++L)
-        if (live[L]) publish(L);
-      for (;;) {
-        bool any = false;
+        for (int t = 0; t < KS; ++t)
 #pragma unroll
-        for (int L = 0; L < NL; ++L) {
-          if (!live[L]) continue;
-          any = true;
-          double v[3];
-          // poll every CTA's slot of this lane's reduction, fixed-order sum (group_wait)
-          {
-            const unsigned long long* const ring = lane_slots(L) + (size_t)(st[L].seq % 3) * gs * 4;
-            constexpr int KS = (kMaxGroupCTAs + 31) / 32;
-            unsigned long long u[KS][3];
+          for (int j2 = 0; j2 < 3; ++j2) u[t][j2] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
+        for (;;) {
+          bool done = true;
 #pragma unroll
-            for (int t = 0; t < KS; ++t)
+          for (int t = 0; t < KS; ++t)
 #pragma unroll
-              for (int j = 0; j < 3; ++j) u[t][j] = lane + 32 * t < gs ? kSlotEmpty : 0ull;
-            for (;;) {
-              bool done = true;
+            for (int j2 = 0; j2 < 3; ++j2)
+              if (u[t][j2] == kSlotEmpty) u[t][j2] = ld_relaxed_gpu_u64(&ring[(lane + 32 * t) * 4 + j2]);
 #pragma unroll
-              for (int t = 0; t < KS; ++t)
+          for (int t = 0; t < KS; ++t)
 #pragma unroll
-                for (int j = 0; j < 3; ++j)
-                  if (u[t][j] == kSlotEmpty) u[t][j] = ld_relaxed_gpu_u64(&ring[(lane + 32 * t) * 4 + j]);
+            for (int j2 = 0; j2 < 3; ++j2) done = done && u[t][j2] != kSlotEmpty;
+          if (__all_sync(0xffffffffu, done)) break;
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the peers' export-band stores
 #pragma unroll
-              for (int t = 0; t < KS; ++t)
+        for (int j2 = 0; j2 < 3; ++j2) {
+          double acc = 0.0;
 #pragma unroll
-                for (int j = 0; j < 3; ++j) done = done && u[t][j] != kSlotEmpty;
-              if (__all_sync(0xffffffffu, done)) break;
-            }
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the peers' export-band stores
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              double acc = 0.0;
-#pragma unroll
-              for (int t = 0; t < KS; ++t) acc += __longlong_as_double((long long)u[t][j]);
-              v[j] = warp_allsum(acc);
-            }
-          }
-          // PCG scalars of iteration it (R28; R7 breakdowns)
-          const int it = st[L].its + 1;
-          const double sigma = v[0];
-          if (lane == 0) {
-            if (sigma == 0.0) {
-              st[L].seq = st[L].seq + 1;
-              st[L].live = 2;  // breakdown: prolong d as it stands
-            } else {
-              const double rho = st[L].rho;
-              const double alpha = rho / sigma;
-              const double rho_new = rho - 2.0 * alpha * v[1] + alpha * alpha * v[2];
-              const bool stop = it >= m || !(rho_new > 0.0);
-              st[L].alpha = alpha;
-              st[L].beta = rho_new / rho;
-              st[L].rho = rho_new;
-              st[L].its = it;
-              st[L].seq = st[L].seq + 1;
-              st[L].live = stop ? 3 : 1;  // 3: last pass B, then prolong
-            }
-          }
-          __syncwarp();
-          const int phase = st[L].live;
-          nbar_arrive(bar_res(L), NT);
-          if (phase == 1) {
-            publish(L);
+          for (int t = 0; t < KS; ++t) acc += __longlong_as_double((long long)u[t][j2]);
+          v[j2] = warp_allsum(acc);
+        }
+        // PCG scalars of iteration it (R28; R7 breakdowns)
+        const int it = st[L].its + 1;
+        const double sigma = v[0];
+        if (lane == 0) {
+          if (sigma == 0.0) {
+            st[L].seq = st[L].seq + 1;
+            st[L].live = 2;  // breakdown: prolong d as it stands
           } else {
-            live[L] = false;
+            const double rho = st[L].rho;
+            const double alpha = rho / sigma;
+            const double rho_new = rho - 2.0 * alpha * v[1] + alpha * alpha * v[2];
+            const bool stop = it >= m || !(rho_new > 0.0);
+            st[L].alpha = alpha;
+            st[L].beta = rho_new / rho;
+            st[L].rho = rho_new;
+            st[L].its = it;
+            st[L].seq = st[L].seq + 1;
+            st[L].live = stop ? 3 : 1;  // 3: last pass B, then prolong
           }
         }
-        if (!any) break;
+        __syncwarp();
+        polled[L] = true;
+      };
+      auto next_live = [&](int from) {  // first live lane after `from`, cyclic (from itself last)
+        int r = -1;
+#pragma unroll
+        for (int k2 = NL; k2 >= 1; --k2) {
+          const int L2 = (from + k2) % NL;
+          if (live[L2]) r = L2;
+        }
+        return r;
+      };
+#pragma unroll
+      for (int L = 0; L < NL; ++L) {
+        polled[L] = false;
+        if (live[L]) {
+          take_part(L);
+          publish(L);
+        }
+      }
+      int R = next_live(NL - 1);
+      bool delivered = false;
+      while (R >= 0) {
+        if (!delivered) {
+          if (!polled[R]) poll(R);
+          nbar_arrive(bar_res(R), NT);
+        }
+        delivered = false;
+        polled[R] = false;
+        if (st[R].live != 1) {  // the lane's last pass: no more partials from it
+          live[R] = false;
+          R = next_live(R);
+          continue;
+        }
+        const int Rn = next_live(R);  // the result the compute warps need after PART(R)
+        if (Rn != R && !polled[Rn]) poll(Rn);  // while they run R's passes
+        take_part(R);
+        if (Rn != R) {
+          nbar_arrive(bar_res(Rn), NT);
+          delivered = true;
+        }
+        publish(R);
+        R = Rn;
       }
     } else {
       // ================= compute warps =================
@@ -410,12 +440,11 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
         const double* spdg = lane_pdg(L);
         const double* spdi = lane_pdi(L);
         double v[3] = {0.0, 0.0, 0.0};
-        double rr[2][4];
-        tm_ld4(tcol(L, 0, 0), rr[0]);
-        tm_ld_wait();
 #pragma unroll
         for (int b = 0; b < RPT / 4; ++b) {
-          if (b + 1 < RPT / 4) tm_ld4(tcol(L, 0, 4 * (b + 1)), rr[(b + 1) & 1]);  // in flight during rows of b
+          double rr4[4];
+          tm_ld4(tcol(L, 0, 4 * b), rr4);
+          tm_ld_wait();
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * b + u;
@@ -429,7 +458,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
               const double qi = __fma_rn(spdg[pt], pi, off);
               q[L][j] = qi;
               const double di = spdi[pt];
-              const double zi = __dmul_rn(di, rr[b & 1][u]);
+              const double zi = __dmul_rn(di, rr4[u]);
               const double dq = __dmul_rn(di, qi);
               v[0] += pi * qi;
               v[1] += zi * qi;
@@ -437,7 +466,6 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
               if (i < band.x || i >= band.y) __stcg(&R2_PUB(pub_q, it & 1, rb)[i], qi);
             }
           }
-          tm_ld_wait();
         }
         // this warp's partials -> shared memory, then hand them to the reduction warp
 #pragma unroll
