@@ -384,6 +384,40 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
           }
         }
         __syncwarp();
+        // NL = 2: the ghost zones of p_{it+1} (R29) are staged here, off the compute
+        // warps' path (they run the other lane's passes meanwhile); the published
+        // q_it, r_{it-1}, p_it of the neighbours are visible after the acquire above
+        if (NL == 2 && st[L].live == 1) {
+          const int rb = st[L].rb, nr = st[L].nr;
+          const int4 band = st[L].band;
+          const int ng = band.z + band.w;
+          const double alpha = st[L].alpha, beta = st[L].beta;
+          double* sp = lane_sp(L);
+          constexpr int GB = 4;  // ghost rows per lane in flight
+          for (int t0 = 0; t0 < ng; t0 += 32 * GB) {
+            double gq[GB], gr[GB], gp[GB];
+            uint32_t gc[GB];
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+              const int t = t0 + u * 32 + lane;
+              if (t < ng) {
+                const int li = t < band.z ? t - band.z : nr + (t - band.z);
+                gq[u] = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
+                gr[u] = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
+                gp[u] = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
+                gc[u] = __ldg(&D.code[rb + li]);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+              const int t = t0 + u * 32 + lane;
+              if (t < ng) {
+                const int li = t < band.z ? t - band.z : nr + (t - band.z);
+                sp[li] = __fma_rn(beta, gp[u], __dmul_rn(sinv[gc[u]], __fma_rn(-alpha, gq[u], gr[u])));
+              }
+            }
+          }
+        }
         polled[L] = true;
       };
       auto next_live = [&](int from) {  // first live lane after `from`, cyclic (from itself last)
@@ -501,7 +535,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
             double gq[kGR], gr[kGR], gpv[kGR];
             uint32_t gc[kGR];
             auto ghost_row = [&](int t) { return t < band.z ? t - band.z : nr + (t - band.z); };
-            if (!stop) {
+            if (NL == 1 && !stop) {
 #pragma unroll
               for (int u = 0; u < kGR; ++u) {
                 const int t = ct + u * NC;
@@ -544,7 +578,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
               tm_st4(tcol(L, 1, 4 * b), dd);
               tm_st4(tcol(L, 0, 4 * b), rr);
             }
-            if (!stop) {
+            if (NL == 1 && !stop) {
 #pragma unroll
               for (int u = 0; u < kGR; ++u) {
                 const int t = ct + u * NC;
