@@ -174,6 +174,12 @@ __device__ __forceinline__ void tm_st4(uint32_t taddr, const double (&v)[4]) {
                : "memory");
 }
 __device__ __forceinline__ void tm_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Warp-specialised CTA: warp 0 is the REDUCTION warp (sums the compute warps'
 // partials, publishes them to the group's slot ring, polls it, computes alpha /
@@ -206,6 +212,8 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
   auto lane_pdg = [&](int L) { return lane_pv(L) + kMaxPat * W; };
   auto lane_pdi = [&](int L) { return lane_pdg(L) + kMaxPat; };
   auto lane_pdl = [&](int L) { return reinterpret_cast<int32_t*>(lane_pdi(L) + kMaxPat); };  // [kMaxPat][W]
+  const int gmax = glo_max + ghi_max;
+  double* const sstage = smem + (size_t)NL * lane_words;  // ghost staging: q [gmax] | r [gmax]
 
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ct = threadIdx.x - 32;  // compute thread index (< 0 in the reduction warp)
@@ -384,40 +392,6 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
           }
         }
         __syncwarp();
-        // NL = 2: the ghost zones of p_{it+1} (R29) are staged here, off the compute
-        // warps' path (they run the other lane's passes meanwhile); the published
-        // q_it, r_{it-1}, p_it of the neighbours are visible after the acquire above
-        if (NL == 2 && st[L].live == 1) {
-          const int rb = st[L].rb, nr = st[L].nr;
-          const int4 band = st[L].band;
-          const int ng = band.z + band.w;
-          const double alpha = st[L].alpha, beta = st[L].beta;
-          double* sp = lane_sp(L);
-          constexpr int GB = 4;  // ghost rows per lane in flight
-          for (int t0 = 0; t0 < ng; t0 += 32 * GB) {
-            double gq[GB], gr[GB], gp[GB];
-            uint32_t gc[GB];
-#pragma unroll
-            for (int u = 0; u < GB; ++u) {
-              const int t = t0 + u * 32 + lane;
-              if (t < ng) {
-                const int li = t < band.z ? t - band.z : nr + (t - band.z);
-                gq[u] = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
-                gr[u] = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
-                gp[u] = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
-                gc[u] = __ldg(&D.code[rb + li]);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < GB; ++u) {
-              const int t = t0 + u * 32 + lane;
-              if (t < ng) {
-                const int li = t < band.z ? t - band.z : nr + (t - band.z);
-                sp[li] = __fma_rn(beta, gp[u], __dmul_rn(sinv[gc[u]], __fma_rn(-alpha, gq[u], gr[u])));
-              }
-            }
-          }
-        }
         polled[L] = true;
       };
       auto next_live = [&](int from) {  // first live lane after `from`, cyclic (from itself last)
@@ -529,24 +503,20 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
           const double* spdi = lane_pdi(L);
           if (phase != 2) {
             const bool stop = phase == 3;
-            // ghost rows of p_{it+1} (R29): loads issued before pass B
-            constexpr int kGR = 2;
+            // ghost rows of p_{it+1} (R29): the neighbours' published q_it and r_{it-1}
+            // are copied into the staging buffer asynchronously (cp.async, no
+            // registers) while pass B runs; p_it of a ghost row is already in sp
+            // (bitwise the owner's value).  The L1 lines of the published arrays were
+            // invalidated by the reduction warp's acquire fence (CCTL.IVALL).
             const int ng = band.z + band.w;
-            double gq[kGR], gr[kGR], gpv[kGR];
-            uint32_t gc[kGR];
             auto ghost_row = [&](int t) { return t < band.z ? t - band.z : nr + (t - band.z); };
-            if (NL == 1 && !stop) {
-#pragma unroll
-              for (int u = 0; u < kGR; ++u) {
-                const int t = ct + u * NC;
-                if (t < ng) {
-                  const int li = ghost_row(t);
-                  gq[u] = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
-                  gr[u] = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
-                  gpv[u] = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
-                  gc[u] = __ldg(&D.code[rb + li]);
-                }
+            if (!stop) {
+              for (int t = ct; t < ng; t += NC) {
+                const int li = ghost_row(t);
+                cp_async8(&sstage[t], &R2_PUB(pub_q, it & 1, rb)[li]);
+                cp_async8(&sstage[gmax + t], &R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
               }
+              cp_async_commit();
             }
             // pass B: d += alpha p, r -= alpha q, p_{it+1} = D^-1 r + beta p (own rows)
 #pragma unroll
@@ -578,19 +548,12 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
               tm_st4(tcol(L, 1, 4 * b), dd);
               tm_st4(tcol(L, 0, 4 * b), rr);
             }
-            if (NL == 1 && !stop) {
-#pragma unroll
-              for (int u = 0; u < kGR; ++u) {
-                const int t = ct + u * NC;
-                if (t < ng)
-                  sp[ghost_row(t)] = __fma_rn(beta, gpv[u], __dmul_rn(sinv[gc[u]], __fma_rn(-alpha, gq[u], gr[u])));
-              }
-              for (int t = ct + kGR * NC; t < ng; t += NC) {
+            if (!stop) {
+              cp_async_wait_all();  // this thread's own copies
+              for (int t = ct; t < ng; t += NC) {
                 const int li = ghost_row(t);
-                const double q_ = __ldcg(&R2_PUB(pub_q, it & 1, rb)[li]);
-                const double r_ = __ldcg(&R2_PUB(pub_r, (it - 1) & 1, rb)[li]);
-                const double p_ = __ldcg(&R2_PUB(pub_p, it & 1, rb)[li]);
-                sp[li] = __fma_rn(beta, p_, __dmul_rn(sinv[__ldg(&D.code[rb + li])], __fma_rn(-alpha, q_, r_)));
+                sp[li] = __fma_rn(beta, sp[li],
+                                  __dmul_rn(sinv[__ldg(&D.code[rb + li])], __fma_rn(-alpha, sstage[t], sstage[gmax + t])));
               }
             }
             tm_st_wait();

@@ -381,10 +381,12 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
       chunk = chunk_rows(nmax, gs);
       resident_layout(c, gs, true, Lo);
       if (!Lo.pat) break;  // not a row-pattern matrix: v1 below
-      const size_t need = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL) + r2_static;
-      if (need + 1024 <= (size_t)smem_optin) {
+      // NL lanes + the ghost staging buffer (q, r of the widest ghost zones)
+      const size_t dyn = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL) +
+                         (size_t)16 * (Lo.glo_max + Lo.ghi_max);
+      if (dyn + r2_static + 1024 <= (size_t)smem_optin) {
         lanes = NL;
-        smem = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL);
+        smem = dyn;
       }
     }
   }
