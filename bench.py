@@ -153,6 +153,15 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_onchip(kernel):
+    """On-chip counters of `kernel` from the committed ncu summary (profiles/ncu_onchip.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_onchip.json")) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def ncu_traffic(kernel):
     """dram bytes per launch of `kernel` from the committed ncu summary, or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -433,7 +442,7 @@ def main():
             continue
         avg_ms = kms / cnt
         rec = {"launches": cnt, "avg_us": avg_ms * 1e3, "share": kms / tot_ms if tot_ms else None}
-        if name in ("k_resident_pcg", "k_small_pcg"):
+        if name in ("k_resident_pcg", "k_resident2", "k_small_pcg"):
             rec["compulsory_bytes"] = bpl
             bpl = per_it * M_INNER + ktimes["k_prolong"][2]
         rec["bytes_per_launch"] = bpl
@@ -442,15 +451,38 @@ def main():
     dom = max((k for k in kern if kern[k]["bytes_per_launch"]), key=lambda k: kern[k]["share"] or 0)
     peak, peak_src = measured_peaks()
     tr = ncu_traffic(dom)
-    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
-            "frac": kern[dom]["gbs"] / peak, "traffic": tr, "peak_source": peak_src,
-            "bytes_per_launch": kern[dom]["bytes_per_launch"],
-            "bytes_model": "DESIGN.md §5: compulsory bytes of real rows/entries of the streamed (tiled) iteration, "
-                           "SELL-Z / int32 SELL indices, FP64 values"}
-    if "compulsory_bytes" in kern[dom]:
-        roof["note"] = ("on-chip resident local solve: achieved = bytes the tiled path streams for the same "
-                        f"{M_INNER} iterations / launch time; the launch's own HBM traffic is the compulsory "
-                        f"{kern[dom]['compulsory_bytes'] / 1e9:.2f} GB (traffic), frac > 1 = beyond the streaming roofline")
+    if dom in ("k_resident2", "k_resident_pcg"):
+        # the whole local solve runs on chip: its HBM traffic is only the compulsory
+        # once-per-sweep part, so the bound is ON-CHIP.  Model ("RESIDENT
+        # roofline"): algorithmic shared-memory bytes of one PCG iteration of the
+        # row-pattern SpMV + update = 5 p reads (40 B) + pattern id (1 B) + p read and
+        # write in the update (16 B) = 57 B per Omega-row, x m iterations x rows, against
+        # the shared-memory bandwidth 148 SMs x 128 B/clk x 1.965 GHz = 37.2 TB/s (B200
+        # unit counts and max clock, B200_PROFILING.md / B300_MICROARCH.md)
+        rows = float(stats["rows_local"])
+        smem_bytes = 57.0 * rows * M_INNER
+        smem_peak = 148 * 128 * 1.965  # GB/s
+        avg_s = kern[dom]["avg_us"] * 1e-6
+        roof = {"bound": "smem", "kernel": dom, "achieved": smem_bytes / avg_s / 1e9, "peak": smem_peak,
+                "unit": "GB/s", "frac": smem_bytes / avg_s / 1e9 / smem_peak, "traffic": tr,
+                "peak_source": "derived: 148 SMs x 128 B/clk shared memory x 1.965 GHz (B200 unit counts, max SM clock)",
+                "bytes_per_launch": smem_bytes,
+                "bytes_model": "on-chip: 57 B of shared memory per Omega-row per PCG iteration (5 p gathers, pattern id, "
+                               "p update), x m x rows; r, d live in tensor memory (k_resident2)",
+                "hbm": {"compulsory_bytes": kern[dom].get("compulsory_bytes"),
+                        "gbs": (kern[dom].get("compulsory_bytes") or 0) / avg_s / 1e9,
+                        "frac": (kern[dom].get("compulsory_bytes") or 0) / avg_s / 1e9 / peak,
+                        "streamed_model_gbs": kern[dom]["gbs"],
+                        "note": "HBM is not this kernel's bound: its DRAM traffic is the compulsory once-per-sweep "
+                                "bytes; streamed_model_gbs = the bytes the tiled path would stream for the same "
+                                "iterations / launch time (context only)"},
+                "ncu": ncu_onchip(dom)}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": kern[dom]["gbs"] / peak, "traffic": tr, "peak_source": peak_src,
+                "bytes_per_launch": kern[dom]["bytes_per_launch"],
+                "bytes_model": "DESIGN.md §5: compulsory bytes of real rows/entries of the streamed (tiled) iteration, "
+                               "SELL-Z / int32 SELL indices, FP64 values"}
     pcg_bytes = sum(kern[k]["bytes_per_launch"] * kern[k]["launches"] for k in kern if kern[k]["bytes_per_launch"])
     pcg_ms = sum(ktimes[k][1] for k in kern if kern[k]["bytes_per_launch"])
     # e2e through ras_solve with pinned host buffers

@@ -1610,7 +1610,8 @@ ras_status ras_kernel_times(const ras_ctx* c, ras_kernel_time_t* out, int32_t ma
   if (!c || !n_out) return RAS_EINVAL;
   const char* names[K_NKINDS] = {"k_residual", "k_spmv_dot", c->ic ? "k_update_dot<ic>" : "k_update_dot",
                                  c->ic ? "k_pupdate_z" : "k_pupdate", "k_prolong", "k_pack", "control",
-                                 "k_trsv", "k_zdot", "k_small_pcg", "k_resident_pcg", "k_band_chol"};
+                                 "k_trsv", "k_zdot", "k_small_pcg", c->resid_lanes ? "k_resident2" : "k_resident_pcg",
+                                 "k_band_chol"};
   const double bytes[K_NKINDS] = {c->mb.residual, c->mb.spmv_dot, c->mb.update_dot, c->mb.pupdate,
                                   c->mb.prolong,  c->mb.pack,     0.0,              c->mb.trsv,
                                   c->mb.zdot,     c->mb.local_solve, c->mb.local_solve, c->mb.band};
