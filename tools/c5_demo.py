@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--modes", default="sync,async:central,async:decentral")
     ap.add_argument("--robin", type=float, default=0.0)
+    ap.add_argument("--tol", type=float, default=1e-8)
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -72,7 +73,7 @@ def main():
         t_setup = time.perf_counter() - t1
         if world > 1:
             dist.barrier()
-        st, _ = s.solve(1e-8, a.iters, mode, gather=False)
+        st, _ = s.solve(a.tol, a.iters, mode, gather=False)
         d = s.stats()
         t = torch.tensor([d["time_to_solution_s"]], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -80,6 +81,9 @@ def main():
         res.append({"mode": mode, "detector": det if mode == "async" else None, "status": int(st), "robin": a.robin,
                     "time_s": float(t[0]), "sweeps_or_max_updates": d["sweeps"], "updates_min": d["updates_min"],
                     "rel_residual": d["final_rel_residual"], "pcg_path": d["pcg_path"], "setup_s": t_setup,
+                    "resident_lanes": d["resident_lanes"], "resident_pattern": d["resident_pattern"],
+                    "verified": d["verified"], "phase_s": {k: d[k] for k in ("t_residual", "t_local_solve",
+                                                                            "t_exchange", "t_convcheck")},
                     "resumes": d["resumes"], "per_sweep_ms": 1e3 * float(t[0]) / max(d["sweeps"], 1)})
         s.close()
     if rank == 0:
