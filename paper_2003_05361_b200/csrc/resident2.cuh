@@ -129,8 +129,17 @@ __device__ __forceinline__ void group_wait(double (&v)[NV], double* bc, const un
 
 // Shared-memory words (doubles) of one lane: p with ghost zones, pattern ids,
 // pattern table (values [kMaxPat][W], diagonal, its reciprocal, int32 deltas [kMaxPat][W]).
-__host__ __device__ constexpr int r2_lane_words(int glo, int chunk, int ghi, int W) {
-  return (glo + chunk + ghi) + ((chunk + 7) & ~7) / 8 + kMaxPat * (W + 2) + (kMaxPat * W + 1) / 2;
+// PAT: + the pattern table; !PAT: + the chunk's SELL-Z slice bases (int32 [slices][W]).
+__host__ __device__ constexpr int r2_lane_words(int glo, int chunk, int ghi, int W, bool pat) {
+  return (glo + chunk + ghi) + ((chunk + 7) & ~7) / 8 +
+         (pat ? kMaxPat * (W + 2) + (kMaxPat * W + 1) / 2 : ((chunk + 31) / 32 * W + 1) / 2);
+}
+
+// Off-diagonal sum of a SELL-Z row whose slice has a wide group (int32 columns):
+// the generic decoder, out of line so its registers do not burden the hot loop.
+template <int W>
+__device__ __noinline__ double r2_wide_row(const Sell& L, int64_t row, const double* tab, const double* p_rowspace) {
+  return resident_row<W, true>(L, row, tab, [&](int32_t col) { return p_rowspace[col]; });
 }
 
 // Per-lane state kept in shared memory (registers are for the rows' q).
@@ -188,9 +197,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // never wait for the release fence or the poll of a reduction they do not need yet.
 constexpr int kNC_R2 = kNT_R2 - 32;  // compute threads
 
-template <int RPT, int W, int NL>
+// PAT: row-pattern dictionary SpMV (stencil matrices: <= kMaxPat distinct rows per
+// chunk, no matrix stream); !PAT: the SELL-Z local matrix streamed from L2 every
+// iteration (codes / column offsets / slice bases; irregular subdomains such as
+// Voronoi cells, whose chunks hold hundreds of distinct rows), one batch of four
+// rows' entries in flight while the previous batch is computed.
+template <int RPT, int W, int NL, bool PAT>
 static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int nsub, SmallSubs SS, ResidentCtl RC,
-                                                                   Diag D, const int32_t* __restrict__ own_slot,
+                                                                   Sell Lm, Diag D, const int32_t* __restrict__ own_slot,
                                                                    double* __restrict__ x, Scal S, Ctl C, int32_t m,
                                                                    int32_t chunk_max, int32_t glo_max, int32_t ghi_max,
                                                                    int32_t ntable) {
@@ -200,18 +214,20 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
   extern __shared__ double smem[];
   __shared__ double red[NL][3][NCW];  // compute warps' partials per lane
   __shared__ double sinv[256];         // __drcp_rn of every dictionary value (ghost rows' D^-1)
+  __shared__ double stab[256];         // !PAT: the dictionary values (matrix entries and diagonal)
   __shared__ R2Lane st[NL];
   __shared__ uint32_t s_tbase;
   // per-lane shared memory: p (+ ghost zones) | pattern ids | pattern table
   const int pstride = glo_max + chunk_max + ghi_max;
   const int idbytes = (chunk_max + 7) & ~7;
-  const int lane_words = r2_lane_words(glo_max, chunk_max, ghi_max, W);
+  const int lane_words = r2_lane_words(glo_max, chunk_max, ghi_max, W, PAT);
   auto lane_sp = [&](int L) { return smem + (size_t)L * lane_words + glo_max; };
   auto lane_id = [&](int L) { return reinterpret_cast<uint8_t*>(smem + (size_t)L * lane_words + pstride); };
   auto lane_pv = [&](int L) { return smem + (size_t)L * lane_words + pstride + idbytes / 8; };  // [kMaxPat][W]
   auto lane_pdg = [&](int L) { return lane_pv(L) + kMaxPat * W; };
   auto lane_pdi = [&](int L) { return lane_pdg(L) + kMaxPat; };
   auto lane_pdl = [&](int L) { return reinterpret_cast<int32_t*>(lane_pdi(L) + kMaxPat); };  // [kMaxPat][W]
+  auto lane_kb = [&](int L) { return reinterpret_cast<int32_t*>(lane_pv(L)); };  // !PAT: [slices][W] slice bases
   const int gmax = glo_max + ghi_max;
   double* const sstage = smem + (size_t)NL * lane_words;  // ghost staging: q [gmax] | r [gmax]
 
@@ -223,7 +239,11 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
                      (uint32_t)__cvta_generic_to_shared(&s_tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = threadIdx.x; i < ntable; i += NT) sinv[i] = __drcp_rn(__ldg(&D.table[i]));
+  for (int i = threadIdx.x; i < ntable; i += NT) {
+    const double v = __ldg(&D.table[i]);
+    stab[i] = v;
+    sinv[i] = __drcp_rn(v);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -277,7 +297,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
       }
       for (int i = threadIdx.x; i < nr; i += NT) {
         sp[i] = __ldcg(&R2_PUB(pub_p, 1, rb)[i]);  // p_1 = z_0
-        sdc[i] = __ldg(&RC.pid[rb + i]);
+        sdc[i] = PAT ? __ldg(&RC.pid[rb + i]) : __ldg(&D.code[rb + i]);  // pattern id | diagonal code
       }
       if (ct >= 0) {
 #pragma unroll
@@ -291,7 +311,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
           tm_st4(tcol(L, 0, 4 * b), rr);
         }
       }
-      const int p0 = RC.pat_off[lp * gs + c], np = RC.pat_cnt[lp * gs + c];
+      const int p0 = PAT ? RC.pat_off[lp * gs + c] : 0, np = PAT ? RC.pat_cnt[lp * gs + c] : 0;
       double* spv = lane_pv(L);
       int32_t* spdl = lane_pdl(L);
       for (int t = threadIdx.x; t < np * W; t += NT) {
@@ -302,6 +322,10 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
         const double dg = __ldg(&RC.pat_diag[p0 + t]);
         lane_pdg(L)[t] = dg;
         lane_pdi(L)[t] = __drcp_rn(dg);
+      }
+      if (!PAT) {
+        int32_t* skb = lane_kb(L);
+        for (int t = threadIdx.x; t < (nr + 31) / 32 * W; t += NT) skb[t] = __ldg(&Lm.kbase[(size_t)(rb >> 5) * W + t]);
       }
     }
     tm_st_wait();
@@ -448,8 +472,34 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
         const double* spdg = lane_pdg(L);
         const double* spdi = lane_pdi(L);
         double v[3] = {0.0, 0.0, 0.0};
+        // !PAT: SELL-Z entries of four rows (codes, 16-bit column offsets, slice bases)
+        constexpr int W4 = W / 4 > 0 ? W / 4 : 1, W2 = W / 2 > 0 ? W / 2 : 1;
+        uint32_t zc[4][W4], zd[4][W2];
+        const int32_t* skb = lane_kb(L);
+        auto zload = [&](int b) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = (4 * b + u) * NC + ct;
+            if (i < nr) {
+              const int64_t row = (int64_t)rb + i;
+              if (W == 4) {
+                zc[u][0] = __ldg(reinterpret_cast<const unsigned int*>(Lm.code) + row);
+                const uint2 dd = __ldg(reinterpret_cast<const uint2*>(Lm.d16) + row);
+                zd[u][0] = dd.x;
+                zd[u][W2 - 1] = dd.y;
+              } else {
+                const uint2 cc = __ldg(reinterpret_cast<const uint2*>(Lm.code) + row);
+                zc[u][0] = cc.x;
+                zc[u][W4 - 1] = cc.y;
+                const uint4 dd = __ldg(reinterpret_cast<const uint4*>(Lm.d16) + row);
+                zd[u][0] = dd.x, zd[u][1] = dd.y, zd[u][2] = dd.z, zd[u][W2 - 1] = dd.w;
+              }
+            }
+          }
+        };
 #pragma unroll
         for (int b = 0; b < RPT / 4; ++b) {
+          if (!PAT) zload(b);  // this batch's entries (in flight with the TMEM load)
           double rr4[4];
           tm_ld4(tcol(L, 0, 4 * b), rr4);
           tm_ld_wait();
@@ -460,12 +510,32 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
             if (i < nr) {
               const double pi = sp[i];
               const int pt = sdc[i];
-              double off = 0.0;
+              double off = 0.0, dg, di;
+              if (PAT) {
 #pragma unroll
-              for (int k = 0; k < W; ++k) off += spv[pt * W + k] * sp[i + spdl[pt * W + k]];
-              const double qi = __fma_rn(spdg[pt], pi, off);
+                for (int k = 0; k < W; ++k) off += spv[pt * W + k] * sp[i + spdl[pt * W + k]];
+                dg = spdg[pt];
+                di = spdi[pt];
+              } else {
+                const int32_t* kb = skb + (i >> 5) * W;  // this row's slice bases (shared memory)
+                bool wide = false;
+#pragma unroll
+                for (int k = 0; k < W; ++k) wide = wide || kb[k] < 0;
+                if (!wide) {
+#pragma unroll
+                  for (int k = 0; k < W; ++k) {
+                    const uint32_t code = (zc[u][k / 4] >> (8 * (k % 4))) & 0xffu;
+                    const int li = kb[k] - rb + (int)((zd[u][k / 2] >> (16 * (k % 2))) & 0xffffu);
+                    off += stab[code] * sp[li];
+                  }
+                } else {  // a slice with a wide group (int32 columns): generic decoder
+                  off = r2_wide_row<W>(Lm, (int64_t)rb + i, stab, sp - rb);
+                }
+                dg = stab[pt];
+                di = sinv[pt];
+              }
+              const double qi = __fma_rn(dg, pi, off);
               q[L][j] = qi;
-              const double di = spdi[pt];
               const double zi = __dmul_rn(di, rr4[u]);
               const double dq = __dmul_rn(di, qi);
               v[0] += pi * qi;
@@ -536,7 +606,7 @@ static __global__ void __launch_bounds__(kNT_R2, 1) k_resident2(int lp_base, int
                   if (!stop) {
                     const double rn = __fma_rn(-alpha, q[L][j], rr[u]);
                     rr[u] = rn;
-                    const double pn = __fma_rn(beta, pi, __dmul_rn(spdi[sdc[i]], rn));
+                    const double pn = __fma_rn(beta, pi, __dmul_rn(PAT ? spdi[sdc[i]] : sinv[sdc[i]], rn));
                     sp[i] = pn;
                     if (i < band.x || i >= band.y) {
                       __stcg(&R2_PUB(pub_r, it & 1, rb)[i], rn);

@@ -207,23 +207,28 @@ static const void* resident_kernel(int rpt, bool z, int w, bool tol, bool pat) {
 #undef RAS_RK
 }
 
-// k_resident2 instantiations: rows per thread x SELL-Z width (4 / 8) x lanes
-static const void* resident2_kernel(int rpt, int w, int lanes) {
-#define RAS_R2(RPT)                                                                                   \
-  if (lanes == 2) return w == 4 ? (const void*)k_resident2<RPT, 4, 2> : (const void*)k_resident2<RPT, 8, 2>; \
-  return w == 4 ? (const void*)k_resident2<RPT, 4, 1> : (const void*)k_resident2<RPT, 8, 1>;
-  if (rpt <= 4) {
-    RAS_R2(4)
-  } else if (rpt <= 8) {
-    RAS_R2(8)
-  } else if (rpt <= 12) {
-    RAS_R2(12)
-  } else if (rpt <= 16) {
-    RAS_R2(16)
+// k_resident2 instantiations: rows per thread x SELL-Z width (4 / 8) x lanes x row-pattern SpMV
+template <int RPT, int NL, bool PAT>
+static const void* r2_fn(int w) {
+  return w == 4 ? (const void*)k_resident2<RPT, 4, NL, PAT> : (const void*)k_resident2<RPT, 8, NL, PAT>;
+}
+template <int RPT, bool PAT>
+static const void* r2_fn_l(int w, int lanes) {
+  if constexpr (RPT <= 16) {
+    if (lanes == 2) return r2_fn<RPT, 2, PAT>(w);
   }
-  if (lanes == 2) return nullptr;
-  return w == 4 ? (const void*)k_resident2<kR2MaxRPT, 4, 1> : (const void*)k_resident2<kR2MaxRPT, 8, 1>;
-#undef RAS_R2
+  return lanes == 1 ? r2_fn<RPT, 1, PAT>(w) : nullptr;
+}
+template <bool PAT>
+static const void* resident2_kernel_p(int rpt, int w, int lanes) {
+  if (rpt <= 4) return r2_fn_l<4, PAT>(w, lanes);
+  if (rpt <= 8) return r2_fn_l<8, PAT>(w, lanes);
+  if (rpt <= 12) return r2_fn_l<12, PAT>(w, lanes);
+  if (rpt <= 16) return r2_fn_l<16, PAT>(w, lanes);
+  return r2_fn_l<kR2MaxRPT, PAT>(w, lanes);
+}
+static const void* resident2_kernel(int rpt, int w, int lanes, bool pat) {
+  return pat ? resident2_kernel_p<true>(rpt, w, lanes) : resident2_kernel_p<false>(rpt, w, lanes);
 }
 
 // Per-chunk export bands / ghost zones and (PAT) row-pattern tables of every
@@ -379,10 +384,9 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
       const int maxrpt = std::min(kR2ColBlk / 4 / NL, kR2MaxRPT);
       if (!pick((nl + NL - 1) / NL, maxrpt * kNC_R2, &k, &gs)) continue;
       chunk = chunk_rows(nmax, gs);
-      resident_layout(c, gs, true, Lo);
-      if (!Lo.pat) break;  // not a row-pattern matrix: v1 below
+      resident_layout(c, gs, true, Lo);  // row patterns if every chunk has <= kMaxPat, else the SELL-Z stream
       // NL lanes + the ghost staging buffer (q, r of the widest ghost zones)
-      const size_t dyn = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL) +
+      const size_t dyn = (size_t)NL * 8 * r2_lane_words(Lo.glo_max, chunk, Lo.ghi_max, c->zwL, Lo.pat) +
                          (size_t)16 * (Lo.glo_max + Lo.ghi_max);
       if (dyn + r2_static + 1024 <= (size_t)smem_optin) {
         lanes = NL;
@@ -417,7 +421,7 @@ static ras_status setup_resident(ras_ctx* c, int nmax) {
   } else {
     rpt = need <= 4 ? 4 : need <= 8 ? 8 : kResidMaxRPT;
   }
-  const void* fn = lanes ? resident2_kernel(rpt, c->zwL, lanes)
+  const void* fn = lanes ? resident2_kernel(rpt, c->zwL, lanes, Lo.pat)
                          : resident_kernel(rpt, c->z, c->z ? c->zwL : c->wL, tol, Lo.pat);
   if (!fn) return RAS_OK;
   TRY(allow_smem(c, fn));
@@ -1052,7 +1056,7 @@ static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m,
   RAS_CUDA(c, cudaMemsetAsync(c->d_resid_slots, 0xff,
                               (size_t)c->RC.ngroups * std::max(c->resid_lanes, 1) * 3 * kResidNV * c->RC.gs * 8, s));
   const bool v2 = c->resid_lanes > 0 && !(inner_tol > 0.0);
-  const void* fn = v2 ? resident2_kernel(c->resid_rpt, c->zwL, c->resid_lanes)
+  const void* fn = v2 ? resident2_kernel(c->resid_rpt, c->zwL, c->resid_lanes, c->resid_pat)
                       : resident_kernel(c->resid_rpt, c->z, c->z ? c->zwL : c->wL, inner_tol > 0.0, c->resid_pat);
   int lp0 = lp_first, nsub = nsub_;
   const int32_t* own = c->d_own_slot;
@@ -1061,7 +1065,7 @@ static ras_status enq_resident_pcg(ras_ctx* c, cudaStream_t s, Ctl C, int32_t m,
   int32_t ntable = c->z ? (int32_t)c->plan->z_table.size() : 0;
   void* args1[] = {&lp0, &nsub, &c->SS, &c->RC, &c->L,      &c->D,      &own, &x,  &c->S,
                    &C,   &m,    &inner_tol,     &chunk_max, &glo,       &ghi, &ntable};
-  void* args2[] = {&lp0, &nsub, &c->SS, &c->RC, &c->D, &own, &x, &c->S, &C, &m, &chunk_max, &glo, &ghi, &ntable};
+  void* args2[] = {&lp0, &nsub, &c->SS, &c->RC, &c->L, &c->D, &own, &x, &c->S, &C, &m, &chunk_max, &glo, &ghi, &ntable};
   void** args = v2 ? args2 : args1;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(c->RC.ngroups * c->RC.gs));

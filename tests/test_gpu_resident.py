@@ -98,3 +98,27 @@ def test_resident_irregular_converges_sync_and_async():
         assert st == 0 and t["pcg_path"] == 3 and t["resident_pattern"] == 0, (mode, t)
         assert O.verify_global(A, x, b, 1e-8)[0]
     s.close()
+
+
+@pytest.mark.parametrize("lanes_case", ["one_lane_big_cells", "two_lanes"])
+def test_resident2_sell_z_stream_on_voronoi_cells(lanes_case):
+    # Voronoi cells: hundreds of distinct rows per chunk -> k_resident2 without the
+    # row-pattern table, the SELL-Z local matrix streamed from L2 (the C5 path)
+    if lanes_case == "one_lane_big_cells":
+        N, P, gamma, m = 1500, 2, 4, 6   # ~1.1 M-row cells: chunks beyond two lanes' capacity
+    else:
+        N, P, gamma, m = 700, 6, 3, 8
+    A = ri.laplace_2d(N)
+    b = ri.rhs(A.n, 0)
+    owner = ri.voronoi_partition(N, N, P, seed=2, lloyd=4, balance=40)
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, path="resident"))
+    K = 2
+    st, x = s.solve(1e-300, K, "sync")
+    t = s.stats()
+    assert t["pcg_path"] == 3 and t["resident_pattern"] == 0 and t["resident_lanes"] >= 1, t
+    s.close()
+    subs = O.setup(A, b, owner, gamma)
+    for sb in subs:
+        O.make_local_solver(sb, "jacobi", m)
+    ref = O.ras_sync(A, b, subs, 1e-300, K, record_iterates=True)
+    assert rel(x, ref.iterates[K]) <= 1e-10, rel(x, ref.iterates[K])

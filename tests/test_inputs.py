@@ -122,3 +122,13 @@ def test_varcoef_2d_is_spd_m_matrix_and_reduces_to_laplacian():
     assert len(np.unique(A.data)) <= 4 + 13  # few distinct values (4 weights, sums of 4 of them)
     one = ri.varcoef_2d(6, 5, levels=(1.0,))
     np.testing.assert_array_equal(one.to_scipy().toarray(), ri.laplace_2d(6, 5).to_scipy().toarray())
+
+
+def test_balanced_voronoi_cells_nearly_equal_and_connected():
+    # lloyd + power-diagram balancing: a graph partitioner's balance constraint
+    # stand-in for C5 (cells within a few % of n / P), still valid 4-connected cells
+    o = ri.voronoi_partition(300, 260, 12, seed=3, lloyd=6, balance=60)
+    c = np.bincount(o, minlength=12)
+    assert c.min() > 0.93 * c.mean() and c.max() < 1.07 * c.mean(), c
+    plain = np.bincount(ri.voronoi_partition(300, 260, 12, seed=3), minlength=12)
+    assert plain.max() / plain.mean() > c.max() / c.mean()  # balancing did something

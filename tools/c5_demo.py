@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--modes", default="sync,async:central,async:decentral")
     ap.add_argument("--robin", type=float, default=0.0)
     ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--unbalanced", action="store_true", help="plain Voronoi cells (default: Lloyd + power-diagram balanced)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -49,7 +50,8 @@ def main():
     owner = None
     for seed in range(1, 50):
         try:
-            owner = ri.voronoi_partition(N, N, P, seed=seed)
+            owner = (ri.voronoi_partition(N, N, P, seed=seed) if a.unbalanced
+                     else ri.voronoi_partition(N, N, P, seed=seed, lloyd=8, balance=60))
             break
         except ValueError:
             continue
