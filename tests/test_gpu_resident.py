@@ -105,12 +105,16 @@ def test_resident2_sell_z_stream_on_voronoi_cells(lanes_case):
     # Voronoi cells: hundreds of distinct rows per chunk -> k_resident2 without the
     # row-pattern table, the SELL-Z local matrix streamed from L2 (the C5 path)
     if lanes_case == "one_lane_big_cells":
-        N, P, gamma, m = 1500, 2, 4, 6   # ~1.1 M-row cells: chunks beyond two lanes' capacity
+        # one 1.69 M-row subdomain of the variable-coefficient matrix: one lane,
+        # chunks of ~11.4 K rows, never a row-pattern table
+        N, P, gamma, m = 1300, 1, 0, 6
+        A = ri.varcoef_2d(N, N, seed=5)
+        owner = np.zeros(N * N, np.int32)
     else:
         N, P, gamma, m = 700, 6, 3, 8
-    A = ri.laplace_2d(N)
+        A = ri.laplace_2d(N)
+        owner = ri.voronoi_partition(N, N, P, seed=2, lloyd=4, balance=40)
     b = ri.rhs(A.n, 0)
-    owner = ri.voronoi_partition(N, N, P, seed=2, lloyd=4, balance=40)
     s = R.Solver(A, b, owner, gamma, R.options("jacobi", m, path="resident"))
     K = 2
     st, x = s.solve(1e-300, K, "sync")
