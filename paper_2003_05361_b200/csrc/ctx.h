@@ -129,6 +129,8 @@ struct ras_ctx {
   // IC(0)/ILU(0) path (a3')
   bool ic = false;
   double* d_z = nullptr;
+  double* d_y = nullptr;    // forward-solve output of the sync-free trisolve
+  bool trsv_sf = true;      // sync-free trisolve (k_trsv_sf); RAS_TRSV=level selects k_trsv
   ras::TriBuf tri_f, tri_b;
   uint32_t* d_trsv_ctr = nullptr;  // [2][nl + 1] chunk counters (per subdomain + batched)
   ras::Scal S{};

@@ -501,7 +501,17 @@ static ras_status upload_factors(ras_ctx* c) {
   TRY(upload_tri(c, F, c->tri_f));
   TRY(upload_tri(c, B, c->tri_b));
   TRY(zalloc(c, &c->d_z, (size_t)c->rows_pad));
+  TRY(zalloc(c, &c->d_y, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_trsv_ctr, (size_t)2 * (c->nl + 1)));
+  {
+    const char* e = getenv("RAS_TRSV");  // A/B knob: "level" = the level-barrier kernel
+    c->trsv_sf = !(e && std::strcmp(e, "level") == 0);
+  }
+  if (c->trsv_sf) {  // arm y and z with the sentinel (the solves re-arm each other afterwards)
+    k_trsv_arm<<<148 * 4, 256, 0, c->stream>>>(c->rows_pad, c->d_y, c->d_z);
+    RAS_CUDA(c, cudaGetLastError());
+    RAS_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
   c->ic = true;
   const double rows = (double)c->plan->rows_local;
   c->mb.update_dot = rows * (8 /*p*/ + 8 /*q*/ + 16 /*r*/ + 16 /*d*/);
@@ -972,11 +982,23 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
     int32_t* done = T.d_lev_done;
     RAS_CUDA(c, cudaMemsetAsync(ctr, 0, 4, s));
     int32_t c0 = 0, nch = T.nchunks;
+    if (R.lp >= 0) {
+      c0 = T.sub_c0[R.lp];
+      nch = T.sub_nc[R.lp];
+    }
+    if (c->trsv_sf) {
+      // sync-free: forward in -> y (re-arms z), backward y -> z (re-arms y)
+      const double* src = dir == 0 ? in : c->d_y;
+      double* dst = dir == 0 ? c->d_y : z;
+      double* rearm = dir == 0 ? z : c->d_y;
+      const unsigned g = (unsigned)std::max(1, std::min((nch + kThreads / 32 - 1) / (kThreads / 32), 148 * 8));
+      KL(s, K_TRSV, g, kThreads, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
+         (const int32_t*)c->S.active, C);
+      continue;
+    }
     if (R.lp < 0) {
       RAS_CUDA(c, cudaMemsetAsync(done, 0, (size_t)T.nlev_slots * 4, s));
     } else {
-      c0 = T.sub_c0[R.lp];
-      nch = T.sub_nc[R.lp];
       RAS_CUDA(c, cudaMemsetAsync(done + T.sub_lev_off[R.lp], 0, (size_t)T.sub_nlev[R.lp] * 4, s));
     }
     const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));

@@ -39,9 +39,14 @@ def main():
     kt = s.kernel_times()
     st = s.stats()
     tot = sum(v[1] for v in kt.values())
+    # levels of one triangular solve of a corner subdomain (natural order on the
+    # gamma-hop Omega_p of a box: deepest row x+y+z = 3(N/2 - 1) + gamma)
+    levels = 3 * (N // 2 - 1) + 4 + 1
     print(json.dumps({"experiment": "c4_demo", "grid": [N, N, N], "unknowns": N ** 3, "subdomains": 8, "overlap": 4,
                       "local_solver": f"{a.solver}-PCG m=10", "inputs_s": t1 - t0, "setup_s": t2 - t1,
                       "ms_per_sweep": tot / a.sweeps, "pcg_path": st["pcg_path"],
+                      "trsv": os.environ.get("RAS_TRSV", "sync-free"), "levels_per_solve": levels,
+                      "us_per_level": (1e3 * kt["k_trsv"][1] / kt["k_trsv"][0] / levels) if kt.get("k_trsv", (0,))[0] else None,
                       "kernels": {k: {"launches": v[0], "ms_per_sweep": v[1] / a.sweeps, "share": v[1] / tot}
                                   for k, v in kt.items() if v[0]}}), flush=True)
 
