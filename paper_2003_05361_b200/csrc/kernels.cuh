@@ -651,10 +651,10 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
   }
 }
 
-// Sync-free variant (round 2): no level barriers.  A warp claims one chunk (up to
+// Sync-free variant (round 2): no level barriers.  A CTA claims one chunk (up to
 // 256 rows of one level of one subdomain) at a time, in the same topological
-// (level) order; each lane solves rows ch.x + lane, + 32, ... and, for every
-// dependency j, spins on out[j] itself until it no longer holds the sentinel --
+// (level) order; each thread solves one row and, for every dependency j, spins
+// on out[j] itself until it no longer holds the sentinel --
 // the value IS the ready flag (8-byte stores are single-copy atomic), so a
 // dependency costs one L2 round trip, not a flag + a value.  The sentinel is a
 // signalling-NaN pattern no arithmetic produces (results are quieted).  Sentinel
@@ -663,6 +663,9 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
 // solve, row by row after it read them.  A claimed chunk's dependencies lie in
 // earlier claims of running warps, so every spin terminates.
 constexpr unsigned long long kTrsvSent = 0xfff4dead0000beefull;
+#ifndef RAS_TRSV_SF_SLEEP
+#define RAS_TRSV_SF_SLEEP 32  // ns back-off between polls of a dependency
+#endif
 __device__ __forceinline__ double ld_relaxed_f64_gpu(const double* p) {
   double v;
   asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
@@ -675,31 +678,38 @@ static __global__ void __launch_bounds__(kThreads) k_trsv_sf(TriDev T, int use_b
                                                              uint32_t* counter, const double* __restrict__ in,
                                                              double* out, double* rearm,
                                                              const int32_t* __restrict__ active, Ctl C) {
+  __shared__ int s_c;
   pdl_start();
-  const int lane = threadIdx.x & 31;
   const double sent = __longlong_as_double((long long)kTrsvSent);
   for (;;) {
-    int c = 0;
-    if (lane == 0) c = (int)atomicAdd(counter, 1u);
-    c = __shfl_sync(0xffffffffu, c, 0);
+    // a CTA claims one chunk (<= 256 rows of one level): one row per thread
+    if (threadIdx.x == 0) s_c = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int c = s_c;
+    __syncthreads();
     if (c >= nchunk) return;
     const int cid = use_batched ? T.batched[c] : c0 + c;
     const int4 ch = T.chunk[cid];
     const bool skip = stopped(C, ch.z) || !active[ch.z];
-    for (int k = ch.x + lane; k < ch.y; k += 32) {
+    const int k = ch.x + threadIdx.x;
+    if (k < ch.y) {
       const int32_t i = __ldg(&T.rows[k]);
       const double xin = __ldcg(&in[i]);
       st_relaxed_f64_gpu(&rearm[i], sent);  // the other solve's output, consumed before this launch
-      if (skip) continue;
-      double s = xin;
-      const int32_t e1 = __ldg(&T.rp[k + 1]);
-      for (int32_t e = __ldg(&T.rp[k]); e < e1; ++e) {
-        const double* dep = &out[__ldg(&T.col[e])];
-        double v = ld_relaxed_f64_gpu(dep);
-        while (__double_as_longlong(v) == (long long)kTrsvSent) v = ld_relaxed_f64_gpu(dep);
-        s -= __ldg(&T.val[e]) * v;
+      if (!skip) {
+        double s = xin;
+        const int32_t e1 = __ldg(&T.rp[k + 1]);
+        for (int32_t e = __ldg(&T.rp[k]); e < e1; ++e) {
+          const double* dep = &out[__ldg(&T.col[e])];
+          double v = ld_relaxed_f64_gpu(dep);
+          while (__double_as_longlong(v) == (long long)kTrsvSent) {
+            __nanosleep(RAS_TRSV_SF_SLEEP);
+            v = ld_relaxed_f64_gpu(dep);
+          }
+          s -= __ldg(&T.val[e]) * v;
+        }
+        st_relaxed_f64_gpu(&out[i], s / __ldg(&T.diag[i]));
       }
-      st_relaxed_f64_gpu(&out[i], s / __ldg(&T.diag[i]));
     }
   }
 }

@@ -991,7 +991,7 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
       const double* src = dir == 0 ? in : c->d_y;
       double* dst = dir == 0 ? c->d_y : z;
       double* rearm = dir == 0 ? z : c->d_y;
-      const unsigned g = (unsigned)std::max(1, std::min((nch + kThreads / 32 - 1) / (kThreads / 32), 148 * 8));
+      const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));
       KL(s, K_TRSV, g, kThreads, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
          (const int32_t*)c->S.active, C);
       continue;
