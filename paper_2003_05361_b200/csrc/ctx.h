@@ -130,7 +130,7 @@ struct ras_ctx {
   bool ic = false;
   double* d_z = nullptr;
   double* d_y = nullptr;    // forward-solve output of the sync-free trisolve
-  bool trsv_sf = true;      // sync-free trisolve (k_trsv_sf); RAS_TRSV=level selects k_trsv
+  bool trsv_sf = false;     // sync-free trisolve (k_trsv_sf, RAS_TRSV=sf); default k_trsv (level barriers)
   ras::TriBuf tri_f, tri_b;
   uint32_t* d_trsv_ctr = nullptr;  // [2][nl + 1] chunk counters (per subdomain + batched)
   ras::Scal S{};

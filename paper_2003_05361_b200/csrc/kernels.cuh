@@ -645,8 +645,10 @@ static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batc
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(&lev_done[T.sub_lev_off[lp] + lev], 1);
+      // release: the CTA's out[] stores (ordered before this thread by the barrier)
+      // before the count; one fire-and-forget reduction instead of a full
+      // sequentially-consistent fence + atomic
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&lev_done[T.sub_lev_off[lp] + lev]) : "memory");
     }
   }
 }

@@ -504,8 +504,10 @@ static ras_status upload_factors(ras_ctx* c) {
   TRY(zalloc(c, &c->d_y, (size_t)c->rows_pad));
   TRY(zalloc(c, &c->d_trsv_ctr, (size_t)2 * (c->nl + 1)));
   {
-    const char* e = getenv("RAS_TRSV");  // A/B knob: "level" = the level-barrier kernel
-    c->trsv_sf = !(e && std::strcmp(e, "level") == 0);
+    // A/B knob: "sf" = the sync-free kernel (measured 2x slower than the level
+    // barriers on B200: profiles/r02_trsv.md), default the level-barrier kernel
+    const char* e = getenv("RAS_TRSV");
+    c->trsv_sf = e && std::strcmp(e, "sf") == 0;
   }
   if (c->trsv_sf) {  // arm y and z with the sentinel (the solves re-arm each other afterwards)
     k_trsv_arm<<<148 * 4, 256, 0, c->stream>>>(c->rows_pad, c->d_y, c->d_z);
@@ -991,7 +993,11 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
       const double* src = dir == 0 ? in : c->d_y;
       double* dst = dir == 0 ? c->d_y : z;
       double* rearm = dir == 0 ? z : c->d_y;
-      const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));
+      static const int sf_grid = [] {  // A/B knob: CTAs of the sync-free solve (default 2 per SM)
+        const char* e = getenv("RAS_TRSV_SF_CTAS");
+        return e ? std::max(1, atoi(e)) : 148 * 2;
+      }();
+      const unsigned g = (unsigned)std::max(1, std::min(nch, sf_grid));
       KL(s, K_TRSV, g, kThreads, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
          (const int32_t*)c->S.active, C);
       continue;
