@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the small-config time-to-solution runs")
+    ap.add_argument("--config", default="c2", choices=["c2", "c5"],
+                    help="c2: C2 at N=1 / C3-style weak scaling at N>1 (default); c5: C5-shaped weak scaling "
+                         "(8 balanced irregular cells of ~1.56 M unknowns per GPU; 10^8 at N=8)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--tts", action="store_true", help="also run to rel. residual 1e-8 (long)")
     ap.add_argument("--scale", type=int, default=SUB, help="owned side per subdomain (debug)")
@@ -182,9 +185,26 @@ def dist_env():
     return rank, world, local
 
 
-def build_rank_problem(N, rank, scale=SUB):
-    """Row window of the global Laplacian + RHS + owner array for one rank."""
+def build_rank_problem(N, rank, scale=SUB, config="c2"):
+    """Row window of the global Laplacian + RHS + owner array for one rank.
+    config "c5": BASELINE configs[4] shape per GPU -- 8 balanced irregular cells of
+    ~1.56 M unknowns per GPU (Voronoi + Lloyd + power-diagram balancing, the graph-
+    partitioner stand-in), N x 12.5 M unknowns in total (10^8 at N = 8)."""
     from paper_2003_05361_b200 import partition_regular
+
+    if config == "c5":
+        import numpy as np_
+
+        side = int(round((12.5e6 * N) ** 0.5))
+        P = 8 * N
+        owner = ri.voronoi_partition(side, side, P, seed=1, lloyd=8, balance=60)
+        s2r = (np_.arange(P) * N) // P
+        rows = np_.nonzero(s2r[owner] == rank)[0]
+        r0 = max(0, int(rows.min()) - (GAMMA + 1) * side)
+        r1 = min(side * side, int(rows.max()) + 1 + (GAMMA + 1) * side)
+        A = ri.laplace_2d_rows(side, side, r0, r1)
+        b = ri.rhs_rows(side * side, r0, r1, 0)
+        return dict(nx=side, ny=side, n=side * side, P=P, px=0, py=0, owner=owner, A=A, b=b)
 
     px, py = TILES.get(N, (4, 4 * N))
     nx, ny = px * scale, py * scale
@@ -332,12 +352,17 @@ def run_reference(args):
 METRIC = "RAS iterations/s (sync sweeps/s); time-to-solution to 1e-8 in `tts`; SpMV GB/s in `spmv_gbs`"
 
 
-def config_dict(N, nx, ny, P, mode):
+def config_dict(N, nx, ny, P, mode, config="c2"):
     # identical in both arms (the driver compares them); the working set of the
     # sweep (r, p, d, b, x, matrix ~ 12 B/row) is >= 1.3 GB per GPU at C2 >> 126 MB L2
     ws = 8.0 * nx * ny * 10
-    return {"workload": (f"{'C2' if N == 1 else 'C3-weak'}: 2D 5-pt Laplacian {nx}x{ny} ({nx * ny / 1e6:.1f}M unknowns), "
-                         f"{P} subdomains of {SUB}^2 ({P // N}/GPU), overlap {GAMMA}, Jacobi-PCG m={M_INNER}, {mode} RAS"),
+    if config == "c5":
+        name = (f"C5-shaped: 2D 5-pt Laplacian {nx}x{ny} ({nx * ny / 1e6:.1f}M unknowns), {P} balanced irregular "
+                f"(graph-partition stand-in) subdomains ({P // N}/GPU), overlap {GAMMA}, Jacobi-PCG m={M_INNER}, {mode} RAS")
+    else:
+        name = (f"{'C2' if N == 1 else 'C3-weak'}: 2D 5-pt Laplacian {nx}x{ny} ({nx * ny / 1e6:.1f}M unknowns), "
+                f"{P} subdomains of {SUB}^2 ({P // N}/GPU), overlap {GAMMA}, Jacobi-PCG m={M_INNER}, {mode} RAS")
+    return {"workload": name,
             "grid": [nx, ny], "subdomains": P, "subdomains_per_gpu": P // N, "overlap": GAMMA,
             "inner_iters": M_INNER, "mode": mode, "precision": "fp64",
             "parallelism": f"domain decomposition, {P // N} subdomains per GPU x {N} GPU",
@@ -373,7 +398,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     t_setup0 = time.perf_counter()
-    prob = build_rank_problem(N, rank, args.scale)
+    prob = build_rank_problem(N, rank, args.scale, args.config)
     opts = R.options("jacobi", M_INNER, plain=args.plain, fuse_p=args.fuse_p, path=args.path, robin=args.robin)
     solver = R.Solver(prob["A"], prob["b"], prob["owner"], GAMMA, opts,
                       comm={"rank": rank, "world": world, "device": local, "nccl_id": nccl_id,
@@ -518,11 +543,11 @@ def main():
         tts["bench_workload"] = {"time_s": time.perf_counter() - t0, "device_time_s": s2["time_to_solution_s"],
                                  "sweeps": s2["sweeps"], "inner_iters_total": s2["inner_iters_total"],
                                  "final_rel_residual": s2["final_rel_residual"], "converged": bool(s2["converged"])}
-    do_small = rank == 0 and N == 1 and not args.no_tts
+    do_small = rank == 0 and N == 1 and not args.no_tts and args.config == "c2"
     if do_small:
         tts.update(gpu_tts_small(R))
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+    if rank == 0 and N == 1 and not args.no_cpu_baseline and args.config == "c2":
         val, det = oracle_sweeps(nx, ny, prob["px"], prob["py"], K=3)
         o_tts = {}
         if do_small:
@@ -548,7 +573,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "sweeps/s",
             "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(N, nx, ny, P, mode),
+            "config": config_dict(N, nx, ny, P, mode, args.config),
             "subdomain_updates_per_s": updates_per_s,
             "spmv_gbs": res["gbs"] if res else None,
             "spmv_frac": (res["gbs"] / peak) if res else None,
