@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RAS_ABI_VERSION 3
+#define RAS_ABI_VERSION 4
 
 typedef struct ras_ctx ras_ctx; /* opaque; one per rank (process) */
 
@@ -150,6 +150,11 @@ typedef struct {
    * (the restricted iteration diverges without overlap), else RAS_EINVAL. */
   double robin;
   double reserved_d[3];
+  int32_t device_setup;          /* 1 (default): the gamma-hop overlap sets Omega_p / Gamma_p, the owned and
+                                    halo slot maps and the receive counts are built by CUDA kernels
+                                    (row a0 on the device); 0: by the host BFS of the plan (ras_plan.h).
+                                    Both give identical plans (bit-exact, tested) */
+  int32_t reserved_j[3];
 } ras_options;
 
 /* Transport of a multi-rank context (ras_comm.transport). */

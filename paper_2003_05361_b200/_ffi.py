@@ -19,7 +19,7 @@ RAS_LS_JACOBI_PCG, RAS_LS_IC0_PCG, RAS_LS_ILU0_PCG, RAS_LS_EXACT_PCG, RAS_LS_CHO
 RAS_DET_CENTRAL, RAS_DET_DECENTRAL = 0, 1
 RAS_PCG_AUTO, RAS_PCG_TILED, RAS_PCG_BLOCK, RAS_PCG_RESIDENT = range(4)
 RAS_TRANSPORT_NCCL, RAS_TRANSPORT_LOOPBACK = 0, 1
-ABI_VERSION = 3  # include/ras.h RAS_ABI_VERSION
+ABI_VERSION = 4  # include/ras.h RAS_ABI_VERSION
 
 I32, I64, F64, U8 = C.c_int32, C.c_int64, C.c_double, C.c_uint8
 P = C.POINTER
@@ -38,7 +38,8 @@ class RasOptions(C.Structure):
     _fields_ = [("local_solver", I32), ("inner_iters", I32), ("inner_tol", F64), ("detector", I32),
                 ("local_crit_owned_only", I32), ("max_resumes", I32), ("use_graphs", I32), ("poll_interval", I32),
                 ("async_timeout_s", F64), ("scripted_flags", I32), ("fuse_p", I32), ("matrix_format", I32), ("stage_p", I32),
-                ("pcg_path", I32), ("async_persistent", I32), ("force_first_stop", I32), ("persistent_grid", I32), ("robin", F64), ("reserved_d", F64 * 3)]
+                ("pcg_path", I32), ("async_persistent", I32), ("force_first_stop", I32), ("persistent_grid", I32), ("robin", F64), ("reserved_d", F64 * 3),
+                ("device_setup", I32), ("reserved_j", I32 * 3)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libras_b200.so")
-SOURCES = ["plan.cpp", "factor.cpp", "zformat.cpp", "comm.cu", "solver.cu", "async.cu"]
+SOURCES = ["plan.cpp", "factor.cpp", "zformat.cpp", "comm.cu", "setup_dev.cu", "solver.cu", "async.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3"]
 

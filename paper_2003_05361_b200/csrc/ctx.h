@@ -203,6 +203,8 @@ ras_status async_setup(ras_ctx* c);
 ras_status async_set_b2(ras_ctx* c);  // re-upload the Eq. 2 ||b~_p||^2 after ras_set_rhs
 void async_free(ras_ctx* c);
 ras_status put_stress(ras_ctx* c, int64_t epochs, int64_t words, int64_t* out4);  // R17 stress test
+ras_status plan_build_device(ras_ctx* c, ras_plan** out, const ras_csr* A, const double* b, const ras_partition* part,
+                             int32_t overlap);  // row a0 on the device (setup_dev.cu)
 }  // namespace ras
 
 #define TRY(x)                   \

@@ -59,7 +59,7 @@ static void check_rows(const ras_plan* pl) {
   }
 }
 
-static void build_phase1(ras_plan* pl, const ras_partition* part) {
+static void build_phase1(ras_plan* pl, const ras_partition* part, const PlanDeviceHook* hook) {
   const int64_t n = pl->n;
   const int32_t P = pl->P;
   // ---- subdomain -> rank ----
@@ -91,6 +91,19 @@ static void build_phase1(ras_plan* pl, const ras_partition* part) {
   for (int32_t p = 0; p < P; ++p)
     if (count[p] == 0) throw fail(RAS_EINVAL, "subdomain " + std::to_string(p) + " is empty");
 
+  if (hook) {
+    // overlap sets, owned / halo slots, receive counts built on the device
+    // (setup_dev.cu); the host keeps only the bookkeeping below
+    ras_status st = hook->fn(hook->user, pl, part);
+    if (st != RAS_OK) throw fail(st, tls_error());
+    if (pl->n_own > INT32_MAX / 2) throw fail(RAS_EINVAL, "too many owned rows on one rank for int32 slots");
+    pl->send_gid.assign(pl->world, {});
+    pl->send_slot.assign(pl->world, {});
+    pl->send_remote_off.assign(pl->world, 0);
+    pl->send_set.assign(pl->world, 0);
+    pl->send_set[pl->rank] = 1;
+    return;
+  }
   // ---- gamma-hop BFS per local subdomain (R1, P136-140) ----
   Window W{pl};
   std::vector<int32_t> mark(n, -1), gmark(n, -1);
@@ -395,6 +408,14 @@ extern "C" {
 
 ras_status ras_plan_build(ras_plan** out, const ras_csr* A, const double* b, const ras_partition* part,
                           int32_t overlap, int32_t rank, int32_t world) {
+  return ras::plan_build_ex(out, A, b, part, overlap, rank, world, nullptr);
+}
+
+}  // extern "C"
+
+namespace ras {
+ras_status plan_build_ex(ras_plan** out, const ras_csr* A, const double* b, const ras_partition* part, int32_t overlap,
+                         int32_t rank, int32_t world, const PlanDeviceHook* hook) {
   if (!out) {
     ras::set_tls_error("ras_plan_build: out is NULL");
     return RAS_EINVAL;
@@ -423,7 +444,7 @@ ras_status ras_plan_build(ras_plan** out, const ras_csr* A, const double* b, con
     pl->A_val = A->val;
     pl->b_win = b;
     ras::check_rows(pl);
-    ras::build_phase1(pl, part);
+    ras::build_phase1(pl, part, hook);
     *out = pl;
     return RAS_OK;
   } catch (const Fail& f) {
@@ -436,6 +457,10 @@ ras_status ras_plan_build(ras_plan** out, const ras_csr* A, const double* b, con
     return RAS_ENOMEM;
   }
 }
+
+}  // namespace ras
+
+extern "C" {
 
 ras_status ras_plan_get_info(const ras_plan* pl, ras_plan_info* info) {
   if (!pl || !info) return RAS_EINVAL;

@@ -58,6 +58,19 @@ struct SubPlan {
 
 }  // namespace ras
 
+// Device-side phase 1 (setup_dev.cu): fills, for every local subdomain, omega /
+// owned / ghosts / nbr_subs / nbr_cnt / own_off / nown, and the rank's slot map,
+// own_gid, halo_gid, halo_off, n_own, n_halo -- exactly what the host BFS of
+// plan.cpp computes.  Returns a ras_status (message via set_tls_error).
+namespace ras {
+struct PlanDeviceHook {
+  ras_status (*fn)(void* user, ras_plan* pl, const ras_partition* part);
+  void* user;
+};
+ras_status plan_build_ex(ras_plan** out, const ras_csr* A, const double* b, const ras_partition* part, int32_t overlap,
+                         int32_t rank, int32_t world, const PlanDeviceHook* hook);
+}  // namespace ras
+
 struct ras_plan {
   int64_t n = 0;
   int32_t P = 0, rank = 0, world = 1, gamma = 0;

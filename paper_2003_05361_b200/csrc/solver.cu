@@ -774,8 +774,9 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
     RAS_CUDA(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
   }
-  // ---- plan (host, CPU-side) ----
-  ras_status s = ras_plan_build(&c->plan, A, b, part, overlap, c->rank, c->world);
+  // ---- plan: overlap sets and index maps on the device (default) or the host ----
+  ras_status s = c->opt.device_setup ? plan_build_device(c, &c->plan, A, b, part, overlap)
+                                     : ras_plan_build(&c->plan, A, b, part, overlap, c->rank, c->world);
   if (s != RAS_OK) return set_err(c, s, tls_error());
   if (c->world > 1) {
     if (c->loopback) {
@@ -1464,6 +1465,7 @@ ras_status ras_options_default(ras_options* o) {
   o->poll_interval = 4;
   o->async_timeout_s = 1800.0;
   o->async_persistent = 2;
+  o->device_setup = 1;
   return RAS_OK;
 }
 

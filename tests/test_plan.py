@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert {n for n, _, _ in R._ffi.SIGNATURES} == names
-    assert lib.ras_abi_version() == R._ffi.ABI_VERSION == 3
+    assert lib.ras_abi_version() == R._ffi.ABI_VERSION == 4
     # provenance: the loaded library was built from exactly this tree
     from paper_2003_05361_b200.build import source_hash
 
