@@ -84,6 +84,7 @@ struct ras_ctx {
   std::vector<ras::DevBuf> bufs;
   std::string err;
   double setup_s = 0.0;
+  double setup_phase[4] = {};  // plan, finalize, upload + layouts, async runtime (RAS_SETUP_TRACE)
   double b2_global = 0.0;  // ||b||^2
 
   // ---- device arrays ----

@@ -775,9 +775,11 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
     c->own_stream = true;
   }
   // ---- plan: overlap sets and index maps on the device (default) or the host ----
+  const double ts0 = now_s();
   ras_status s = c->opt.device_setup ? plan_build_device(c, &c->plan, A, b, part, overlap)
                                      : ras_plan_build(&c->plan, A, b, part, overlap, c->rank, c->world);
   if (s != RAS_OK) return set_err(c, s, tls_error());
+  c->setup_phase[0] = now_s() - ts0;
   if (c->world > 1) {
     if (c->loopback) {
       TRY(loop_join(c, comm->nccl_unique_id));
@@ -794,9 +796,13 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
     return set_err(c, RAS_EINVAL, "robin (ORAS transmission parameter) must be in [0, 1)");
   if (c->opt.robin > 0.0 && overlap < 1)
     return set_err(c, RAS_EINVAL, "robin > 0 (ORAS) needs overlap >= 1: without overlap the iteration diverges (R30)");
+  const double ts1 = now_s();
   s = ras_plan_finalize(c->plan);
   if (s != RAS_OK) return set_err(c, s, tls_error());
+  const double ts2 = now_s();
   TRY(upload_plan(c));
+  c->setup_phase[1] = ts2 - ts1;
+  c->setup_phase[2] = now_s() - ts2;
   // ||b||^2 over all ranks (owned rows), fixed order on one rank, NCCL sum across ranks
   c->b2_global = c->plan->b2_global_local;
   TRY(coll_allreduce_f64(c, &c->b2_global, 1, false));
@@ -807,8 +813,15 @@ static ras_status setup_impl(ras_ctx* c, const ras_csr* A, const double* b, cons
   } else if (c->opt.local_solver != RAS_LS_JACOBI_PCG && c->opt.local_solver != RAS_LS_EXACT_PCG) {
     return set_err(c, RAS_EINVAL, "unknown local solver");
   }
+  const double ts3 = now_s();
   TRY(async_setup(c));
   RAS_CUDA(c, cudaDeviceSynchronize());
+  c->setup_phase[3] = now_s() - ts3;
+  if (getenv("RAS_SETUP_TRACE"))
+    fprintf(stderr, "[ras setup rank %d] plan (overlap sets + maps, %s) %.3f s, finalize (matrices) %.3f s, "
+                    "upload + kernel layouts %.3f s, async runtime %.3f s\n",
+            c->rank, c->opt.device_setup ? "device" : "host", c->setup_phase[0], c->setup_phase[1], c->setup_phase[2],
+            c->setup_phase[3]);
   return RAS_OK;
 }
 
