@@ -41,7 +41,7 @@ def _worker(rank, world, nccl_id, cfg, q):
             b = b[r0:r1]
         s = R.Solver(A, b, owner, gamma,
                      R.options(cfg["solver"], cfg["m"], detector=cfg.get("detector", "decentral"),
-                               path=cfg.get("path", "auto")),
+                               path=cfg.get("path", "auto"), async_persistent=cfg.get("persistent", 2)),
                      comm={"rank": rank, "world": world, "device": rank, "nccl_id": nccl_id})
         out = {}
         for k in cfg.get("ks", []):
@@ -106,10 +106,13 @@ def test_multi_gpu_sync_parity(world, path):
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("detector", ["central", "decentral"])
-def test_multi_gpu_async_p2p_converges(detector):
+@pytest.mark.parametrize("persistent", [0, 1])
+def test_multi_gpu_async_p2p_converges(detector, persistent):
+    # persistent = 1: the in-kernel NVLink puts, version bumps and cross-GPU detector
+    # boards of k_async_persistent; 0: the per-subdomain stream driver
     nx, ny = 80, 80
     cfg = dict(nx=nx, ny=ny, P=6, gamma=4, solver="jacobi", m=10, converge="async", detector=detector,
-               owner=ri.voronoi_partition(nx, ny, 6, seed=2))
+               owner=ri.voronoi_partition(nx, ny, 6, seed=2), persistent=persistent)
     res = _run(2, cfg)
     A = ri.laplace_2d(nx, ny)
     b = ri.rhs(nx * ny, 0)
