@@ -9,7 +9,7 @@ residual, local solves, restricted prolongation, exchange, global check).
 
 value     = RAS iterations/s = sync sweeps / s (max over ranks); the aggregate
             subdomain updates/s (subdomains x sweeps/s) is the extra key `subdomain_updates_per_s`
-e2e       = the same through ras_solve() with pinned HOST x0 / x_out, copies inside
+e2e       = the same through the public API with pinned HOST x0 / x_out (each rank its owned values), copies inside
 roofline  = dominant kernel: algorithmic bytes / CUDA-event duration vs measured HBM copy peak
 spmv_gbs  = the residual SpMV (k_residual, a1+a2): algorithmic bytes / event time
 tts       = time-to-solution to rel. residual 1e-8 (P474-480) on C1 and the 256^2 / 512^2
@@ -510,27 +510,31 @@ def main():
                                "SELL-Z / int32 SELL indices, FP64 values"}
     pcg_bytes = sum(kern[k]["bytes_per_launch"] * kern[k]["launches"] for k in kern if kern[k]["bytes_per_launch"])
     pcg_ms = sum(ktimes[k][1] for k in kern if kern[k]["bytes_per_launch"])
-    # e2e through ras_solve with pinned host buffers
+    # e2e through the public API with pinned HOST buffers: every step copies this
+    # rank's owned x0 in and its owned x^{k+1} out (ras_solve_device with host
+    # pointers: the distributed form of ras_solve -- no global gather, so the bytes
+    # per rank stay constant as N grows); Bi / Bo are summed over the ranks
     e2e = None
     if not args.no_e2e:
-        x0 = torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
-        xo = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
-        _solve_host(solver, x0, xo, mode)  # untimed warm-up: first-use buffers (global-order x) allocated here
+        n_own = solver.owned_gids().size
+        x0 = torch.zeros(n_own, dtype=torch.float64, pin_memory=True)
+        xo = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
+        solver.solve_device(1e-300, 1, mode, x0.data_ptr(), xo.data_ptr())  # untimed warm-up
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            _solve_host(solver, x0, xo, mode)
+            solver.solve_device(1e-300, 1, mode, x0.data_ptr(), xo.data_ptr())
         barrier()
         el = time.perf_counter() - t0
         te = torch.tensor([el], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
-        d2h = n * 8  # x_out: the assembled global vector (NCCL allreduce on device, one D2H copy)
         e2e = {"value": args.e2e_steps / el, "unit": "sweeps/s", "h2d_bytes_per_step": n * 8,
-               "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "note": "each step = ras_solve(x0=pinned host, max_iters=1, x_out=pinned host): H2D x0, one sweep + "
-                       "final check, gather, D2H x"}
+               "d2h_bytes_per_step": n * 8, "steps": args.e2e_steps,
+               "note": "each step = ras_solve_device(x0 = pinned host owned values, max_iters=1, x_out = pinned host "
+                       "owned values) on every rank: H2D x0 (+ halo exchange), one sweep + final check, D2H x; bytes "
+                       "summed over ranks (= n x 8 each way)"}
     # time-to-solution (P474-480): the bench workload itself only with --tts (C2 needs
     # ~1e5 sweeps, ~7 min); C1 and the 256^2 / 512^2 analogues always at N=1
     tts = {}
@@ -643,17 +647,6 @@ def gpu_tts_small(R):
         s.close()
         out[name] = rec
     return out
-
-
-def _solve_host(solver, x0, xo, mode):
-    import ctypes as C
-
-    from paper_2003_05361_b200 import _ffi as F
-
-    st = F.lib().ras_solve(solver._h, 1e-300, 1, F.RAS_SYNC if mode == "sync" else F.RAS_ASYNC,
-                           x0.ctypes.data_as(C.POINTER(C.c_double)), xo.ctypes.data_as(C.POINTER(C.c_double)))
-    if st not in (F.RAS_OK, F.RAS_ENOCONV):
-        raise RuntimeError(F.lib().ras_last_error(solver._h))
 
 
 if __name__ == "__main__":

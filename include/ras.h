@@ -239,9 +239,11 @@ ras_status ras_set_rhs(ras_ctx* ctx, const double* b);
 ras_status ras_solve(ras_ctx* ctx, double tol, int64_t max_iters, ras_mode mode, const double* x0,
                      double* x_out);
 
-/* Device-resident variant for benchmarks: x0 / x_out are DEVICE pointers to this
- * rank's owned values (len ras_stats_t-independent: ras_owned_count()), ordered
- * as ras_owned_gids(); either may be NULL. */
+/* Distributed variant: x0 / x_out hold only THIS rank's owned values (len
+ * ras_owned_count(), ordered as ras_owned_gids()), as device pointers or host
+ * pointers (pinned or pageable; unified addressing picks the copy direction);
+ * either may be NULL.  No global gather: every rank moves n_own values, so the
+ * host<->device traffic of a solve does not grow with the number of GPUs. */
 ras_status ras_solve_device(ras_ctx* ctx, double tol, int64_t max_iters, ras_mode mode, const double* x0_owned_dev,
                             double* x_owned_dev);
 

@@ -1624,7 +1624,7 @@ ras_status ras_solve_device(ras_ctx* c, double tol, int64_t max_iters, ras_mode 
   c->launches = 0;
   kt_reset(c);
   if (x0_owned_dev) {
-    RAS_CUDA(c, cudaMemcpyAsync(c->d_x, x0_owned_dev, c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
+    RAS_CUDA(c, cudaMemcpyAsync(c->d_x, x0_owned_dev, c->n_own * 8, cudaMemcpyDefault, c->stream));
   } else {
     RAS_CUDA(c, cudaMemsetAsync(c->d_x, 0, c->n_own * 8, c->stream));
   }
@@ -1638,7 +1638,7 @@ ras_status ras_solve_device(ras_ctx* c, double tol, int64_t max_iters, ras_mode 
   ras_status s = solve_common(c, tol, max_iters, mode);
   if (s != RAS_OK && s != RAS_ENOCONV && s != RAS_EVERIFY) return s;
   finish_stats(c, mode, now_s() - t0);
-  if (x_owned_dev) RAS_CUDA(c, cudaMemcpyAsync(x_owned_dev, c->d_x, c->n_own * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (x_owned_dev) RAS_CUDA(c, cudaMemcpyAsync(x_owned_dev, c->d_x, c->n_own * 8, cudaMemcpyDefault, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
   kt_collect(c);
   if (s != RAS_OK) return s;

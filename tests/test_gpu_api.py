@@ -148,3 +148,22 @@ def test_phase_times_populated(mode, path):
     if mode == "sync":
         assert tot >= 0.5 * t["time_to_solution_s"], t
     s.close()
+
+
+def test_solve_device_accepts_host_owned_buffers():
+    # ras_solve_device with HOST pointers (the distributed e2e form): same iterate as
+    # the gathered ras_solve, restricted to the owned values
+    A, b, owner, gamma, m = setup()
+    s = R.Solver(A, b, owner, gamma, R.options("jacobi", m))
+    gids = s.owned_gids()
+    x0 = np.zeros(len(gids))
+    xo = np.empty(len(gids))
+    s.solve_device(1e-300, 4, "sync", x0.ctypes.data, xo.ctypes.data)
+    _, xg = s.solve(1e-300, 4, "sync")
+    np.testing.assert_array_equal(xo, xg[gids])
+    # warm start from host owned values continues the iteration
+    y = np.empty(len(gids))
+    s.solve_device(1e-300, 3, "sync", xo.ctypes.data, y.ctypes.data)
+    _, x7 = s.solve(1e-300, 7, "sync")
+    assert rel(y, x7[gids]) <= 1e-12
+    s.close()
