@@ -22,6 +22,7 @@
 //                v declares when c_v AND all; STOP floods over the tree.
 // After every local subdomain stopped: barrier, halo refresh, true residual
 // (P346-348); if it fails, flags are cleared and iteration resumes (R20).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -56,6 +57,8 @@ struct DetDev {
   const int32_t* force;   // test hook (ras_options.force_first_stop): nonzero -> every flag reads as set
   double* phase;          // [nl][kNPhase] device seconds per phase (ras_stats_t t_*), summed over updates
   unsigned long long* phase_last;  // [nl] globaltimer of the subdomain's last phase boundary
+  int32_t lockstep;       // diagnostic (RAS_PERSISTENT_LOCKSTEP=1, one CTA per subdomain): grid barriers
+                          // between every residual and every write -> the synchronous sweep (R33 study)
 };
 
 // Phase accounting of asynchronous updates (ras_stats_t t_residual ... t_convcheck,
@@ -358,6 +361,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       }
       __syncthreads();
       if (s_stop) continue;
+      if (det.lockstep) cooperative_groups::this_grid().sync();  // every residual read x^k
       // a3: the whole local PCG in shared memory; a4: x[S_p] += d
       const int its = v[0] != 0.0 ? block_pcg<RPT, WL, Z>(L, D, r0, n, sp, sr, sd, v[0], v[1], m, inner_tol, red) : 0;
       if (threadIdx.x == 0) phase_mark(det, lp, PH_SOLVE);
@@ -367,6 +371,7 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
           if (sl >= 0) st_relaxed_f64(&x[sl], ld_relaxed_f64(&x[sl]) + sd[i]);
         }
       if (threadIdx.x == 0) phase_mark(det, lp, PH_PROL);
+      if (det.lockstep) cooperative_groups::this_grid().sync();  // every write landed before the next residuals
       // a5 (multi-GPU): owner values other GPUs need, stored straight into their
       // halo storage over NVLink; then a system-scope fence and a version bump in
       // each destination's board (MPI_Put + flush analogue, P394-396)
@@ -580,6 +585,10 @@ ras_status async_setup(ras_ctx* c) {
   A->d_b2 = db2;
   TRY(zalloc(c, &A->d_force, 1));
   D.force = A->d_force;
+  {
+    const char* e = getenv("RAS_PERSISTENT_LOCKSTEP");
+    D.lockstep = e && e[0] == '1';
+  }
   TRY(zalloc(c, &D.phase, (size_t)std::max(nl, 1) * kNPhase));
   TRY(zalloc(c, &D.phase_last, (size_t)std::max(nl, 1)));
   D.boards = A->d_boards;
