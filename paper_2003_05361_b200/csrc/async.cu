@@ -411,6 +411,23 @@ static const void* async_persistent_kernel(int rpt, bool z, int wr, int wl) {
 #undef RAS_AP
 }
 
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first launch,
+// and that load can wait for kernels already running.  With loopback virtual
+// ranks on one device, rank A's kernel may be spinning on a flag rank B's kernel
+// sets while B launches something for the first time: a deadlock.  So every
+// kernel an asynchronous solve launches is loaded at setup.
+static ras_status preload_async_kernels(ras_ctx* c) {
+  const void* fns[] = {(const void*)k_phase, (const void*)k_detect, (const void*)k_detect_scripted,
+                       (const void*)k_put, (const void*)k_mirror_stops};
+  cudaFuncAttributes fa;
+  for (const void* f : fns) RAS_CUDA(c, cudaFuncGetAttributes(&fa, f));
+  for (int rpt : {4, 9, 14})
+    for (int z = 0; z < 2; ++z)
+      for (int wr : {4, 8})
+        for (int wl : {4, 8}) RAS_CUDA(c, cudaFuncGetAttributes(&fa, async_persistent_kernel(rpt, z, wr, wl)));
+  return RAS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -643,6 +660,7 @@ ras_status async_setup(ras_ctx* c) {
   TRY(upload(c, &A->d_put_peer_off, A->put_peer_off, 1));
   A->streams.resize(nl);
   for (auto& s : A->streams) RAS_CUDA(c, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  TRY(preload_async_kernels(c));
   return RAS_OK;
 }
 
@@ -985,12 +1003,22 @@ static __global__ void k_stress_read(const unsigned long long* win, int64_t word
   __shared__ unsigned long long s_cnt[3];
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
   int last = 0;
-  unsigned long long obs = 0;
+  unsigned long long obs = 0, t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_v = ld_acquire_sys(ver);
+    if (threadIdx.x == 0) {
+      s_v = ld_acquire_sys(ver);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (s_v < epochs && t - t0 > 60ull * 1000000000ull) s_v = -1;  // writer never finished: give up (no GPU hang)
+    }
     __syncthreads();
     const int v = s_v;
+    if (v < 0) {
+      obs = 0;  // reported as zero observations: the caller's check fails
+      break;
+    }
     if (v < last && threadIdx.x == 0) atomicAdd(&s_cnt[2], 1ull);
     last = v;
     unsigned long long torn = 0, stale = 0;
@@ -1016,11 +1044,17 @@ ras_status put_stress(ras_ctx* c, int64_t epochs, int64_t words, int64_t* out4) 
   if (words < 1 || words > c->n_own + c->n_halo || epochs < 1 || epochs > (1 << 30))
     return set_err(c, RAS_EINVAL, "put stress test: words must be in [1, storage of the reader], epochs >= 1");
   int32_t* ver = A->board + 3 * c->plan->P;  // VER section of this rank's board, word 0
+  // every allocation before the barrier: with loopback virtual ranks on one device
+  // a cudaMalloc / cudaFree may wait for the whole device, i.e. for the other
+  // rank's spinning reader, which waits for this rank's writer (deadlock)
+  unsigned long long* d_out = nullptr;
+  TRY(zalloc(c, &d_out, 4));
+  cudaFuncAttributes fa;  // loaded now, not at a launch racing the other rank's spinning kernel
+  RAS_CUDA(c, cudaFuncGetAttributes(&fa, k_stress_write));
+  RAS_CUDA(c, cudaFuncGetAttributes(&fa, k_stress_read));
   RAS_CUDA(c, cudaMemsetAsync(ver, 0, 4, c->stream));
   RAS_CUDA(c, cudaMemsetAsync(c->d_x, 0, (size_t)words * 8, c->stream));
   TRY(coll_barrier(c));  // the reader's window and counter are clear before the writer starts
-  unsigned long long* d_out = nullptr;
-  TRY(zalloc(c, &d_out, 4));
   if (c->rank == 0) {
     k_stress_write<<<1, 1024, 0, c->stream>>>((unsigned long long*)A->peer_x[1], words, epochs,
                                               A->peer_board[1] + 3 * c->plan->P);
@@ -1031,8 +1065,8 @@ ras_status put_stress(ras_ctx* c, int64_t epochs, int64_t words, int64_t* out4) 
   std::vector<unsigned long long> h(4, 0);
   RAS_CUDA(c, cudaMemcpyAsync(h.data(), d_out, 32, cudaMemcpyDeviceToHost, c->stream));
   RAS_CUDA(c, cudaStreamSynchronize(c->stream));
-  dfree(c, d_out);
   TRY(coll_barrier(c));
+  dfree(c, d_out);
   for (int i = 0; i < 4; ++i) out4[i] = (int64_t)h[i];
   return RAS_OK;
 }

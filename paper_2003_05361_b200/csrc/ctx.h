@@ -49,6 +49,11 @@ struct TriBuf {
   std::vector<int32_t> sub_c0, sub_nc, sub_lev_off, sub_nlev;
   int32_t* d_lev_done = nullptr;
   double bytes = 0.0;      // algorithmic bytes of one solve
+  // cluster-resident solve (k_trsv_cl): position-ordered ELL copy, only when every
+  // row has <= 4 dependencies
+  bool cl_ok = false;
+  TriCl cl{};
+  std::vector<int32_t> sub_max_lev;  // rows of the largest level per subdomain
 };
 
 struct KTimer {
@@ -131,6 +136,11 @@ struct ras_ctx {
   bool ic = false;
   double* d_z = nullptr;
   double* d_y = nullptr;    // forward-solve output of the sync-free trisolve
+  int trsv_cl_max = 0;      // largest usable cluster size of k_trsv_cl (16 with the non-portable opt-in, else 8)
+  int trsv_cl_force = 0;    // RAS_TRSV_CL: fixed cluster size (tests), 0 = sized to the widest level
+  std::vector<int> trsv_cl_fit;  // co-resident clusters of k_trsv_cl per cluster size (-1 = not queried)
+  int trsv_cl_nt = 512;    // RAS_TRSV_CL_NT: row-taking threads per CTA (tests)
+  int trsv_mode = 0;        // 0 = cluster-resident when usable (default), 1 = level barriers (k_trsv), 2 = sync-free
   bool trsv_sf = false;     // sync-free trisolve (k_trsv_sf, RAS_TRSV=sf); default k_trsv (level barriers)
   ras::TriBuf tri_f, tri_b;
   uint32_t* d_trsv_ctr = nullptr;  // [2][nl + 1] chunk counters (per subdomain + batched)

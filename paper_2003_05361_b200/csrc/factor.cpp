@@ -152,6 +152,12 @@ static void add_tri(const ras_plan* pl, int lp, const RowList& M, const std::vec
   T.sub_lev_off.push_back((int32_t)T.lev_nchunks.size());
   T.sub_nlev.push_back(nlev);
   T.sub_chunk_begin.push_back((int32_t)T.chunk.size());
+  T.sub_pos_off.push_back((int32_t)T.lev_pos.size());
+  int64_t maxlev = 0;
+  for (int32_t l = 0; l <= nlev; ++l) T.lev_pos.push_back((int32_t)(base + cnt[l]));
+  for (int32_t l = 0; l < nlev; ++l) maxlev = std::max<int64_t>(maxlev, cnt[l + 1] - cnt[l]);
+  T.sub_max_lev.push_back((int32_t)maxlev);
+  for (int64_t i = 0; i < n; ++i) T.max_deps = std::max<int32_t>(T.max_deps, (int32_t)(M.ptr[i + 1] - M.ptr[i]));
   for (int32_t l = 0; l < nlev; ++l) {
     int32_t nch = 0;
     for (int64_t a = cnt[l]; a < cnt[l + 1]; a += kChunk) {

@@ -716,6 +716,167 @@ static __global__ void __launch_bounds__(kThreads) k_trsv_sf(TriDev T, int use_b
   }
 }
 
+// Cluster-resident variant (r2, default when every row has <= 4 dependencies):
+// ONE thread-block cluster per subdomain walks that subdomain's levels, the
+// level's rows split over the cluster's CTAs (one row per thread, more rows
+// only when a level exceeds the cluster's threads).  Between levels the cluster
+// meets at the hardware cluster barrier (barrier.cluster arrive.release /
+// wait.acquire, ~0.2 us) instead of a level counter in L2 polled by one thread
+// per chunk.  The matrix is re-laid out by level-ordered position (row, divisor,
+// <= 4 dependency columns padded with -1 and their values: no rp indirection),
+// so every static operand of a row is one independent load; rows of levels l+1
+// and l+2 are fetched into registers while level l is solved and while the
+// cluster barrier is in flight.  The per-level critical path is the barrier
+// plus one L2 round trip for the dependencies' values.  Subdomains (clusters)
+// never wait on each other.  Same arithmetic and summation order as k_trsv.
+constexpr int kNT_TRC = 512;  // 128 registers: two levels x kTrcRPT rows prefetched
+struct TriCl {
+  const int32_t* lev_pos;      // per subdomain nlev + 1 positions
+  const int32_t* sub_pos_off;  // per subdomain offset into lev_pos
+  const int32_t* sub_nlev;
+  const int32_t* prow;         // per position: row-space row
+  const double* pdiv;          // per position: divisor
+  const int4* pcol;            // per position: dependency rows, -1 = none
+  const double2* pval;         // per position: 2 x (two dependency values)
+};
+struct TrcRow {
+  int32_t i;
+  int4 c;
+  double in, dv;
+  double2 v01, v23;
+};
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ int ld_rank0_shared(const int* p) {  // DSMEM read of CTA 0's copy
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  int v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(r) : "memory");
+  return v;
+}
+// static operands of a row (independent loads), then its input value (needs
+// the row index: issued one level later, when that index has long arrived)
+__device__ __forceinline__ void trc_fetch_static(const TriCl& T, int32_t k, int32_t kend, TrcRow& P) {
+  P.i = -1;
+  if (k < kend) {
+    P.i = __ldg(&T.prow[k]);
+    P.dv = __ldg(&T.pdiv[k]);
+    P.c = __ldg(&T.pcol[k]);
+    P.v01 = __ldg(&T.pval[2 * (int64_t)k]);
+    P.v23 = __ldg(&T.pval[2 * (int64_t)k + 1]);
+  }
+}
+__device__ __forceinline__ void trc_fetch_in(const double* __restrict__ in, TrcRow& P) {
+  if (P.i >= 0) P.in = __ldg(&in[P.i]);
+}
+__device__ __forceinline__ void trc_fetch(const TriCl& T, int32_t k, int32_t kend, const double* __restrict__ in,
+                                          TrcRow& P) {
+  trc_fetch_static(T, k, kend, P);
+  trc_fetch_in(in, P);
+}
+__device__ __forceinline__ void trc_solve(const TrcRow& P, double* out) {
+  if (P.i < 0) return;
+  // all dependency loads in flight before the first use (L2: written this launch)
+  const double o0 = P.c.x >= 0 ? __ldcg(&out[P.c.x]) : 0.0;
+  const double o1 = P.c.y >= 0 ? __ldcg(&out[P.c.y]) : 0.0;
+  const double o2 = P.c.z >= 0 ? __ldcg(&out[P.c.z]) : 0.0;
+  const double o3 = P.c.w >= 0 ? __ldcg(&out[P.c.w]) : 0.0;
+  double s = P.in;
+  if (P.c.x >= 0) s -= P.v01.x * o0;
+  if (P.c.y >= 0) s -= P.v01.y * o1;
+  if (P.c.z >= 0) s -= P.v23.x * o2;
+  if (P.c.w >= 0) s -= P.v23.y * o3;
+  __stcg(&out[P.i], s / P.dv);
+}
+// one level: the RPT prefetched rows (k0 + u * stride), then (levels wider than
+// the cluster's RPT rows per thread) the rest, fetched on the spot
+template <int RPT>
+__device__ __forceinline__ void trc_level(const TriCl& T, const TrcRow (&P)[RPT], int32_t k0, int32_t kend,
+                                          int32_t stride, const double* __restrict__ in, double* out) {
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) trc_solve(P[u], out);
+  for (int32_t k = k0 + RPT * stride; k < kend; k += stride) {
+    TrcRow Q;
+    trc_fetch(T, k, kend, in, Q);
+    trc_solve(Q, out);
+  }
+}
+template <int RPT>
+__device__ __forceinline__ void trc_fetch_level(const TriCl& T, int32_t k0, int32_t kend, int32_t stride,
+                                                TrcRow (&P)[RPT]) {
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) trc_fetch_static(T, k0 + u * stride, kend, P[u]);
+}
+template <int RPT>
+__device__ __forceinline__ void trc_fetch_level_in(const double* __restrict__ in, TrcRow (&P)[RPT]) {
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) trc_fetch_in(in, P[u]);
+}
+constexpr int kTrcRPT = 2;        // prefetched rows per thread and level
+constexpr int kTrcLevSmem = 4096;  // level positions staged in shared memory (more levels: k_trsv)
+static __global__ void __launch_bounds__(kNT_TRC, 1) k_trsv_cl(TriCl T, int32_t lp_base, int32_t ntu,
+                                                               const double* __restrict__ in, double* out,
+                                                               const int32_t* __restrict__ active, Ctl C) {
+  constexpr int RPT = kTrcRPT;
+  __shared__ int s_skip;
+  __shared__ int32_t s_lev[kTrcLevSmem];
+  pdl_start();
+  const int32_t ncl = (int32_t)cluster_size(), rank = (int32_t)cluster_rank();
+  const int lp = lp_base + (int)(blockIdx.x / ncl);
+  // the skip decision is CTA 0's, read by all over DSMEM (a stop flag may flip
+  // during the launch; the cluster must agree or its barriers would hang)
+  if (rank == 0 && threadIdx.x == 0) s_skip = (stopped(C, lp) || !active[lp]) ? 1 : 0;
+  const int32_t* glev = T.lev_pos + T.sub_pos_off[lp];
+  const int32_t nlev = T.sub_nlev[lp];
+  // level positions in shared memory: the cluster barrier's acquire invalidates
+  // L1 every level, shared memory stays
+  // (the host launches this kernel only when nlev < kTrcLevSmem)
+  for (int32_t l = threadIdx.x; l <= nlev; l += kNT_TRC) s_lev[l] = __ldg(&glev[l]);
+  cluster_arrive();
+  cluster_wait();
+  const int skip = ld_rank0_shared(&s_skip);
+  cluster_arrive();  // CTA 0 stays until every CTA has read its flag
+  cluster_wait();
+  if (skip) return;
+  const int32_t* lev = s_lev;
+  // ntu (<= kNT_TRC) threads per CTA take rows (a test knob; the rest only meet
+  // the barriers); thread t of CTA r takes rows lev[l] + (r * ntu + t) + u * stride
+  const int32_t stride = ncl * ntu, my = (int32_t)threadIdx.x < ntu ? rank * ntu + (int32_t)threadIdx.x : (1 << 30);
+  // software pipeline over levels, in the window between arrive and wait of
+  // level l's barrier: the input values of level l+1's rows, the static
+  // operands of level l+2's rows
+  TrcRow A[RPT], B[RPT];
+  trc_fetch_level<RPT>(T, lev[0] + my, lev[1], stride, A);
+  trc_fetch_level_in<RPT>(in, A);
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) B[u].i = -1;
+  if (nlev > 1) trc_fetch_level<RPT>(T, lev[1] + my, lev[2], stride, B);
+  for (int32_t l = 0; l < nlev; l += 2) {
+    trc_level<RPT>(T, A, lev[l] + my, lev[l + 1], stride, in, out);
+    cluster_arrive();
+    if (l + 1 < nlev) trc_fetch_level_in<RPT>(in, B);
+    if (l + 2 < nlev) trc_fetch_level<RPT>(T, lev[l + 2] + my, lev[l + 3], stride, A);
+    cluster_wait();
+    if (l + 1 < nlev) {
+      trc_level<RPT>(T, B, lev[l + 1] + my, lev[l + 2], stride, in, out);
+      cluster_arrive();
+      if (l + 2 < nlev) trc_fetch_level_in<RPT>(in, A);
+      if (l + 3 < nlev) trc_fetch_level<RPT>(T, lev[l + 3] + my, lev[l + 4], stride, B);
+      cluster_wait();
+    }
+  }
+}
+
 // fill with the sync-free trisolve's sentinel (setup, solve start)
 static __global__ void k_trsv_arm(int64_t n, double* a, double* b) {
   const double sent = __longlong_as_double((long long)kTrsvSent);

@@ -32,6 +32,10 @@ struct TriHost {
   std::vector<int32_t> sub_chunk_begin, sub_chunk_end;  // per subdomain (contiguous, level order)
   std::vector<int32_t> sub_lev_off, sub_nlev;           // per subdomain: offset into lev_nchunks
   std::vector<int32_t> lev_nchunks;                     // chunks per (subdomain, level)
+  std::vector<int32_t> lev_pos;      // per subdomain: nlev + 1 level-ordered positions (level l = [pos[l], pos[l+1]))
+  std::vector<int32_t> sub_pos_off;  // per subdomain: offset into lev_pos (= sub_lev_off + subdomain)
+  std::vector<int32_t> sub_max_lev;  // per subdomain: rows of its largest level
+  int32_t max_deps = 0;              // most dependencies of any row (ELL width of the cluster solve)
   int64_t max_levels = 0;
 };
 

@@ -486,6 +486,32 @@ static ras_status upload_tri(ras_ctx* c, const TriHost& H, TriBuf& B) {
   B.sub_nc.resize(H.sub_chunk_begin.size());
   for (size_t i = 0; i < B.sub_nc.size(); ++i) B.sub_nc[i] = H.sub_chunk_end[i] - H.sub_chunk_begin[i];
   TRY(zalloc(c, &B.d_lev_done, (size_t)std::max(B.nlev_slots, 1)));
+  B.sub_max_lev = H.sub_max_lev;
+  B.cl_ok = H.max_deps <= 4 && H.max_levels < kTrcLevSmem;  // k_trsv_cl: <= 4 deps / row, levels staged in smem
+  if (B.cl_ok) {  // k_trsv_cl: the factor re-laid out by level-ordered position
+    const size_t np = H.rows.size();
+    std::vector<double> pdiv(np), pval(4 * np, 0.0);
+    std::vector<int4> pcol(np);
+    for (size_t k = 0; k < np; ++k) {
+      pdiv[k] = H.diag[H.rows[k]];
+      int32_t cc[4] = {-1, -1, -1, -1};
+      for (int32_t e = H.rp[k], q = 0; e < H.rp[k + 1]; ++e, ++q) {
+        cc[q] = H.col[e];
+        pval[4 * k + q] = H.val[e];
+      }
+      pcol[k] = make_int4(cc[0], cc[1], cc[2], cc[3]);
+    }
+    int32_t *lp, *spo, *snl;
+    double *dv, *pv;
+    int4* pc;
+    TRY(upload(c, &lp, H.lev_pos, 1));
+    TRY(upload(c, &spo, H.sub_pos_off, 1));
+    TRY(upload(c, &snl, H.sub_nlev, 1));
+    TRY(upload(c, &dv, pdiv, 1));
+    TRY(upload(c, &pc, pcol, 1));
+    TRY(upload(c, &pv, pval, 2));
+    B.cl = TriCl{lp, spo, snl, rows, dv, pc, (const double2*)pv};
+  }
   // algorithmic bytes of one solve: per real row rows/rp/in/out/diag, per entry val+col
   B.bytes = (double)pl->rows_local * (4 + 4 + 8 + 8 + 8) + (double)(pl->nnz_local - pl->rows_local) / 2.0 * 12.0;
   return RAS_OK;
@@ -508,6 +534,30 @@ static ras_status upload_factors(ras_ctx* c) {
     // barriers on B200: profiles/r02_trsv.md), default the level-barrier kernel
     const char* e = getenv("RAS_TRSV");
     c->trsv_sf = e && std::strcmp(e, "sf") == 0;
+    c->trsv_mode = c->trsv_sf ? 2 : (e && std::strcmp(e, "level") == 0) ? 1 : 0;
+  }
+  if (c->trsv_mode == 0 && c->tri_f.cl_ok && c->tri_b.cl_ok) {
+    // cluster-resident solve: 16-CTA clusters with the non-portable opt-in when the
+    // device can hold one, else the portable 8
+    RAS_CUDA(c, cudaFuncSetAttribute(k_trsv_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    c->trsv_cl_max = 8;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(kNT_TRC);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_trsv_cl, &cfg) == cudaSuccess && ncl > 0) c->trsv_cl_max = 16;
+    cudaGetLastError();
+    const char* f = getenv("RAS_TRSV_CL");
+    const char* t = getenv("RAS_TRSV_CL_NT");
+    c->trsv_cl_force = f ? std::max(1, std::min(c->trsv_cl_max, atoi(f))) : 0;
+    c->trsv_cl_nt = t ? std::max(32, std::min(kNT_TRC, atoi(t))) : kNT_TRC;
   }
   if (c->trsv_sf) {  // arm y and z with the sentinel (the solves re-arm each other afterwards)
     k_trsv_arm<<<148 * 4, 256, 0, c->stream>>>(c->rows_pad, c->d_y, c->d_z);
@@ -900,6 +950,47 @@ static void pdl_launch(cudaStream_t s, unsigned grid, unsigned block, Kern k, Ar
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k, args...);
 }
+// clusters of k_trsv_cl of size k that fit the device at once (cached per k)
+static int trsv_cl_fit(ras_ctx* c, int k) {
+  if (c->trsv_cl_fit.empty()) c->trsv_cl_fit.assign(17, -1);
+  if (c->trsv_cl_fit[k] < 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)k);
+    cfg.blockDim = dim3(kNT_TRC);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)k;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_trsv_cl, &cfg) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    c->trsv_cl_fit[k] = n;
+    if (getenv("RAS_TRSV_DEBUG")) fprintf(stderr, "k_trsv_cl: %d co-resident clusters of %d CTAs\n", n, k);
+  }
+  return c->trsv_cl_fit[k];
+}
+
+// k_trsv_cl: cluster launch (+ PDL)
+static void cl_launch(cudaStream_t s, unsigned grid, unsigned ncl, TriCl T, int32_t lp_base, int32_t ntu,
+                      const double* in, double* out, const int32_t* active, Ctl C) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kNT_TRC);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = ncl;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, k_trsv_cl, T, lp_base, ntu, in, out, active, C);
+}
 #define KL(strm, kind, grid, block, KERNEL, ...) LAUNCH_ON(strm, kind, pdl_launch(strm, grid, block, KERNEL, __VA_ARGS__))
 
 // ---------------------------------------------------------------------------
@@ -1014,6 +1105,30 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
       const unsigned g = (unsigned)std::max(1, std::min(nch, sf_grid));
       KL(s, K_TRSV, g, kThreads, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
          (const int32_t*)c->S.active, C);
+      continue;
+    }
+    if (c->trsv_cl_max > 0) {
+      // cluster-resident: one cluster per subdomain, sized to the widest level
+      const int l0 = R.lp < 0 ? 0 : R.lp, nsub = R.lp < 0 ? c->nl : 1;
+      int32_t wide = 1;
+      for (int lp = l0; lp < l0 + nsub; ++lp) wide = std::max(wide, T.sub_max_lev[lp]);
+      // one row per thread where the widest level allows (up to kTrcRPT are
+      // prefetched, more are fetched on the spot), shrunk until all nsub clusters
+      // fit the GPU at once (no second wave of clusters)
+      int ncl = c->trsv_cl_force;
+      if (!ncl) {
+        const int want = std::min(c->trsv_cl_max, (int)((wide + c->trsv_cl_nt - 1) / c->trsv_cl_nt));
+        ncl = want;
+        for (int k = want; k >= 1; --k)
+          if (trsv_cl_fit(c, k) >= nsub) {
+            ncl = k;
+            break;
+          }
+      }
+      const double* src = dir == 0 ? in : c->d_q;
+      double* dst = dir == 0 ? c->d_q : z;
+      LAUNCH_ON(s, K_TRSV, cl_launch(s, (unsigned)(nsub * ncl), (unsigned)ncl, T.cl, (int32_t)l0, (int32_t)c->trsv_cl_nt, src, dst,
+                                     (const int32_t*)c->S.active, C));
       continue;
     }
     if (R.lp < 0) {

@@ -4,6 +4,8 @@ The oracle factors A_p with the textbook IC(0) recurrence / IKJ ILU(0) and
 applies M^-1 with scipy triangular solves; the GPU factors on the host in
 independent C++ and solves with level-scheduled chunked kernels.  Sync
 iterates must agree to 1e-10 (FP64)."""
+import functools
+
 import numpy as np
 import pytest
 
@@ -59,9 +61,16 @@ def test_ic0_converges_sync_and_async():
     s.close()
 
 
-@pytest.mark.parametrize("kind", ["ic0", "ilu0"])
-@pytest.mark.parametrize("case", ["3d", "2d"])
-def test_ic_multi_chunk_levels_match_oracle(kind, case):
+# trisolve kernels: the cluster-resident default (one cluster per subdomain, sized
+# to the widest level), the same forced to 4-CTA clusters of 128 row threads
+# (levels spread over CTAs + several rows per thread), one CTA of 64 row threads
+# (levels 14x wider than the CTA), and the level-barrier kernel k_trsv
+TRSV = {"cl": {}, "cl4x128": {"RAS_TRSV_CL": "4", "RAS_TRSV_CL_NT": "128"},
+        "cl1x64": {"RAS_TRSV_CL": "1", "RAS_TRSV_CL_NT": "64"}, "level": {"RAS_TRSV": "level"}}
+
+
+@functools.lru_cache(maxsize=None)
+def _multi_chunk_case(kind, case):
     # levels wider than one 256-row chunk of k_trsv: the level-wait across >= 2
     # chunks per level (P320-323 level-set solves).  3D 64^3 in 2x2x2 with
     # overlap 2: 34^3-row subdomains whose widest level has ~870 rows (4 chunks);
@@ -83,8 +92,18 @@ def test_ic_multi_chunk_levels_match_oracle(kind, case):
     widest = np.bincount(O.level_sets(L0, lower=True)).max()
     assert widest > 256, widest
     ref = O.ras_sync(A, b, subs, 1e-300, K, record_iterates=True)
+    return A, b, owner, gamma, m, K, ref
+
+
+@pytest.mark.parametrize("trsv", list(TRSV))
+@pytest.mark.parametrize("kind", ["ic0", "ilu0"])
+@pytest.mark.parametrize("case", ["3d", "2d"])
+def test_ic_multi_chunk_levels_match_oracle(kind, case, trsv, monkeypatch):
+    for k, v in TRSV[trsv].items():
+        monkeypatch.setenv(k, v)
+    A, b, owner, gamma, m, K, ref = _multi_chunk_case(kind, case)
     s = R.Solver(A, b, owner, gamma, R.options(kind, m))
     for k in (1, K):
         st, x = s.solve(1e-300, k, "sync")
-        assert rel(x, ref.iterates[k]) <= 1e-10, (kind, case, k, rel(x, ref.iterates[k]))
+        assert rel(x, ref.iterates[k]) <= 1e-10, (kind, case, trsv, k, rel(x, ref.iterates[k]))
     s.close()

@@ -1,3 +1,6 @@
+"""R33 evidence, step 1 (R33, profiles/r02_r33_investigation.md): 256^2 Laplacian,
+16 strips, overlap 4, async to 1e-8 -- the persistent kernel vs the stream driver with fixed-m
+Jacobi-PCG (m = 5, 20, 60) and with exact local solves, and the sync sweep count beside them."""
 import os, sys, json
 sys.path.insert(0, os.getcwd())
 import numpy as np
