@@ -54,6 +54,10 @@ struct TriBuf {
   bool cl_ok = false;
   TriCl cl{};
   std::vector<int32_t> sub_max_lev;  // rows of the largest level per subdomain
+  // DSMEM-routed solve (k_trsv_ds): routing tables for cluster size ds_ncl
+  bool ds_ok = false;
+  int ds_ncl = 0;
+  TriDs ds{};
 };
 
 struct KTimer {
@@ -140,6 +144,7 @@ struct ras_ctx {
   int trsv_cl_force = 0;    // RAS_TRSV_CL: fixed cluster size (tests), 0 = sized to the widest level
   std::vector<int> trsv_cl_fit;  // co-resident clusters of k_trsv_cl per cluster size (-1 = not queried)
   int trsv_cl_nt = 512;    // RAS_TRSV_CL_NT: row-taking threads per CTA (tests)
+  bool trsv_ds = false;     // DSMEM-routed solves (k_trsv_ds) for both factors
   int trsv_mode = 0;        // 0 = cluster-resident when usable (default), 1 = level barriers (k_trsv), 2 = sync-free
   bool trsv_sf = false;     // sync-free trisolve (k_trsv_sf, RAS_TRSV=sf); default k_trsv (level barriers)
   ras::TriBuf tri_f, tri_b;

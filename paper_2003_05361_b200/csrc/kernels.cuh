@@ -877,6 +877,196 @@ static __global__ void __launch_bounds__(kNT_TRC, 1) k_trsv_cl(TriCl T, int32_t 
   }
 }
 
+// DSMEM-routed variant (r2, default where it applies): the same cluster-per-
+// subdomain level walk, but a row's dependencies never travel through global
+// memory.  When row d (level l-1) is solved, its value is pushed straight into
+// the shared memory of each CTA that consumes it (st.async.shared::cluster,
+// completing bytes on that CTA's mbarrier); a CTA starts level l once its
+// mbarrier has counted all the bytes its level-l rows need.  The cluster still
+// meets once per level, but at a RELAXED barrier (no release fence: ~70 ns, and
+// no wait for the prefetch loads in flight, which a release's MEMBAR.ALL.GPU
+// would wait for -- profiles/r02_trsv_cl_summary.md); it only bounds the skew
+// between CTAs to one level, which makes the double-buffered receive slots and
+// the mbarrier phases safe.  Applies when every dependency of a level-l row is
+// in level l-1 (stencil factors in natural order), a row has <= 4 dependencies
+// and <= 4 consumers, and a CTA holds <= kTrdRows rows per thread of a level;
+// the routing (consumer CTA, receive slot) is precomputed for a fixed cluster
+// size (setup, solver.cu).  Receive slot of dependency q of the row with local
+// index j in its CTA's block of the level: j * 4 + q.  Same products in the same
+// order as k_trsv: bitwise the same result.
+constexpr int kNT_TRD = 512;
+constexpr int kTrdRows = 3;                       // rows per thread and level (2 prefetched)
+constexpr int kTrdSlots = 4 * kTrdRows * kNT_TRD;  // receive slots per parity
+struct TriDs {
+  const int32_t* lev_pos;      // per subdomain nlev + 1 positions
+  const int32_t* sub_pos_off;  // per subdomain offset into lev_pos
+  const int32_t* sub_nlev;
+  const int32_t* rb_off;       // per subdomain offset into rbytes
+  const int32_t* rbytes;       // per (subdomain, level, CTA): bytes of dependency values the CTA receives
+  const int32_t* prow;         // per position: row | ndeps << 29
+  const double* pdiv;          // per position: divisor
+  const double2* pval;         // per position: 2 x (two dependency values)
+  const int4* psend;           // per position: consumers (CTA << 16 | receive slot), -1 = none
+};
+struct TrdRow {
+  uint32_t pr;  // row | ndeps << 29, ~0u = none; decoded only where used (no ALU on a load in flight)
+  int4 snd;
+  double in, dv;
+  double2 v01, v23;
+};
+constexpr uint32_t kTrdNone = 0xffffffffu;
+__device__ __forceinline__ void trd_fetch_static(const TriDs& T, int32_t k, bool ok, TrdRow& P) {
+  P.pr = kTrdNone;
+  if (ok) {  // predicated loads: the prefetch window issues them and moves on
+    P.pr = (uint32_t)__ldg(&T.prow[k]);
+    P.dv = __ldg(&T.pdiv[k]);
+    P.snd = __ldg(&T.psend[k]);
+    P.v01 = __ldg(&T.pval[2 * (int64_t)k]);
+    P.v23 = __ldg(&T.pval[2 * (int64_t)k + 1]);
+  }
+}
+__device__ __forceinline__ void trd_fetch_in(const double* __restrict__ in, TrdRow& P) {
+  if (P.pr != kTrdNone) P.in = __ldg(&in[P.pr & 0x1fffffffu]);
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(mb)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mb);
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+// push v into slot `e & 0xffff` of CTA `e >> 16`'s receive area (rcv_next: this
+// CTA's address of that area), completing 8 bytes on its mbarrier mb_next
+__device__ __forceinline__ void trd_send(int32_t e, double v, uint32_t rcv_next, uint32_t mb_next) {
+  if (e < 0) return;
+  const uint32_t cta = (uint32_t)e >> 16, slot = (uint32_t)e & 0xffffu;
+  uint32_t ra, rm;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(rcv_next + 8u * slot), "r"(cta));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rm) : "r"(mb_next), "r"(cta));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
+               "l"(__double_as_longlong(v)), "r"(rm)
+               : "memory");
+}
+__device__ __forceinline__ void trd_solve(const TrdRow& P, const double* rcv_j, double* out, uint32_t rcv_next,
+                                          uint32_t mb_next) {
+  if (P.pr == kTrdNone) return;
+  const uint32_t nd = P.pr >> 29;
+  double s = P.in;
+  if (nd > 0) s -= P.v01.x * rcv_j[0];
+  if (nd > 1) s -= P.v01.y * rcv_j[1];
+  if (nd > 2) s -= P.v23.x * rcv_j[2];
+  if (nd > 3) s -= P.v23.y * rcv_j[3];
+  const double o = s / P.dv;
+  trd_send(P.snd.x, o, rcv_next, mb_next);
+  trd_send(P.snd.y, o, rcv_next, mb_next);
+  trd_send(P.snd.z, o, rcv_next, mb_next);
+  trd_send(P.snd.w, o, rcv_next, mb_next);
+  out[P.pr & 0x1fffffffu] = o;  // the result (read by the next kernel)
+}
+static __global__ void __launch_bounds__(kNT_TRD, 1) k_trsv_ds(TriDs T, int32_t lp_base, const double* __restrict__ in,
+                                                               double* out, const int32_t* __restrict__ active, Ctl C) {
+  extern __shared__ double rcv[];  // [2][kTrdSlots]
+  __shared__ uint64_t mbar[2];
+  __shared__ int s_skip;
+  __shared__ int2 s_blk[kTrcLevSmem];  // per level: this CTA's block [k0, kend) of positions
+  pdl_start();
+  const int32_t ncl = (int32_t)cluster_size(), rank = (int32_t)cluster_rank();
+  const int lp = lp_base + (int)(blockIdx.x / ncl);
+  const int32_t t = (int32_t)threadIdx.x;
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&mbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (rank == 0) s_skip = (stopped(C, lp) || !active[lp]) ? 1 : 0;
+  }
+  const int32_t* glev = T.lev_pos + T.sub_pos_off[lp];
+  const int32_t nlev = T.sub_nlev[lp];
+  // level l: CTA r's block = positions b + r q + [0, q), q = ceil(n_l / ncl); row j
+  // of the block is thread j % NT's row u = j / NT
+  for (int32_t l = t; l < nlev; l += kNT_TRD) {
+    const int32_t b = __ldg(&glev[l]), e = __ldg(&glev[l + 1]), q = (e - b + ncl - 1) / ncl;
+    s_blk[l] = make_int2(b + rank * q, min(e, b + (rank + 1) * q));
+  }
+  cluster_arrive();
+  cluster_wait();
+  const int skip = ld_rank0_shared(&s_skip);
+  const int32_t* rb = T.rbytes + T.rb_off[lp];  // [level][ncl]
+  if (!skip && t == 0) {  // levels 1 and 2 armed; level l + 2 re-armed after level l
+    if (nlev > 1) mbar_arm(&mbar[1], (uint32_t)__ldg(&rb[1 * ncl + rank]));
+    if (nlev > 2) mbar_arm(&mbar[0], (uint32_t)__ldg(&rb[2 * ncl + rank]));
+  }
+  cluster_arrive();  // CTA 0 stays until every CTA has read its flag; every mbarrier initialised
+  cluster_wait();
+  if (skip) return;
+  const uint32_t rcv_s = (uint32_t)__cvta_generic_to_shared(rcv);
+  const uint32_t mb_s[2] = {(uint32_t)__cvta_generic_to_shared(&mbar[0]), (uint32_t)__cvta_generic_to_shared(&mbar[1])};
+  auto blk = [&](int32_t l, int32_t& k0, int32_t& kend) {
+    const int2 bk = s_blk[l];
+    k0 = bk.x;
+    kend = bk.y;
+  };
+  auto fetch = [&](int32_t l, TrdRow(&P)[2]) {
+    int32_t k0, ke;
+    blk(l, k0, ke);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) trd_fetch_static(T, k0 + u * kNT_TRD + t, k0 + u * kNT_TRD + t < ke, P[u]);
+  };
+  auto fetch_in = [&](TrdRow(&P)[2]) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) trd_fetch_in(in, P[u]);
+  };
+  auto level = [&](int32_t l, const TrdRow(&P)[2]) {
+    const int par = l & 1;
+    if (l > 0) mbar_wait(&mbar[par], (uint32_t)(((l - 1) >> 1) & 1));  // phase of level l on mbar[l & 1]
+    const double* rc = rcv + par * kTrdSlots;
+    const uint32_t rn = rcv_s + 8u * (uint32_t)((par ^ 1) * kTrdSlots), mn = mb_s[par ^ 1];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) trd_solve(P[u], rc + 4 * (u * kNT_TRD + t), out, rn, mn);
+    int32_t k0, ke;
+    blk(l, k0, ke);
+    for (int u = 2; u < kTrdRows; ++u) {  // a third row of a wide level, fetched on the spot
+      TrdRow Q;
+      trd_fetch_static(T, k0 + u * kNT_TRD + t, k0 + u * kNT_TRD + t < ke, Q);
+      trd_fetch_in(in, Q);
+      trd_solve(Q, rc + 4 * (u * kNT_TRD + t), out, rn, mn);
+    }
+  };
+  auto rearm = [&](int32_t l) {  // after the barrier that ended level l - 2 (its phase is over): arm level l
+    if (t == 0 && l < nlev) mbar_arm(&mbar[l & 1], (uint32_t)__ldg(&rb[l * ncl + rank]));
+  };
+  TrdRow A[2], B[2];
+  fetch(0, A);
+  fetch_in(A);
+  B[0].pr = B[1].pr = kTrdNone;
+  if (nlev > 1) fetch(1, B);
+  for (int32_t l = 0; l < nlev; l += 2) {
+    level(l, A);
+    if (l + 1 < nlev) fetch_in(B);
+    if (l + 2 < nlev) fetch(l + 2, A);
+    cluster_sync_relaxed();
+    if (l >= 2) rearm(l + 2);  // levels 1 and 2 were armed at the start
+    if (l + 1 < nlev) {
+      level(l + 1, B);
+      if (l + 2 < nlev) fetch_in(A);
+      if (l + 3 < nlev) fetch(l + 3, B);
+      cluster_sync_relaxed();
+      rearm(l + 3);
+    }
+  }
+  cluster_sync_relaxed();  // no CTA leaves while a peer's st.async may still target it
+}
+
 // fill with the sync-free trisolve's sentinel (setup, solve start)
 static __global__ void k_trsv_arm(int64_t n, double* a, double* b) {
   const double sent = __longlong_as_double((long long)kTrsvSent);

@@ -517,6 +517,86 @@ static ras_status upload_tri(ras_ctx* c, const TriHost& H, TriBuf& B) {
   return RAS_OK;
 }
 
+// k_trsv_ds routing tables of one factor for cluster size ncl (DSMEM-routed
+// solve, kernels.cuh): false if the factor does not qualify (a dependency outside
+// the previous level, > 4 dependencies or consumers, a level wider than
+// kTrdRows rows per thread of the cluster)
+static bool build_ds(ras_ctx* c, const TriHost& H, int ncl, TriBuf& B, ras_status* st) {
+  *st = RAS_OK;
+  const size_t np = H.rows.size();
+  const int nl = (int)H.sub_nlev.size();
+  std::vector<int32_t> pos_of_row((size_t)c->rows_pad, -1), lev_of(np, -1), prow(np), rb_off(nl + 1, 0), rbytes;
+  std::vector<int4> psend(np, make_int4(-1, -1, -1, -1));
+  for (size_t k = 0; k < np; ++k) {
+    if (H.rows[k] >= (1 << 29)) return false;
+    pos_of_row[H.rows[k]] = (int32_t)k;
+  }
+  for (int lp = 0; lp < nl; ++lp) {
+    const int32_t* lev = H.lev_pos.data() + H.sub_pos_off[lp];
+    const int nlev = H.sub_nlev[lp];
+    rb_off[lp] = (int32_t)rbytes.size();
+    rbytes.resize(rbytes.size() + (size_t)nlev * ncl, 0);
+    for (int l = 0; l < nlev; ++l)
+      for (int32_t k = lev[l]; k < lev[l + 1]; ++k) lev_of[k] = l;
+    for (int l = 0; l < nlev; ++l) {
+      const int32_t b = lev[l], n = lev[l + 1] - b, q = (n + ncl - 1) / ncl;
+      if (q > kTrdRows * kNT_TRD) return false;
+      for (int32_t k = b; k < lev[l + 1]; ++k) {
+        const int32_t r = (k - b) / q, j = (k - b) % q, nd = H.rp[k + 1] - H.rp[k];
+        if (nd > 4) return false;
+        prow[k] = H.rows[k] | (nd << 29);
+        rbytes[rb_off[lp] + (size_t)l * ncl + r] += 8 * nd;
+        for (int32_t qd = 0; qd < nd; ++qd) {
+          const int32_t d = pos_of_row[H.col[H.rp[k] + qd]];
+          if (d < 0 || lev_of[d] != l - 1) return false;
+          int32_t* sd = &psend[d].x;
+          int w = 0;
+          while (w < 4 && sd[w] >= 0) ++w;
+          if (w == 4) return false;
+          sd[w] = (r << 16) | (j * 4 + qd);
+        }
+      }
+    }
+  }
+  rb_off[nl] = (int32_t)rbytes.size();
+  std::vector<double> pdiv(np), pval(4 * np, 0.0);
+  for (size_t k = 0; k < np; ++k) {
+    pdiv[k] = H.diag[H.rows[k]];
+    for (int32_t e = H.rp[k], qd = 0; e < H.rp[k + 1]; ++e, ++qd) pval[4 * k + qd] = H.val[e];
+  }
+  int32_t *dlp, *dspo, *dsnl, *drbo, *drb, *dpr;
+  double *ddv, *dpv;
+  int4* dps;
+  if ((*st = upload(c, &dlp, H.lev_pos, 1)) || (*st = upload(c, &dspo, H.sub_pos_off, 1)) ||
+      (*st = upload(c, &dsnl, H.sub_nlev, 1)) || (*st = upload(c, &drbo, rb_off, 1)) || (*st = upload(c, &drb, rbytes, 1)) ||
+      (*st = upload(c, &dpr, prow, 1)) || (*st = upload(c, &ddv, pdiv, 1)) || (*st = upload(c, &dpv, pval, 2)) ||
+      (*st = upload(c, &dps, psend, 1)))
+    return false;
+  B.ds = TriDs{dlp, dspo, dsnl, drbo, drb, dpr, ddv, (const double2*)dpv, dps};
+  B.ds_ok = true;
+  B.ds_ncl = ncl;
+  return true;
+}
+
+static int trsv_ds_fit(ras_ctx* c, int k) {  // co-resident k_trsv_ds clusters of k CTAs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)k);
+  cfg.blockDim = dim3(kNT_TRD);
+  cfg.dynamicSmemBytes = (size_t)2 * kTrdSlots * sizeof(double);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)k;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_trsv_ds, &cfg) != cudaSuccess) n = 0;
+  cudaGetLastError();
+  if (getenv("RAS_TRSV_DEBUG")) fprintf(stderr, "k_trsv_ds: %d co-resident clusters of %d CTAs\n", n, k);
+  return n;
+}
+
 static ras_status upload_factors(ras_ctx* c) {
   TriHost F, B;
   try {
@@ -558,6 +638,34 @@ static ras_status upload_factors(ras_ctx* c) {
     const char* t = getenv("RAS_TRSV_CL_NT");
     c->trsv_cl_force = f ? std::max(1, std::min(c->trsv_cl_max, atoi(f))) : 0;
     c->trsv_cl_nt = t ? std::max(32, std::min(kNT_TRC, atoi(t))) : kNT_TRC;
+    // DSMEM-routed solve where both factors qualify: one cluster size for every
+    // launch (the routing depends on it): one row per thread where the widest level
+    // allows, shrunk until all local subdomains' clusters are co-resident
+    // (RAS_TRSV_DS_CL forces a size; RAS_TRSV=cl keeps k_trsv_cl)
+    const char* fd = getenv("RAS_TRSV_DS_CL");
+    const char* e = getenv("RAS_TRSV");
+    if (!(e && std::strcmp(e, "cl") == 0)) {
+      RAS_CUDA(c, cudaFuncSetAttribute(k_trsv_ds, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      RAS_CUDA(c, cudaFuncSetAttribute(k_trsv_ds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(2 * kTrdSlots * sizeof(double))));
+      int32_t wide = 1;
+      for (int32_t w : c->tri_f.sub_max_lev) wide = std::max(wide, w);
+      for (int32_t w : c->tri_b.sub_max_lev) wide = std::max(wide, w);
+      const int lo = (int)((wide + kTrdRows * kNT_TRD - 1) / (kTrdRows * kNT_TRD));
+      const int want = std::min(c->trsv_cl_max, (int)((wide + kNT_TRD - 1) / kNT_TRD));
+      int ncl = fd ? std::max(1, std::min(c->trsv_cl_max, atoi(fd))) : lo;
+      if (!fd)
+        for (int k = want; k >= lo; --k)
+          if (trsv_ds_fit(c, k) >= c->nl) {
+            ncl = k;
+            break;
+          }
+      ras_status st = RAS_OK;
+      if (lo <= c->trsv_cl_max && build_ds(c, F, ncl, c->tri_f, &st) && build_ds(c, B, ncl, c->tri_b, &st))
+        c->trsv_ds = true;
+      if (st != RAS_OK) return st;
+      if (getenv("RAS_TRSV_DEBUG")) fprintf(stderr, "k_trsv_ds: %s, cluster %d\n", c->trsv_ds ? "on" : "off", ncl);
+    }
   }
   if (c->trsv_sf) {  // arm y and z with the sentinel (the solves re-arm each other afterwards)
     k_trsv_arm<<<148 * 4, 256, 0, c->stream>>>(c->rows_pad, c->d_y, c->d_z);
@@ -973,6 +1081,26 @@ static int trsv_cl_fit(ras_ctx* c, int k) {
   return c->trsv_cl_fit[k];
 }
 
+// k_trsv_ds: cluster launch (+ PDL), receive slots in dynamic shared memory
+static void ds_launch(cudaStream_t s, unsigned grid, unsigned ncl, TriDs T, int32_t lp_base, const double* in,
+                      double* out, const int32_t* active, Ctl C) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kNT_TRD);
+  cfg.dynamicSmemBytes = (size_t)2 * kTrdSlots * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = ncl;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, k_trsv_ds, T, lp_base, in, out, active, C);
+}
+
 // k_trsv_cl: cluster launch (+ PDL)
 static void cl_launch(cudaStream_t s, unsigned grid, unsigned ncl, TriCl T, int32_t lp_base, int32_t ntu,
                       const double* in, double* out, const int32_t* active, Ctl C) {
@@ -1105,6 +1233,15 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
       const unsigned g = (unsigned)std::max(1, std::min(nch, sf_grid));
       KL(s, K_TRSV, g, kThreads, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
          (const int32_t*)c->S.active, C);
+      continue;
+    }
+    if (c->trsv_ds) {
+      // DSMEM-routed: one cluster of the routing's size per subdomain
+      const int l0 = R.lp < 0 ? 0 : R.lp, nsub = R.lp < 0 ? c->nl : 1, ncl = T.ds_ncl;
+      const double* src = dir == 0 ? in : c->d_q;
+      double* dst = dir == 0 ? c->d_q : z;
+      LAUNCH_ON(s, K_TRSV, ds_launch(s, (unsigned)(nsub * ncl), (unsigned)ncl, T.ds, (int32_t)l0, src, dst,
+                                     (const int32_t*)c->S.active, C));
       continue;
     }
     if (c->trsv_cl_max > 0) {

@@ -61,12 +61,15 @@ def test_ic0_converges_sync_and_async():
     s.close()
 
 
-# trisolve kernels: the cluster-resident default (one cluster per subdomain, sized
-# to the widest level), the same forced to 4-CTA clusters of 128 row threads
-# (levels spread over CTAs + several rows per thread), one CTA of 64 row threads
-# (levels 14x wider than the CTA), and the level-barrier kernel k_trsv
-TRSV = {"cl": {}, "cl4x128": {"RAS_TRSV_CL": "4", "RAS_TRSV_CL_NT": "128"},
-        "cl1x64": {"RAS_TRSV_CL": "1", "RAS_TRSV_CL_NT": "64"}, "level": {"RAS_TRSV": "level"}}
+# trisolve kernels: the DSMEM-routed default k_trsv_ds (one cluster per
+# subdomain, dependencies pushed into the consumers' shared memory), the same
+# with 2-CTA clusters (routing across CTAs), the cluster-resident k_trsv_cl (own
+# cluster sizing; forced to 4-CTA clusters of 128 row threads = levels spread
+# over CTAs + several rows per thread; one CTA of 64 row threads = levels 14x
+# wider than the CTA), and the level-barrier kernel k_trsv
+TRSV = {"ds": {}, "ds2": {"RAS_TRSV_DS_CL": "2"}, "cl": {"RAS_TRSV": "cl"},
+        "cl4x128": {"RAS_TRSV": "cl", "RAS_TRSV_CL": "4", "RAS_TRSV_CL_NT": "128"},
+        "cl1x64": {"RAS_TRSV": "cl", "RAS_TRSV_CL": "1", "RAS_TRSV_CL_NT": "64"}, "level": {"RAS_TRSV": "level"}}
 
 
 @functools.lru_cache(maxsize=None)
@@ -98,11 +101,15 @@ def _multi_chunk_case(kind, case):
 @pytest.mark.parametrize("trsv", list(TRSV))
 @pytest.mark.parametrize("kind", ["ic0", "ilu0"])
 @pytest.mark.parametrize("case", ["3d", "2d"])
-def test_ic_multi_chunk_levels_match_oracle(kind, case, trsv, monkeypatch):
+def test_ic_multi_chunk_levels_match_oracle(kind, case, trsv, monkeypatch, capfd):
     for k, v in TRSV[trsv].items():
         monkeypatch.setenv(k, v)
+    monkeypatch.setenv("RAS_TRSV_DEBUG", "1")
     A, b, owner, gamma, m, K, ref = _multi_chunk_case(kind, case)
     s = R.Solver(A, b, owner, gamma, R.options(kind, m))
+    err = capfd.readouterr().err
+    if trsv.startswith("ds"):  # the routed kernel really runs (stencil factors qualify)
+        assert "k_trsv_ds: on, cluster " + ("2" if trsv == "ds2" else "") in err, err
     for k in (1, K):
         st, x = s.solve(1e-300, k, "sync")
         assert rel(x, ref.iterates[k]) <= 1e-10, (kind, case, trsv, k, rel(x, ref.iterates[k]))

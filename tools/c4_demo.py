@@ -45,7 +45,7 @@ def main():
     print(json.dumps({"experiment": "c4_demo", "grid": [N, N, N], "unknowns": N ** 3, "subdomains": 8, "overlap": 4,
                       "local_solver": f"{a.solver}-PCG m=10", "inputs_s": t1 - t0, "setup_s": t2 - t1,
                       "ms_per_sweep": tot / a.sweeps, "pcg_path": st["pcg_path"],
-                      "trsv": os.environ.get("RAS_TRSV", "cl"), "levels_per_solve": levels,
+                      "trsv": os.environ.get("RAS_TRSV", "ds"), "levels_per_solve": levels,
                       "us_per_level": (1e3 * kt["k_trsv"][1] / kt["k_trsv"][0] / levels) if kt.get("k_trsv", (0,))[0] else None,
                       "kernels": {k: {"launches": v[0], "ms_per_sweep": v[1] / a.sweeps, "share": v[1] / tot}
                                   for k, v in kt.items() if v[0]}}), flush=True)
