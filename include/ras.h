@@ -61,10 +61,13 @@ typedef enum { RAS_SYNC = 0, RAS_ASYNC = 1 } ras_mode;
 typedef enum {
   RAS_LS_JACOBI_PCG = 0, /* PCG, M = diag(A_p), fixed m iterations (P313-315; R6, R8) */
   RAS_LS_IC0_PCG = 1,    /* PCG, M = L L^T, IC(0) of A_p, level-scheduled trisolves (P317-323; R9).
-                            Trisolve kernel: one thread-block cluster per subdomain walking its
-                            levels (k_trsv_cl) when every factor row has <= 4 dependencies, else
-                            level-counter chunks (k_trsv); environment RAS_TRSV=level|sf forces
-                            k_trsv / the sync-free k_trsv_sf (all three: identical results) */
+                            Trisolve kernel (identical results): one thread-block cluster per
+                            subdomain walking its levels, dependencies pushed through distributed
+                            shared memory (k_trsv_ds) when every dependency lies in the previous
+                            level and rows have <= 4 dependencies / consumers; else the cluster
+                            walk through L2 (k_trsv_cl) when the levels fit its clusters; else
+                            level-counter chunks over the whole GPU (k_trsv).  Environment
+                            RAS_TRSV=cl|level|sf forces k_trsv_cl / k_trsv / the sync-free k_trsv_sf */
   RAS_LS_ILU0_PCG = 2,   /* PCG, M = L U, ILU(0) of A_p (R10) */
   RAS_LS_EXACT_PCG = 3,  /* Jacobi-PCG to ||r|| <= 1e-14 ||r~||, <= 10|Omega_p| iterations:
                             the iterative stand-in for the paper's direct local solve (P317-318; R6) */

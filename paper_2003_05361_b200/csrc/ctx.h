@@ -144,6 +144,7 @@ struct ras_ctx {
   int trsv_cl_force = 0;    // RAS_TRSV_CL: fixed cluster size (tests), 0 = sized to the widest level
   std::vector<int> trsv_cl_fit;  // co-resident clusters of k_trsv_cl per cluster size (-1 = not queried)
   int trsv_cl_nt = 512;    // RAS_TRSV_CL_NT: row-taking threads per CTA (tests)
+  bool trsv_cl_forced = false;  // RAS_TRSV=cl / RAS_TRSV_CL: k_trsv_cl even for levels wider than its prefetch
   bool trsv_ds = false;     // DSMEM-routed solves (k_trsv_ds) for both factors
   int trsv_mode = 0;        // 0 = cluster-resident when usable (default), 1 = level barriers (k_trsv), 2 = sync-free
   bool trsv_sf = false;     // sync-free trisolve (k_trsv_sf, RAS_TRSV=sf); default k_trsv (level barriers)

@@ -644,6 +644,7 @@ static ras_status upload_factors(ras_ctx* c) {
     // (RAS_TRSV_DS_CL forces a size; RAS_TRSV=cl keeps k_trsv_cl)
     const char* fd = getenv("RAS_TRSV_DS_CL");
     const char* e = getenv("RAS_TRSV");
+    c->trsv_cl_forced = (e && std::strcmp(e, "cl") == 0) || f;
     if (!(e && std::strcmp(e, "cl") == 0)) {
       RAS_CUDA(c, cudaFuncSetAttribute(k_trsv_ds, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       RAS_CUDA(c, cudaFuncSetAttribute(k_trsv_ds, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1262,11 +1263,17 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
             break;
           }
       }
+      // a level wider than kTrcRPT rows per thread of one cluster (one huge
+      // subdomain, e.g. C4's 256^3 per GPU) would leave most SMs idle: the
+      // grid-wide level-counter kernel below takes it (unless RAS_TRSV=cl)
+      const bool too_wide = (int64_t)ncl * c->trsv_cl_nt * kTrcRPT < wide;
+      if (!too_wide || c->trsv_cl_forced) {
       const double* src = dir == 0 ? in : c->d_q;
       double* dst = dir == 0 ? c->d_q : z;
       LAUNCH_ON(s, K_TRSV, cl_launch(s, (unsigned)(nsub * ncl), (unsigned)ncl, T.cl, (int32_t)l0, (int32_t)c->trsv_cl_nt, src, dst,
                                      (const int32_t*)c->S.active, C));
       continue;
+      }
     }
     if (R.lp < 0) {
       RAS_CUDA(c, cudaMemsetAsync(done, 0, (size_t)T.nlev_slots * 4, s));
