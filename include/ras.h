@@ -67,7 +67,8 @@ typedef enum {
                             level and rows have <= 4 dependencies / consumers; else the cluster
                             walk through L2 (k_trsv_cl) when the levels fit its clusters; else
                             level-counter chunks over the whole GPU (k_trsv).  Environment
-                            RAS_TRSV=cl|level|sf forces k_trsv_cl / k_trsv / the sync-free k_trsv_sf */
+                            RAS_TRSV=cl|pf|level|sf forces k_trsv_cl / k_trsv with prefetch
+                            (k_trsv_pf, also the fallback for wide levels) / k_trsv / the sync-free k_trsv_sf */
   RAS_LS_ILU0_PCG = 2,   /* PCG, M = L U, ILU(0) of A_p (R10) */
   RAS_LS_EXACT_PCG = 3,  /* Jacobi-PCG to ||r|| <= 1e-14 ||r~||, <= 10|Omega_p| iterations:
                             the iterative stand-in for the paper's direct local solve (P317-318; R6) */

@@ -146,7 +146,7 @@ struct ras_ctx {
   int trsv_cl_nt = 512;    // RAS_TRSV_CL_NT: row-taking threads per CTA (tests)
   bool trsv_cl_forced = false;  // RAS_TRSV=cl / RAS_TRSV_CL: k_trsv_cl even for levels wider than its prefetch
   bool trsv_ds = false;     // DSMEM-routed solves (k_trsv_ds) for both factors
-  int trsv_mode = 0;        // 0 = cluster-resident when usable (default), 1 = level barriers (k_trsv), 2 = sync-free
+  int trsv_mode = 0;        // 0 = cluster kernels when usable (default), 1 = level counters (k_trsv), 2 = sync-free, 3 = k_trsv_pf
   bool trsv_sf = false;     // sync-free trisolve (k_trsv_sf, RAS_TRSV=sf); default k_trsv (level barriers)
   ras::TriBuf tri_f, tri_b;
   uint32_t* d_trsv_ctr = nullptr;  // [2][nl + 1] chunk counters (per subdomain + batched)

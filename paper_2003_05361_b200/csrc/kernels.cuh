@@ -877,6 +877,48 @@ static __global__ void __launch_bounds__(kNT_TRC, 1) k_trsv_cl(TriCl T, int32_t 
   }
 }
 
+// Level-counter variant with prefetch (r2): k_trsv's chunk schedule (chunks of
+// one level claimed in level order, a chunk waits for the previous level's
+// completion count; any number of SMs per subdomain) with k_trsv_cl's
+// position-ordered operands: after claiming its chunk a thread loads its row's
+// static operands and input value BEFORE the level wait, so only the
+// dependencies' values (L2) remain on the per-level chain.  For subdomains whose
+// levels are too wide for one cluster (C4: one 256^3 subdomain per GPU).
+static __global__ void __launch_bounds__(kThreads) k_trsv_pf(TriDev T, TriCl P, int use_batched, int32_t c0,
+                                                             int32_t nchunk, uint32_t* counter, int32_t* lev_done,
+                                                             const double* __restrict__ in, double* out,
+                                                             const int32_t* __restrict__ active, Ctl C) {
+  __shared__ int s_c;
+  pdl_start();
+  for (;;) {
+    if (threadIdx.x == 0) s_c = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int c = s_c;
+    __syncthreads();
+    if (c >= nchunk) return;
+    const int cid = use_batched ? T.batched[c] : c0 + c;
+    const int4 ch = T.chunk[cid];
+    const int lp = ch.z, lev = ch.w;
+    const int32_t* done = lev_done + T.sub_lev_off[lp];
+    const bool skip = stopped(C, lp) || !active[lp];
+    TrcRow R;
+    trc_fetch(P, ch.x + (int32_t)threadIdx.x, skip ? 0 : ch.y, in, R);  // in flight during the wait
+    if (!skip && lev > 0 && threadIdx.x == 0) {
+      const int32_t need = T.lev_nchunks[T.sub_lev_off[lp] + lev - 1];
+      while (ld_acquire_gpu(done + lev - 1) < need) {
+#if RAS_TRSV_SLEEP > 0
+        __nanosleep(RAS_TRSV_SLEEP);
+#endif
+      }
+    }
+    __syncthreads();
+    if (!skip) trc_solve(R, out);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&lev_done[T.sub_lev_off[lp] + lev]) : "memory");
+  }
+}
+
 // DSMEM-routed variant (r2, default where it applies): the same cluster-per-
 // subdomain level walk, but a row's dependencies never travel through global
 // memory.  When row d (level l-1) is solved, its value is pushed straight into

@@ -614,7 +614,7 @@ static ras_status upload_factors(ras_ctx* c) {
     // barriers on B200: profiles/r02_trsv.md), default the level-barrier kernel
     const char* e = getenv("RAS_TRSV");
     c->trsv_sf = e && std::strcmp(e, "sf") == 0;
-    c->trsv_mode = c->trsv_sf ? 2 : (e && std::strcmp(e, "level") == 0) ? 1 : 0;
+    c->trsv_mode = c->trsv_sf ? 2 : (e && std::strcmp(e, "level") == 0) ? 1 : (e && std::strcmp(e, "pf") == 0) ? 3 : 0;
   }
   if (c->trsv_mode == 0 && c->tri_f.cl_ok && c->tri_b.cl_ok) {
     // cluster-resident solve: 16-CTA clusters with the non-portable opt-in when the
@@ -1283,8 +1283,13 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
     const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));
     const double* src = dir == 0 ? in : c->d_q;  // forward: in -> y (in q), backward: y -> z
     double* dst = dir == 0 ? c->d_q : z;
-    KL(s, K_TRSV, g, kThreads, k_trsv, T.dev, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
-       (const int32_t*)c->S.active, C);
+    if (T.cl_ok && c->trsv_mode != 1) {  // position-ordered operands prefetched across the level wait
+      KL(s, K_TRSV, g, kThreads, k_trsv_pf, T.dev, T.cl, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
+         (const int32_t*)c->S.active, C);
+    } else {  // RAS_TRSV=level, or rows with > 4 dependencies
+      KL(s, K_TRSV, g, kThreads, k_trsv, T.dev, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
+         (const int32_t*)c->S.active, C);
+    }
   }
   return RAS_OK;
 }

@@ -66,10 +66,12 @@ def test_ic0_converges_sync_and_async():
 # with 2-CTA clusters (routing across CTAs), the cluster-resident k_trsv_cl (own
 # cluster sizing; forced to 4-CTA clusters of 128 row threads = levels spread
 # over CTAs + several rows per thread; one CTA of 64 row threads = levels 14x
-# wider than the CTA), and the level-barrier kernel k_trsv
+# wider than the CTA), the level-counter kernel with prefetch k_trsv_pf, and
+# the plain level-counter kernel k_trsv
 TRSV = {"ds": {}, "ds2": {"RAS_TRSV_DS_CL": "2"}, "cl": {"RAS_TRSV": "cl"},
         "cl4x128": {"RAS_TRSV": "cl", "RAS_TRSV_CL": "4", "RAS_TRSV_CL_NT": "128"},
-        "cl1x64": {"RAS_TRSV": "cl", "RAS_TRSV_CL": "1", "RAS_TRSV_CL_NT": "64"}, "level": {"RAS_TRSV": "level"}}
+        "cl1x64": {"RAS_TRSV": "cl", "RAS_TRSV_CL": "1", "RAS_TRSV_CL_NT": "64"}, "level": {"RAS_TRSV": "level"},
+        "pf": {"RAS_TRSV": "pf"}}
 
 
 @functools.lru_cache(maxsize=None)
