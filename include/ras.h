@@ -139,11 +139,11 @@ typedef struct {
   ras_pcg_path pcg_path;         /* default RAS_PCG_AUTO */
   int32_t async_persistent;      /* async on one or more GPUs with BLOCK-sized subdomains: one persistent
                                     cooperative kernel per GPU, every CTA iterating its subdomains with no
-                                    host involvement.  2 (default) = only for tolerance-based local solves
-                                    (exact / inner_tol > 0; R33); 1 = also for fixed-m PCG (asynchronous
-                                    convergence then needs rho(|T|) < 1, which inexact PCG local solves do
-                                    not guarantee: measured to diverge on thin strips with wide overlap);
-                                    0 = CUDA streams */
+                                    host involvement.  2 (default) = for tolerance-based local solves
+                                    (exact / inner_tol > 0) and, on one GPU, for fixed-m PCG too, whose
+                                    residuals there read every neighbour's update whole (per-subdomain
+                                    sequence counters: without them fixed-m PCG diverges on thin strips,
+                                    R33); 1 = always; 0 = CUDA streams */
   int32_t force_first_stop;      /* test hook (async): in the first detection round every Eq. 2 flag reads
                                     as set, so detection terminates after a few updates and the
                                     post-termination verification fails -> the R20 resume path runs */

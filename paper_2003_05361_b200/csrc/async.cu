@@ -22,7 +22,6 @@
 //                v declares when c_v AND all; STOP floods over the tree.
 // After every local subdomain stopped: barrier, halo refresh, true residual
 // (P346-348); if it fails, flags are cleared and iteration resumes (R20).
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -38,6 +37,10 @@
 #include "plan_internal.h"
 
 namespace ras {
+
+__device__ __forceinline__ void st_relaxed_gpu_i32(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 struct DetDev {
   int32_t P;
@@ -57,8 +60,14 @@ struct DetDev {
   const int32_t* force;   // test hook (ras_options.force_first_stop): nonzero -> every flag reads as set
   double* phase;          // [nl][kNPhase] device seconds per phase (ras_stats_t t_*), summed over updates
   unsigned long long* phase_last;  // [nl] globaltimer of the subdomain's last phase boundary
-  int32_t lockstep;       // diagnostic (RAS_PERSISTENT_LOCKSTEP=1, one CTA per subdomain): grid barriers
-                          // between every residual and every write -> the synchronous sweep (R33 study)
+  // persistent kernel, one GPU (R33): per-subdomain sequence counters around every
+  // x[S_p] write; a residual is recomputed until no data neighbour wrote during it,
+  // so it sees every neighbour's update whole (default on; RAS_PERSISTENT_SEQLOCK=0
+  // turns it off, which lets fixed-m PCG diverge on thin strips)
+  int32_t* seq;
+  const int32_t* dnb_off;  // [nl+1] data neighbours (owners of Gamma_p / Omega_p rows), local ids
+  const int32_t* dnb;
+  int32_t seqlock;
 };
 
 // Phase accounting of asynchronous updates (ras_stats_t t_residual ... t_convcheck,
@@ -323,6 +332,23 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       double* sd = dglob ? dglob + r0 : smem + 2 * n;  // d: row-private, shared memory or L2
       // a1 + a2: r~ = b~ - [A_p | B_p] x (owner storage read through L2), z = D^-1 r
       double v[3] = {0.0, 0.0, 0.0};
+      __shared__ int32_t s_sv[64];
+      __shared__ int s_retry;
+    seq_retry:  // (whole-update neighbour snapshots, R33)
+      if (det.seqlock) {
+        const int nb0 = det.dnb_off[lp], nnb = min(64, det.dnb_off[lp + 1] - nb0);
+        __syncthreads();
+        if (threadIdx.x == 0) s_retry = 0;
+        __syncthreads();
+        if ((int)threadIdx.x < nnb) {
+          const int32_t sv = ld_acquire_gpu(&det.seq[det.dnb[nb0 + threadIdx.x]]);
+          s_sv[threadIdx.x] = sv;
+          if (sv & 1) s_retry = 1;  // a neighbour is mid-write
+        }
+        __syncthreads();
+        if (s_retry) goto seq_retry;
+        v[0] = v[1] = v[2] = 0.0;
+      }
       for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
         const int64_t row = (int64_t)r0 + i;
         const double ax = resident_row<WR, Z>(Rm, row, tabR, [&](int32_t c) { return ld_relaxed_f64(&x[c]); });
@@ -334,6 +360,15 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
         v[0] += ri * zi;
         v[1] += ri * ri;
         v[2] += __ldg(&own_slot[row]) >= 0 ? ri * ri : 0.0;
+      }
+      if (det.seqlock) {
+        const int nb0 = det.dnb_off[lp], nnb = min(64, det.dnb_off[lp + 1] - nb0);
+        __threadfence();  // the x reads above before the counters' second read
+        __syncthreads();
+        if ((int)threadIdx.x < nnb && ld_acquire_gpu(&det.seq[det.dnb[nb0 + threadIdx.x]]) != s_sv[threadIdx.x])
+          s_retry = 1;
+        __syncthreads();
+        if (s_retry) goto seq_retry;
       }
       block_allsum<3>(v, red);
       // a6: Eq. 2 flag + one detection step (P331-357)
@@ -361,17 +396,28 @@ static __global__ void __launch_bounds__(kNT_SMALL, 1)
       }
       __syncthreads();
       if (s_stop) continue;
-      if (det.lockstep) cooperative_groups::this_grid().sync();  // every residual read x^k
       // a3: the whole local PCG in shared memory; a4: x[S_p] += d
       const int its = v[0] != 0.0 ? block_pcg<RPT, WL, Z>(L, D, r0, n, sp, sr, sd, v[0], v[1], m, inner_tol, red) : 0;
       if (threadIdx.x == 0) phase_mark(det, lp, PH_SOLVE);
+      if (its > 0 && det.seqlock && threadIdx.x == 0) {  // odd: x[S_p] being written
+        st_relaxed_gpu_i32(&det.seq[lp], det.seq[lp] + 1);
+        __threadfence();
+      }
+      if (det.seqlock) __syncthreads();
       if (its > 0)
         for (int i = threadIdx.x; i < n; i += kNT_SMALL) {
           const int32_t sl = __ldg(&own_slot[r0 + i]);
           if (sl >= 0) st_relaxed_f64(&x[sl], ld_relaxed_f64(&x[sl]) + sd[i]);
         }
+      if (its > 0 && det.seqlock) {  // even again: published
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          st_relaxed_gpu_i32(&det.seq[lp], det.seq[lp] + 1);
+        }
+      }
       if (threadIdx.x == 0) phase_mark(det, lp, PH_PROL);
-      if (det.lockstep) cooperative_groups::this_grid().sync();  // every write landed before the next residuals
       // a5 (multi-GPU): owner values other GPUs need, stored straight into their
       // halo storage over NVLink; then a system-scope fence and a version bump in
       // each destination's board (MPI_Put + flush analogue, P394-396)
@@ -603,8 +649,19 @@ ras_status async_setup(ras_ctx* c) {
   TRY(zalloc(c, &A->d_force, 1));
   D.force = A->d_force;
   {
-    const char* e = getenv("RAS_PERSISTENT_LOCKSTEP");
-    D.lockstep = e && e[0] == '1';
+    const char* q = getenv("RAS_PERSISTENT_SEQLOCK");
+    D.seqlock = !(q && q[0] == '0') && W == 1;
+    std::vector<int32_t> off(1, 0), nb;
+    for (int lp = 0; lp < nl; ++lp) {
+      for (int32_t g : pl->subs[lp].nbr_subs) nb.push_back(g);  // one GPU: local id = global id
+      off.push_back((int32_t)nb.size());
+    }
+    int32_t *doff, *dnb;
+    TRY(upload(c, &doff, off, 1));
+    TRY(upload(c, &dnb, nb, 1));
+    D.dnb_off = doff;
+    D.dnb = dnb;
+    TRY(zalloc(c, &D.seq, (size_t)std::max(nl, 1)));
   }
   TRY(zalloc(c, &D.phase, (size_t)std::max(nl, 1) * kNPhase));
   TRY(zalloc(c, &D.phase_last, (size_t)std::max(nl, 1)));
@@ -1099,7 +1156,8 @@ ras_status solve_async(ras_ctx* c, double tol, int64_t max_iters) {
       st = run_scripted(c, tol, max_iters, m, inner_tol);
     } else if (c->path == RAS_PCG_RESIDENT && !c->small) {
       st = run_async_sequential(c, tol, max_iters, m, inner_tol, exact, &timeout);
-    } else if (c->small && (c->opt.async_persistent == 1 || (c->opt.async_persistent == 2 && inner_tol > 0.0))) {
+    } else if (c->small && (c->opt.async_persistent == 1 ||
+                            (c->opt.async_persistent == 2 && (inner_tol > 0.0 || A->det.seqlock)))) {
       st = run_async_persistent(c, tol, max_iters, m, inner_tol, &timeout);
     } else {
       st = run_async_loop(c, tol, max_iters, m, inner_tol, exact, &timeout);
