@@ -136,18 +136,38 @@ def test_async_persistent_more_subdomains_than_ctas():
     s.close()
 
 
-def test_async_persistent_default_is_tolerance_solves_only():
-    # R33: fixed-m inexact local solves default to the stream driver (the fully
-    # concurrent persistent schedule diverges on thin strips with wide overlap);
-    # exact (tolerance) solves take the persistent kernel
+@pytest.mark.parametrize("seqlock", ["1", "0"])
+def test_async_persistent_default(seqlock, monkeypatch):
+    # R33: on one GPU the persistent kernel reads every neighbour's update whole
+    # (sequence counters), so fixed-m local solves take it by default like exact
+    # (tolerance) solves; with the snapshots turned off fixed-m solves go back to
+    # the stream driver (the torn-snapshot schedule diverges on thin strips)
+    monkeypatch.setenv("RAS_PERSISTENT_SEQLOCK", seqlock)
     N = 128
     A = ri.laplace_2d(N)
     b = ri.rhs(N * N, 2)
     owner = R.partition_regular(N, N, 1, 1, 8, 1)
-    for kind, few_launches in (("jacobi", False), ("exact", True)):
+    for kind in ("jacobi", "exact"):
+        few_launches = kind == "exact" or seqlock == "1"
         s = R.Solver(A, b, owner, 4, R.options(kind, 20))
         st, x = s.solve(1e-8, 50000, "async")
         stt = s.stats()
         assert st == 0 and O.verify_global(A, x, b, 1e-8)[0], (kind, stt)
         assert (stt["kernel_launches"] < 50) == few_launches, (kind, stt["kernel_launches"])
         s.close()
+
+
+def test_r33_thin_strips_converge_with_whole_update_snapshots():
+    # the configuration that diverged (1e70) with one CTA per strip and fixed-m
+    # PCG(20) while neighbours' corrections were read half-written (R33): with
+    # whole-update snapshots the fully concurrent schedule converges
+    N = 256
+    A = ri.laplace_2d(N)
+    b = ri.rhs(N * N, 0)
+    owner = R.partition_regular(N, N, 1, 1, 16, 1)
+    s = R.Solver(A, b, owner, 4, R.options("jacobi", 20, async_persistent=1, persistent_grid=16, max_resumes=0))
+    st, x = s.solve(1e-8, 4000, "async")
+    stt = s.stats()
+    assert st == 0 and O.verify_global(A, x, b, 1e-8)[0], stt
+    assert stt["updates_max"] < 2000, stt
+    s.close()
