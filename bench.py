@@ -569,7 +569,7 @@ def main():
                "oracle_tts": o_tts,
                "c2_tts_extrapolated_s": (c2_sweeps / val) if c2_sweeps else None,
                "c2_tts_extrapolation": (f"EXTRAPOLATED: {c2_sweeps} sweeps (GPU sync run to 1e-8, "
-                                        "profiles/bench_r01_tts_c2.json) / oracle sweeps per s" if c2_sweeps else None)}
+                                        "profiles/bench_r02_tts_c2.json) / oracle sweeps per s" if c2_sweeps else None)}
     clocks = clk.summary()
     if rank == 0:
         res = kern.get("k_residual")
@@ -610,7 +610,7 @@ def main():
 def committed_c2_sweeps():
     """GPU sweep count of the committed C2 sync run to 1e-8 (for the labelled extrapolation)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "bench_r01_tts_c2.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "bench_r02_tts_c2.json")) as f:
             d = json.load(f)
         t = d.get("tts") or {}
         t = t.get("bench_workload", t)

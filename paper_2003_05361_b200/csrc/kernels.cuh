@@ -922,9 +922,10 @@ static __global__ void __launch_bounds__(kThreads) k_trsv_pf(TriDev T, TriCl P, 
 // DSMEM-routed variant (r2, default where it applies): the same cluster-per-
 // subdomain level walk, but a row's dependencies never travel through global
 // memory.  When row d (level l-1) is solved, its value is pushed straight into
-// the shared memory of each CTA that consumes it (st.async.shared::cluster,
-// completing bytes on that CTA's mbarrier); a CTA starts level l once its
-// mbarrier has counted all the bytes its level-l rows need.  The cluster still
+// the shared memory of each CTA that consumes it (another CTA: st.async.
+// shared::cluster, completing bytes on that CTA's mbarrier; its own CTA: a plain
+// shared store, most consumers of a stencil row); a CTA starts level l once its
+// mbarrier has counted all the bytes its level-l rows need from other CTAs.  The cluster still
 // meets once per level, but at a RELAXED barrier (no release fence: ~70 ns, and
 // no wait for the prefetch loads in flight, which a release's MEMBAR.ALL.GPU
 // would wait for -- profiles/r02_trsv_cl_summary.md); it only bounds the skew
@@ -986,13 +987,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
         : "memory");
 }
 __device__ __forceinline__ void cluster_sync_relaxed() {
+  __syncthreads();  // the CTA's own plain shared-memory sends, for its consumer threads
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
-// push v into slot `e & 0xffff` of CTA `e >> 16`'s receive area (rcv_next: this
-// CTA's address of that area), completing 8 bytes on its mbarrier mb_next
-__device__ __forceinline__ void trd_send(int32_t e, double v, uint32_t rcv_next, uint32_t mb_next) {
+// push v into slot `e & 0xffff` of CTA `e >> 16`'s receive area: another CTA's by
+// st.async over DSMEM, completing 8 bytes on its mbarrier mb_next (rcv_next: this
+// CTA's address of the area); this CTA's own with a plain shared-memory store
+// (ordered for the consumer threads by the CTA barrier that ends the level)
+__device__ __forceinline__ void trd_send(int32_t e, double v, double* rcv_local, uint32_t rcv_next, uint32_t mb_next,
+                                         uint32_t rank) {
   if (e < 0) return;
   const uint32_t cta = (uint32_t)e >> 16, slot = (uint32_t)e & 0xffffu;
+  if (cta == rank) {
+    rcv_local[slot] = v;
+    return;
+  }
   uint32_t ra, rm;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(rcv_next + 8u * slot), "r"(cta));
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rm) : "r"(mb_next), "r"(cta));
@@ -1000,8 +1009,8 @@ __device__ __forceinline__ void trd_send(int32_t e, double v, uint32_t rcv_next,
                "l"(__double_as_longlong(v)), "r"(rm)
                : "memory");
 }
-__device__ __forceinline__ void trd_solve(const TrdRow& P, const double* rcv_j, double* out, uint32_t rcv_next,
-                                          uint32_t mb_next) {
+__device__ __forceinline__ void trd_solve(const TrdRow& P, const double* rcv_j, double* out, double* rcv_local,
+                                          uint32_t rcv_next, uint32_t mb_next, uint32_t rank) {
   if (P.pr == kTrdNone) return;
   const uint32_t nd = P.pr >> 29;
   double s = P.in;
@@ -1010,10 +1019,10 @@ __device__ __forceinline__ void trd_solve(const TrdRow& P, const double* rcv_j, 
   if (nd > 2) s -= P.v23.x * rcv_j[2];
   if (nd > 3) s -= P.v23.y * rcv_j[3];
   const double o = s / P.dv;
-  trd_send(P.snd.x, o, rcv_next, mb_next);
-  trd_send(P.snd.y, o, rcv_next, mb_next);
-  trd_send(P.snd.z, o, rcv_next, mb_next);
-  trd_send(P.snd.w, o, rcv_next, mb_next);
+  trd_send(P.snd.x, o, rcv_local, rcv_next, mb_next, rank);
+  trd_send(P.snd.y, o, rcv_local, rcv_next, mb_next, rank);
+  trd_send(P.snd.z, o, rcv_local, rcv_next, mb_next, rank);
+  trd_send(P.snd.w, o, rcv_local, rcv_next, mb_next, rank);
   out[P.pr & 0x1fffffffu] = o;  // the result (read by the next kernel)
 }
 static __global__ void __launch_bounds__(kNT_TRD, 1) k_trsv_ds(TriDs T, int32_t lp_base, const double* __restrict__ in,
@@ -1072,16 +1081,17 @@ static __global__ void __launch_bounds__(kNT_TRD, 1) k_trsv_ds(TriDs T, int32_t 
     const int par = l & 1;
     if (l > 0) mbar_wait(&mbar[par], (uint32_t)(((l - 1) >> 1) & 1));  // phase of level l on mbar[l & 1]
     const double* rc = rcv + par * kTrdSlots;
+    double* rl = rcv + (par ^ 1) * kTrdSlots;
     const uint32_t rn = rcv_s + 8u * (uint32_t)((par ^ 1) * kTrdSlots), mn = mb_s[par ^ 1];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) trd_solve(P[u], rc + 4 * (u * kNT_TRD + t), out, rn, mn);
+    for (int u = 0; u < 2; ++u) trd_solve(P[u], rc + 4 * (u * kNT_TRD + t), out, rl, rn, mn, (uint32_t)rank);
     int32_t k0, ke;
     blk(l, k0, ke);
     for (int u = 2; u < kTrdRows; ++u) {  // a third row of a wide level, fetched on the spot
       TrdRow Q;
       trd_fetch_static(T, k0 + u * kNT_TRD + t, k0 + u * kNT_TRD + t < ke, Q);
       trd_fetch_in(in, Q);
-      trd_solve(Q, rc + 4 * (u * kNT_TRD + t), out, rn, mn);
+      trd_solve(Q, rc + 4 * (u * kNT_TRD + t), out, rl, rn, mn, (uint32_t)rank);
     }
   };
   auto rearm = [&](int32_t l) {  // after the barrier that ended level l - 2 (its phase is over): arm level l

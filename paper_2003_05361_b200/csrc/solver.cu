@@ -525,7 +525,8 @@ static bool build_ds(ras_ctx* c, const TriHost& H, int ncl, TriBuf& B, ras_statu
   *st = RAS_OK;
   const size_t np = H.rows.size();
   const int nl = (int)H.sub_nlev.size();
-  std::vector<int32_t> pos_of_row((size_t)c->rows_pad, -1), lev_of(np, -1), prow(np), rb_off(nl + 1, 0), rbytes;
+  std::vector<int32_t> pos_of_row((size_t)c->rows_pad, -1), lev_of(np, -1), cta_of(np, 0), prow(np), rb_off(nl + 1, 0),
+      rbytes;
   std::vector<int4> psend(np, make_int4(-1, -1, -1, -1));
   for (size_t k = 0; k < np; ++k) {
     if (H.rows[k] >= (1 << 29)) return false;
@@ -536,8 +537,13 @@ static bool build_ds(ras_ctx* c, const TriHost& H, int ncl, TriBuf& B, ras_statu
     const int nlev = H.sub_nlev[lp];
     rb_off[lp] = (int32_t)rbytes.size();
     rbytes.resize(rbytes.size() + (size_t)nlev * ncl, 0);
-    for (int l = 0; l < nlev; ++l)
-      for (int32_t k = lev[l]; k < lev[l + 1]; ++k) lev_of[k] = l;
+    for (int l = 0; l < nlev; ++l) {
+      const int32_t b = lev[l], n = lev[l + 1] - b, q = (n + ncl - 1) / ncl;
+      for (int32_t k = b; k < lev[l + 1]; ++k) {
+        lev_of[k] = l;
+        cta_of[k] = (k - b) / q;
+      }
+    }
     for (int l = 0; l < nlev; ++l) {
       const int32_t b = lev[l], n = lev[l + 1] - b, q = (n + ncl - 1) / ncl;
       if (q > kTrdRows * kNT_TRD) return false;
@@ -545,10 +551,12 @@ static bool build_ds(ras_ctx* c, const TriHost& H, int ncl, TriBuf& B, ras_statu
         const int32_t r = (k - b) / q, j = (k - b) % q, nd = H.rp[k + 1] - H.rp[k];
         if (nd > 4) return false;
         prow[k] = H.rows[k] | (nd << 29);
-        rbytes[rb_off[lp] + (size_t)l * ncl + r] += 8 * nd;
         for (int32_t qd = 0; qd < nd; ++qd) {
           const int32_t d = pos_of_row[H.col[H.rp[k] + qd]];
           if (d < 0 || lev_of[d] != l - 1) return false;
+          // only values from other CTAs arrive through the mbarrier (DSMEM);
+          // a CTA's own consumers are written with plain shared-memory stores
+          if (cta_of[d] != r) rbytes[rb_off[lp] + (size_t)l * ncl + r] += 8;
           int32_t* sd = &psend[d].x;
           int w = 0;
           while (w < 4 && sd[w] >= 0) ++w;
