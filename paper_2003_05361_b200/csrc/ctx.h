@@ -55,6 +55,8 @@ struct TriBuf {
   TriCl cl{};
   std::vector<int32_t> sub_max_lev;  // rows of the largest level per subdomain
   // DSMEM-routed solve (k_trsv_ds): routing tables for cluster size ds_ncl
+  int2* d_cdep = nullptr;     // k_trsv_pf: per chunk, the range of chunk ids its rows depend on
+  int32_t* d_cflag = nullptr;  // k_trsv_pf: per chunk, 1 once completed in the current launch
   bool ds_ok = false;
   int ds_ncl = 0;
   TriDs ds{};

@@ -877,16 +877,19 @@ static __global__ void __launch_bounds__(kNT_TRC, 1) k_trsv_cl(TriCl T, int32_t 
   }
 }
 
-// Level-counter variant with prefetch (r2): k_trsv's chunk schedule (chunks of
-// one level claimed in level order, a chunk waits for the previous level's
-// completion count; any number of SMs per subdomain) with k_trsv_cl's
-// position-ordered operands: after claiming its chunk a thread loads its row's
-// static operands and input value BEFORE the level wait, so only the
-// dependencies' values (L2) remain on the per-level chain.  For subdomains whose
-// levels are too wide for one cluster (C4: one 256^3 subdomain per GPU).
+// Chunk-flag variant with prefetch (r2): k_trsv's chunk schedule (chunks of
+// one level claimed in level order; any number of SMs per subdomain) with
+// k_trsv_cl's position-ordered operands: after claiming its chunk a thread loads
+// its row's static operands and input value BEFORE the wait, so only the
+// dependencies' values (L2) remain on the chain.  A chunk waits only for the
+// chunks its rows depend on (range [cdep.x, cdep.y] of earlier chunk ids,
+// precomputed), not for the whole previous level; flags are cleared before each
+// launch and set to `epoch` (1) on completion.  For subdomains whose levels are
+// too wide for one cluster (C4: one 256^3 subdomain per GPU).
 static __global__ void __launch_bounds__(kThreads) k_trsv_pf(TriDev T, TriCl P, int use_batched, int32_t c0,
-                                                             int32_t nchunk, uint32_t* counter, int32_t* lev_done,
-                                                             const double* __restrict__ in, double* out,
+                                                             int32_t nchunk, uint32_t* counter,
+                                                             const int2* __restrict__ cdep, int32_t* cflag,
+                                                             int32_t epoch, const double* __restrict__ in, double* out,
                                                              const int32_t* __restrict__ active, Ctl C) {
   __shared__ int s_c;
   pdl_start();
@@ -898,24 +901,23 @@ static __global__ void __launch_bounds__(kThreads) k_trsv_pf(TriDev T, TriCl P, 
     if (c >= nchunk) return;
     const int cid = use_batched ? T.batched[c] : c0 + c;
     const int4 ch = T.chunk[cid];
-    const int lp = ch.z, lev = ch.w;
-    const int32_t* done = lev_done + T.sub_lev_off[lp];
+    const int lp = ch.z;
     const bool skip = stopped(C, lp) || !active[lp];
     TrcRow R;
     trc_fetch(P, ch.x + (int32_t)threadIdx.x, skip ? 0 : ch.y, in, R);  // in flight during the wait
-    if (!skip && lev > 0 && threadIdx.x == 0) {
-      const int32_t need = T.lev_nchunks[T.sub_lev_off[lp] + lev - 1];
-      while (ld_acquire_gpu(done + lev - 1) < need) {
+    if (!skip && threadIdx.x < 32) {  // one warp polls the producer chunks' flags
+      const int2 dr = __ldg(&cdep[cid]);
+      for (int32_t d = dr.x + (int32_t)threadIdx.x; d <= dr.y; d += 32)
+        while (ld_acquire_gpu(&cflag[d]) != epoch) {
 #if RAS_TRSV_SLEEP > 0
-        __nanosleep(RAS_TRSV_SLEEP);
+          __nanosleep(RAS_TRSV_SLEEP);
 #endif
-      }
+        }
     }
     __syncthreads();
     if (!skip) trc_solve(R, out);
     __syncthreads();
-    if (threadIdx.x == 0)
-      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&lev_done[T.sub_lev_off[lp] + lev]) : "memory");
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(&cflag[cid]), "r"(epoch) : "memory");
   }
 }
 

@@ -511,6 +511,25 @@ static ras_status upload_tri(ras_ctx* c, const TriHost& H, TriBuf& B) {
     TRY(upload(c, &pc, pcol, 1));
     TRY(upload(c, &pv, pval, 2));
     B.cl = TriCl{lp, spo, snl, rows, dv, pc, (const double2*)pv};
+    // k_trsv_pf: the chunks each chunk's rows depend on (chunk ids are in
+    // position = level order, so the range covers earlier chunks only)
+    std::vector<int32_t> pos_of_row((size_t)c->rows_pad, -1), chunk_of(np, 0);
+    for (size_t k = 0; k < np; ++k) pos_of_row[H.rows[k]] = (int32_t)k;
+    for (size_t cc = 0; cc < H.chunk.size(); ++cc)
+      for (int32_t k = H.chunk[cc][0]; k < H.chunk[cc][1]; ++k) chunk_of[k] = (int32_t)cc;
+    std::vector<int2> cdep(H.chunk.size(), make_int2(0, -1));
+    for (size_t cc = 0; cc < H.chunk.size(); ++cc) {
+      int32_t lo = INT32_MAX, hi = -1;
+      for (int32_t k = H.chunk[cc][0]; k < H.chunk[cc][1]; ++k)
+        for (int32_t e = H.rp[k]; e < H.rp[k + 1]; ++e) {
+          const int32_t d = chunk_of[pos_of_row[H.col[e]]];
+          lo = std::min(lo, d);
+          hi = std::max(hi, d);
+        }
+      if (hi >= 0) cdep[cc] = make_int2(lo, hi);
+    }
+    TRY(upload(c, &B.d_cdep, cdep, 1));
+    TRY(zalloc(c, &B.d_cflag, std::max<size_t>(H.chunk.size(), 1)));
   }
   // algorithmic bytes of one solve: per real row rows/rp/in/out/diag, per entry val+col
   B.bytes = (double)pl->rows_local * (4 + 4 + 8 + 8 + 8) + (double)(pl->nnz_local - pl->rows_local) / 2.0 * 12.0;
@@ -1292,8 +1311,11 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
     const double* src = dir == 0 ? in : c->d_q;  // forward: in -> y (in q), backward: y -> z
     double* dst = dir == 0 ? c->d_q : z;
     if (T.cl_ok && c->trsv_mode != 1) {  // position-ordered operands prefetched across the level wait
-      KL(s, K_TRSV, g, kThreads, k_trsv_pf, T.dev, T.cl, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
-         (const int32_t*)c->S.active, C);
+      // the launch's chunk flags cleared in stream order (replay-safe inside the
+      // async driver's captured graphs), completion = 1
+      RAS_CUDA(c, cudaMemsetAsync(T.d_cflag + c0, 0, (size_t)nch * 4, s));
+      KL(s, K_TRSV, g, kThreads, k_trsv_pf, T.dev, T.cl, (int)(R.lp < 0), c0, nch, ctr, (const int2*)T.d_cdep,
+         T.d_cflag, 1, src, dst, (const int32_t*)c->S.active, C);
     } else {  // RAS_TRSV=level, or rows with > 4 dependencies
       KL(s, K_TRSV, g, kThreads, k_trsv, T.dev, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
          (const int32_t*)c->S.active, C);
