@@ -61,14 +61,15 @@ typedef enum { RAS_SYNC = 0, RAS_ASYNC = 1 } ras_mode;
 typedef enum {
   RAS_LS_JACOBI_PCG = 0, /* PCG, M = diag(A_p), fixed m iterations (P313-315; R6, R8) */
   RAS_LS_IC0_PCG = 1,    /* PCG, M = L L^T, IC(0) of A_p, level-scheduled trisolves (P317-323; R9).
-                            Trisolve kernel (identical results): one thread-block cluster per
-                            subdomain walking its levels, dependencies pushed through distributed
-                            shared memory (k_trsv_ds) when every dependency lies in the previous
-                            level and rows have <= 4 dependencies / consumers; else the cluster
-                            walk through L2 (k_trsv_cl) when the levels fit its clusters; else
-                            level-counter chunks over the whole GPU (k_trsv).  Environment
-                            RAS_TRSV=cl|pf|level|sf forces k_trsv_cl / k_trsv with prefetch
-                            (k_trsv_pf, also the fallback for wide levels) / k_trsv / the sync-free k_trsv_sf */
+                            Trisolve kernel (same products in the same order):
+                            one thread-block cluster per subdomain walking its levels, dependencies
+                            pushed through distributed shared memory (k_trsv_ds), when every
+                            dependency lies in the previous level and rows have <= 4 dependencies /
+                            consumers; else the cluster walk through L2 (k_trsv_cl) when the levels
+                            fit its clusters; else chunks over the whole GPU, each waiting for the
+                            chunks it depends on (k_trsv_pf; rows with <= 4 dependencies) or for
+                            the previous level (k_trsv).  Environment RAS_TRSV=cl|pf|level|sf
+                            forces k_trsv_cl / k_trsv_pf / k_trsv / the sync-free k_trsv_sf */
   RAS_LS_ILU0_PCG = 2,   /* PCG, M = L U, ILU(0) of A_p (R10) */
   RAS_LS_EXACT_PCG = 3,  /* Jacobi-PCG to ||r|| <= 1e-14 ||r~||, <= 10|Omega_p| iterations:
                             the iterative stand-in for the paper's direct local solve (P317-318; R6) */
@@ -143,7 +144,8 @@ typedef struct {
                                     (exact / inner_tol > 0) and, on one GPU, for fixed-m PCG too, whose
                                     residuals there read every neighbour's update whole (per-subdomain
                                     sequence counters: without them fixed-m PCG diverges on thin strips,
-                                    R33); 1 = always; 0 = CUDA streams */
+                                    R33; environment RAS_PERSISTENT_SEQLOCK=0 turns them off);
+                                    1 = always; 0 = CUDA streams */
   int32_t force_first_stop;      /* test hook (async): in the first detection round every Eq. 2 flag reads
                                     as set, so detection terminates after a few updates and the
                                     post-termination verification fails -> the R20 resume path runs */
