@@ -19,7 +19,10 @@
 
 namespace ras {
 
-static constexpr int kChunk = 256;
+#ifndef RAS_TRSV_CHUNK
+#define RAS_TRSV_CHUNK 256  // rows per level chunk = threads per CTA of the chunked trisolves (kernels.cuh)
+#endif
+static constexpr int kChunk = RAS_TRSV_CHUNK;
 
 namespace {
 

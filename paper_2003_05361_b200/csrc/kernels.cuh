@@ -581,6 +581,10 @@ static __global__ void __launch_bounds__(kFinThreads) k_finish(int lp_base, Tile
 // a3' (IC(0)/ILU(0)-PCG): M = L U, z = U^-1 L^-1 r by two level-scheduled
 // triangular solves (P320-323, level-set strategy).
 // ---------------------------------------------------------------------------
+#ifndef RAS_TRSV_CHUNK
+#define RAS_TRSV_CHUNK 256  // rows per level chunk (factor.cpp) = threads per CTA of k_trsv / _sf / _pf
+#endif
+constexpr int kTrsvChunk = RAS_TRSV_CHUNK;
 #ifndef RAS_TRSV_SLEEP
 #define RAS_TRSV_SLEEP 64  // ns between polls of a level counter
 #endif
@@ -609,7 +613,7 @@ __device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
 // every chunk of level l-1 of p has completed.  A waited-on chunk was claimed
 // earlier by a running CTA, so the wait always terminates (no co-residency
 // assumption, no inter-launch waiting).
-static __global__ void __launch_bounds__(kThreads) k_trsv(TriDev T, int use_batched, int32_t c0, int32_t nchunk,
+static __global__ void __launch_bounds__(kTrsvChunk) k_trsv(TriDev T, int use_batched, int32_t c0, int32_t nchunk,
                                                           uint32_t* counter, int32_t* lev_done,
                                                           const double* __restrict__ in, double* out,
                                                           const int32_t* __restrict__ active, Ctl C) {
@@ -676,7 +680,7 @@ __device__ __forceinline__ double ld_relaxed_f64_gpu(const double* p) {
 __device__ __forceinline__ void st_relaxed_f64_gpu(double* p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
-static __global__ void __launch_bounds__(kThreads) k_trsv_sf(TriDev T, int use_batched, int32_t c0, int32_t nchunk,
+static __global__ void __launch_bounds__(kTrsvChunk) k_trsv_sf(TriDev T, int use_batched, int32_t c0, int32_t nchunk,
                                                              uint32_t* counter, const double* __restrict__ in,
                                                              double* out, double* rearm,
                                                              const int32_t* __restrict__ active, Ctl C) {
@@ -886,7 +890,7 @@ static __global__ void __launch_bounds__(kNT_TRC, 1) k_trsv_cl(TriCl T, int32_t 
 // precomputed), not for the whole previous level; flags are cleared before each
 // launch and set to `epoch` (1) on completion.  For subdomains whose levels are
 // too wide for one cluster (C4: one 256^3 subdomain per GPU).
-static __global__ void __launch_bounds__(kThreads) k_trsv_pf(TriDev T, TriCl P, int use_batched, int32_t c0,
+static __global__ void __launch_bounds__(kTrsvChunk) k_trsv_pf(TriDev T, TriCl P, int use_batched, int32_t c0,
                                                              int32_t nchunk, uint32_t* counter,
                                                              const int2* __restrict__ cdep, int32_t* cflag,
                                                              int32_t epoch, const double* __restrict__ in, double* out,

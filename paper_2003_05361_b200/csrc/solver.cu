@@ -1259,7 +1259,7 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
         return e ? std::max(1, atoi(e)) : 148 * 2;
       }();
       const unsigned g = (unsigned)std::max(1, std::min(nch, sf_grid));
-      KL(s, K_TRSV, g, kThreads, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
+      KL(s, K_TRSV, g, kTrsvChunk, k_trsv_sf, T.dev, (int)(R.lp < 0), c0, nch, ctr, src, dst, rearm,
          (const int32_t*)c->S.active, C);
       continue;
     }
@@ -1307,17 +1307,17 @@ static ras_status enq_precond(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C,
     } else {
       RAS_CUDA(c, cudaMemsetAsync(done + T.sub_lev_off[R.lp], 0, (size_t)T.sub_nlev[R.lp] * 4, s));
     }
-    const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8));
+    const unsigned g = (unsigned)std::max(1, std::min(nch, 148 * 8 * 256 / kTrsvChunk));
     const double* src = dir == 0 ? in : c->d_q;  // forward: in -> y (in q), backward: y -> z
     double* dst = dir == 0 ? c->d_q : z;
     if (T.cl_ok && c->trsv_mode != 1) {  // position-ordered operands prefetched across the level wait
       // the launch's chunk flags cleared in stream order (replay-safe inside the
       // async driver's captured graphs), completion = 1
       RAS_CUDA(c, cudaMemsetAsync(T.d_cflag + c0, 0, (size_t)nch * 4, s));
-      KL(s, K_TRSV, g, kThreads, k_trsv_pf, T.dev, T.cl, (int)(R.lp < 0), c0, nch, ctr, (const int2*)T.d_cdep,
+      KL(s, K_TRSV, g, kTrsvChunk, k_trsv_pf, T.dev, T.cl, (int)(R.lp < 0), c0, nch, ctr, (const int2*)T.d_cdep,
          T.d_cflag, 1, src, dst, (const int32_t*)c->S.active, C);
     } else {  // RAS_TRSV=level, or rows with > 4 dependencies
-      KL(s, K_TRSV, g, kThreads, k_trsv, T.dev, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
+      KL(s, K_TRSV, g, kTrsvChunk, k_trsv, T.dev, (int)(R.lp < 0), c0, nch, ctr, done, src, dst,
          (const int32_t*)c->S.active, C);
     }
   }
