@@ -943,7 +943,10 @@ static __global__ void __launch_bounds__(kTrsvChunk) k_trsv_pf(TriDev T, TriCl P
 // size (setup, solver.cu).  Receive slot of dependency q of the row with local
 // index j in its CTA's block of the level: j * 4 + q.  Same products in the same
 // order as k_trsv: bitwise the same result.
-constexpr int kNT_TRD = 512;
+#ifndef RAS_NT_TRD
+#define RAS_NT_TRD 512
+#endif
+constexpr int kNT_TRD = RAS_NT_TRD;  // threads per CTA of k_trsv_ds
 constexpr int kTrdRows = 3;                       // rows per thread and level (2 prefetched)
 constexpr int kTrdSlots = 4 * kTrdRows * kNT_TRD;  // receive slots per parity
 struct TriDs {
@@ -1031,7 +1034,7 @@ __device__ __forceinline__ void trd_solve(const TrdRow& P, const double* rcv_j, 
   trd_send(P.snd.w, o, rcv_local, rcv_next, mb_next, rank);
   out[P.pr & 0x1fffffffu] = o;  // the result (read by the next kernel)
 }
-static __global__ void __launch_bounds__(kNT_TRD, 1) k_trsv_ds(TriDs T, int32_t lp_base, const double* __restrict__ in,
+static __global__ void __launch_bounds__(kNT_TRD, 512 / kNT_TRD) k_trsv_ds(TriDs T, int32_t lp_base, const double* __restrict__ in,
                                                                double* out, const int32_t* __restrict__ active, Ctl C) {
   extern __shared__ double rcv[];  // [2][kTrdSlots]
   __shared__ uint64_t mbar[2];
