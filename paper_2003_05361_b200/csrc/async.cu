@@ -792,6 +792,40 @@ static ras_status enqueue_sub_sweep(ras_ctx* c, int lp, cudaStream_t s, double t
   return RAS_OK;
 }
 
+// Two consecutive subdomains updated by one launch of each kernel (RESIDENT path,
+// default; RAS_ASYNC_PAIRS=0 turns it off): both read the latest data and write
+// their own rows -- the asynchronous schedule [[lp, lp+1], ...] (oracle
+// ras_schedule, R34); the RESIDENT kernel runs them as its two lanes.
+static ras_status enqueue_pair_sweep(ras_ctx* c, int lp, cudaStream_t s, double tol, int64_t max_iters, int m,
+                                     double inner_tol, bool exact) {
+  AsyncRt* A = c->async;
+  const ras_plan* pl = c->plan;
+  Range R = range_sub(c, lp);
+  R.ntiles += (unsigned)pl->subs[lp + 1].ntiles;  // tiles of consecutive subdomains are consecutive
+  R.nsub = 2;
+  Ctl C{A->d_lstop, 1};
+  for (int q = lp; q < lp + 2; ++q) k_phase<<<1, 32, 0, s>>>(A->det, q, -1, A->d_lstop);
+  TRY(enq_residual(c, s, R, C));
+  for (int q = lp; q < lp + 2; ++q)
+    k_detect<<<1, 32, 0, s>>>(q, A->det, c->S, tol, max_iters, A->d_lstop, A->h_lstop_dev, A->d_updates, A->d_noconv);
+  c->launches += 4;
+  TRY(enq_pcg(c, s, R, C, m, inner_tol, exact));  // RESIDENT: prolongation fused
+  for (int q = lp; q < lp + 2; ++q) {
+    k_phase<<<1, 32, 0, s>>>(A->det, q, PH_SOLVE, A->d_lstop);
+    c->launches += 1;
+    const int64_t e0 = A->put_off[q], e1 = A->put_off[q + 1];
+    if (e1 > e0) {
+      const unsigned pg = (unsigned)std::min<int64_t>((e1 - e0 + 255) / 256, 148 * 4);
+      k_put<<<pg, 256, 0, s>>>(q, e0, e1, A->d_put_slot, A->d_put_rank, A->d_put_ridx, c->d_x, A->d_peer_x,
+                               A->d_put_ticket, A->d_put_peers + A->put_peer_off[q],
+                               A->put_peer_off[q + 1] - A->put_peer_off[q], A->d_boards, pl->P, pl->subs[q].p,
+                               A->d_lstop, A->det);
+      c->launches += 1;
+    }
+  }
+  return RAS_OK;
+}
+
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -964,6 +998,10 @@ static ras_status run_async_sequential(ras_ctx* c, double tol, int64_t max_iters
   std::vector<cudaEvent_t> ev(Q);
   for (auto& e : ev) RAS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   c->resid_seq = true;
+  // consecutive subdomains updated in pairs (two RESIDENT lanes per launch, R34);
+  // RAS_ASYNC_PAIRS=0: one after another
+  const char* pe = getenv("RAS_ASYNC_PAIRS");
+  const bool pairs = !(pe && pe[0] == '0');
   const double t0 = now_s();
   *timeout = false;
   ras_status st = RAS_OK;
@@ -979,8 +1017,15 @@ static ras_status run_async_sequential(ras_ctx* c, double tol, int64_t max_iters
       *timeout = true;
       break;
     }
-    for (int lp = 0; lp < nl && st == RAS_OK; ++lp)
-      if (!((volatile int32_t*)A->h_lstop)[lp]) st = enqueue_sub_sweep(c, lp, c->stream, tol, max_iters, m, inner_tol, exact);
+    for (int lp = 0; lp < nl && st == RAS_OK; ++lp) {
+      const bool live = !((volatile int32_t*)A->h_lstop)[lp];
+      if (pairs && lp + 1 < nl && live && !((volatile int32_t*)A->h_lstop)[lp + 1]) {
+        st = enqueue_pair_sweep(c, lp, c->stream, tol, max_iters, m, inner_tol, exact);
+        ++lp;
+      } else if (live) {
+        st = enqueue_sub_sweep(c, lp, c->stream, tol, max_iters, m, inner_tol, exact);
+      }
+    }
     if (st != RAS_OK) break;
     RAS_CUDA(c, cudaEventRecord(ev[k % Q], c->stream));
   }

@@ -38,7 +38,8 @@ enum KId { K_RES = 0, K_SPMV, K_UPD, K_PUPD, K_PROL, K_PACK, K_CTRL, K_TRSV, K_Z
 struct Range {
   int64_t tile_base;
   unsigned ntiles;
-  int lp;
+  int lp;        // first local subdomain, -1 = all
+  int nsub = 1;  // subdomains from lp (consecutive; RESIDENT / scalar kernels)
 };
 
 // Device copy of one level-ordered triangular factor (factor.cpp / k_trsv).

@@ -1170,7 +1170,7 @@ Range range_sub(ras_ctx* c, int lp) {
 // per-subdomain scalar step after a streaming kernel (one CTA per subdomain in R)
 template <int OP>
 static void enq_finish(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m = 0, double inner_tol = 0.0) {
-  const unsigned nsub = R.lp < 0 ? (unsigned)c->nl : 1u;
+  const unsigned nsub = R.lp < 0 ? (unsigned)c->nl : (unsigned)R.nsub;
   KL(s, K_CTRL, nsub, kFinThreads, k_finish<OP>, R.lp < 0 ? 0 : R.lp, c->T, c->S, C, m, inner_tol);
 }
 
@@ -1443,7 +1443,7 @@ ras_status enq_pcg(ras_ctx* c, cudaStream_t s, const Range& R, Ctl C, int m, dou
   }
   if (c->small) return enq_small_pcg(c, s, R, C, m, inner_tol);
   if (c->path == RAS_PCG_RESIDENT && (R.lp < 0 || c->resid_seq))
-    return enq_resident_pcg(c, s, C, m, inner_tol, R.lp < 0 ? 0 : R.lp, R.lp < 0 ? c->nl : 1);
+    return enq_resident_pcg(c, s, C, m, inner_tol, R.lp < 0 ? 0 : R.lp, R.lp < 0 ? c->nl : R.nsub);
   if (c->ic) {  // PCG start: z = M^-1 r, p = z, rho = r.z
     TRY(enq_precond(c, s, R, C, c->d_r, c->d_z));
     KL(s, K_ZDOT, g, kNT_STREAM, k_zdot<true>, tb, tiles_next(c), (const double*)c->d_r, (const double*)c->d_z, c->d_p, c->S, C);

@@ -215,10 +215,12 @@ def test_block_path_with_d_in_l2():
     s.close()
 
 
-def test_async_sequential_schedule_on_resident_subdomains():
-    # R34: RESIDENT-sized subdomains in async mode on one GPU run one after
-    # another on one stream (a legal asynchronous, multiplicative-ordered
-    # schedule): converges, verifies, and needs fewer updates than sync sweeps
+@pytest.mark.parametrize("pairs", ["0", "1"])
+def test_async_sequential_schedule_on_resident_subdomains(pairs, monkeypatch):
+    # R34: RESIDENT-sized subdomains in async mode on one GPU run on one stream,
+    # one after another (RAS_ASYNC_PAIRS=0) or two at a time (default) -- legal
+    # asynchronous schedules: converge, verify, and need fewer updates than sync sweeps
+    monkeypatch.setenv("RAS_ASYNC_PAIRS", pairs)
     nx, ny = 262, 250
     A = ri.laplace_2d(nx, ny)
     b = ri.rhs(nx * ny, 2)
@@ -230,4 +232,24 @@ def test_async_sequential_schedule_on_resident_subdomains():
     stt = s.stats()
     assert st == 0 and O.verify_global(A, x, b, 1e-8)[0], stt
     assert stt["updates_max"] < sync_sweeps, (stt["updates_max"], sync_sweeps)
+    s.close()
+
+
+def test_async_paired_resident_updates_match_oracle_schedule(monkeypatch):
+    # R34 (default): RESIDENT-sized subdomains updated two at a time, both reading
+    # the latest data -- the asynchronous schedule [[0, 1], [2, 3]] per round,
+    # written out by oracle.ras_schedule (P163-176)
+    monkeypatch.delenv("RAS_ASYNC_PAIRS", raising=False)
+    nx, ny, m, K = 262, 250, 12, 3
+    A = ri.laplace_2d(nx, ny)
+    b = ri.rhs(nx * ny, 2)
+    owner = R.partition_regular(nx, ny, 1, 2, 2, 1)
+    subs = O.setup(A, b, owner, 4)
+    for sd in subs:
+        O.make_local_solver(sd, "jacobi", m)
+    ref = O.ras_schedule(A, b, subs, [[0, 1], [2, 3]] * K)
+    s = R.Solver(A, b, owner, 4, R.options("jacobi", m, max_resumes=0))
+    st, x = s.solve(1e-300, K, "async")
+    assert s.stats()["pcg_path"] == 3, s.stats()["pcg_path"]
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-10, np.linalg.norm(x - ref) / np.linalg.norm(ref)
     s.close()
