@@ -93,7 +93,8 @@ typedef enum { RAS_DET_CENTRAL = 0, RAS_DET_DECENTRAL = 1 } ras_detector;
  *            local solve with p, r, d in shared memory and q in registers
  *            (a chunk of <= kResidMaxRPT * 768 rows per CTA of its group).  Sync
  *            solves run every local subdomain in one launch; async solves issue
- *            one launch per subdomain update, one after another (R34)
+ *            one launch per two consecutive subdomains' updates (its two lanes),
+ *            one pair after another (R34; RAS_ASYNC_PAIRS=0: singly)
  *   AUTO     BLOCK if it applies, else RESIDENT if it applies, else TILED */
 typedef enum { RAS_PCG_AUTO = 0, RAS_PCG_TILED = 1, RAS_PCG_BLOCK = 2, RAS_PCG_RESIDENT = 3 } ras_pcg_path;
 

@@ -144,7 +144,7 @@ def test_loopback_async_puts_and_boards(detector, persistent):
 
 
 def test_loopback_async_resident_sequential():
-    # R34 across virtual ranks: RESIDENT-sized subdomains, per-rank sequential on-chip
+    # R34 across virtual ranks: RESIDENT-sized subdomains, per-rank paired on-chip
     # updates with puts into the peer's halo storage
     nx, ny = 262, 250
     cfg = dict(nx=nx, ny=ny, P=4, gamma=4, solver="jacobi", m=12, converge="async",
@@ -156,7 +156,7 @@ def test_loopback_async_resident_sequential():
         st, x, stats = res[r][("conv", "async")]
         assert st == 0, stats
         assert O.verify_global(A, x, b, 1e-8)[0]
-        assert stats["pcg_path"] == 3  # the sequential on-chip schedule ran
+        assert stats["pcg_path"] == 3  # the on-chip (R34) schedule ran
         assert stats["fresh_halo_reads"] > 0
 
 

@@ -145,7 +145,7 @@ def test_multi_gpu_sync_converges():
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
 def test_multi_gpu_async_resident_sequential():
-    # R34 on 2 GPUs: RESIDENT-sized subdomains, per-rank sequential updates with
+    # R34 on 2 GPUs: RESIDENT-sized subdomains, per-rank paired updates with
     # NVLink puts to the peer; converges and verifies
     nx, ny = 262, 250
     cfg = dict(nx=nx, ny=ny, P=4, gamma=4, solver="jacobi", m=12, converge="async",
@@ -157,7 +157,7 @@ def test_multi_gpu_async_resident_sequential():
         st, x, stats = res[r][("conv", "async")]
         assert st == 0, stats
         assert O.verify_global(A, x, b, 1e-8)[0]
-        assert stats["pcg_path"] == 3  # RESIDENT: the sequential on-chip schedule ran (R34)
+        assert stats["pcg_path"] == 3  # RESIDENT: the on-chip schedule ran (R34)
 
 
 def _stress_worker(rank, world, nccl_id, q):
